@@ -1,0 +1,194 @@
+/*
+ * sdv2.h — C ABI of the B200-native StreamDiffusionV2 stream-batched causal-DiT hot path.
+ *
+ * Citations: "P:n" = line n of the paper's LaTeX (PAPER.md, arXiv 2511.07399);
+ * SURVEY.md §8 is the scope contract and DESIGN.md lists every reading taken where
+ * the paper is silent.
+ *
+ * The library denoises a live stream of latent chunks (inputs reformulated as
+ * B x T' x H x W with small T') with n = B in-flight (chunk, step) entries per pass
+ * (Stream Batch, P:164 / P:227: "treating the n denoising steps as an effective batch
+ * multiplier").  Each pass ("stage-tick") runs, for every entry, the causal DiT blocks
+ * of this rank: adaLN-modulated norm, QKV/out/FFN projections, 3D RoPE with reset
+ * temporal offsets, attention over the entry's [sink || rolling window] KV
+ * lane, prompt cross-attention, the ring-buffer cache update and,
+ * on the first rank, the motion-aware noise blend.  DiT blocks may be
+ * split across ranks (pipeline parallel); the hand-off buffers are
+ * exposed so the caller's transport (torch.distributed / NCCL) moves them.
+ *
+ * Conventions
+ *  - Every call returns sdv2_status; nothing throws across the ABI.
+ *  - All device work is enqueued on the stream given to sdv2_create; calls return
+ *    before completion.  A handle is single-owner and not thread-safe.
+ *  - The library never calls cudaMalloc: all device memory is the caller-owned
+ *    workspace (sdv2_workspace_bytes), carved at create.  The small pinned host
+ *    staging area for per-tick descriptors is allocated with cudaHostAlloc.
+ *  - Tensors are row-major, fp32 unless stated.
+ */
+#ifndef SDV2_H
+#define SDV2_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SDV2_OK = 0,
+  SDV2_E_INVALID = -1,     /* bad controller / schedule / prompt argument            */
+  SDV2_E_SHAPE = -2,       /* inconsistent model / geometry shape                     */
+  SDV2_E_STATE = -3,       /* call out of order, or wrong pointer role for this rank  */
+  SDV2_E_WORKSPACE = -4,   /* workspace missing or too small                          */
+  SDV2_E_CUDA = -5,        /* CUDA runtime error (text in sdv2_last_error)            */
+  SDV2_E_UNSUPPORTED = -6  /* shape outside what the kernels are built for            */
+} sdv2_status;
+
+typedef enum { SDV2_FP32 = 0, SDV2_BF16 = 1 } sdv2_precision;
+
+/* Model card (SURVEY.md §8(c) C.1–C.8; Wan2.1-shaped causal DiT).
+ * head_dim = dim / num_heads must be even (RoPE pairs) and is 64 or 128 on the bf16 path. */
+typedef struct {
+  int32_t num_blocks, dim, num_heads, ffn_dim;
+  int32_t latent_channels, patch_t, patch_h, patch_w;  /* patch must be (1,2,2) */
+  int32_t text_len, text_dim, freq_dim;                /* freq_dim = 256 */
+  float eps;                                           /* 1e-6 */
+  int32_t norm_center;                                 /* 0 = RMSNorm, 1 = LayerNorm (affine-free) */
+} sdv2_model_desc;
+
+/* Stream geometry ("B x T' x H x W"; P:190 sink set size m; P:472 rolling window). */
+typedef struct {
+  int32_t latent_h, latent_w;   /* latent frame; divisible by the patch */
+  int32_t chunk_frames;         /* T' latent frames per chunk (<= 16)   */
+  int32_t steps;                /* n = B denoising steps = in-flight entries = KV lanes (<= 8) */
+  int32_t sink_chunks;          /* m >= 0 sink chunks (first chunks, refreshed by P:190) */
+  int32_t window_chunks;        /* W >= 1 rolling-window chunks, current chunk included */
+} sdv2_geometry;
+
+/* Pipeline stage of this handle.  world = K stages; this rank owns DiT
+ * blocks [block_begin, block_end).  NULL desc = single stage owning every block. */
+typedef struct {
+  int32_t world, rank, block_begin, block_end;
+} sdv2_pipeline_desc;
+
+/* Weights: fp32 values that are bf16-representable, nn.Linear
+ * layout [out, in], host or device pointers (copied with cudaMemcpyDefault and packed
+ * into the workspace during sdv2_create; the caller may free them afterwards).
+ * Order: the 15 global tensors
+ *   patch_w[d,4C] patch_b[d] txt1_w[d,Dt] txt1_b[d] txt2_w[d,d] txt2_b[d]
+ *   t1_w[d,256] t1_b[d] t2_w[d,d] t2_b[d] tp_w[6d,d] tp_b[6d] head_mod[2,d] head_w[4C,d] head_b[4C]
+ * then, for each block b in [block_begin, block_end), the 27 block tensors
+ *   mod[6,d] wq bq wk bk wv bv wo bo gq gk n3_g n3_b wcq bcq wck bck wcv bcv wco bco gcq gck
+ *   w1[F,d] b1[F] w2[d,F] b2[d]            ([d,d] / [d] unless stated)            */
+typedef struct {
+  const void* const* tensors;
+  int32_t count;
+} sdv2_weights;
+
+/* Per-stream controls (P:190 tau; P:191 T_reset; P:210–219 k, sigma, s_min, s_max, lambda).
+ * timesteps: host array of `steps` strictly decreasing values, t_0 in (0, 1000]; the
+ * noise level of step j of chunk X is sigma = s_X * t_j / t_0 (reading R5).
+ * seed keys the Philox4x32-10 noise (counter layout in DESIGN.md). */
+typedef struct {
+  const float* timesteps;
+  int32_t num_timesteps;
+  int32_t rope_reset_frames;    /* T_reset >= max(m, W) * T', T_reset + T' <= 4096 */
+  int32_t motion_k;             /* window of k+1 motion values, 0 <= k < 64 */
+  float motion_sigma;           /* > 0 */
+  float s_min, s_max;           /* 0 <= s_min < s_max <= 1 */
+  float ema_lambda;             /* in (0, 1] */
+  float sink_tau;               /* in [-1, 1] */
+  uint64_t seed;
+} sdv2_stream_desc;
+
+/* Stage hand-off buffers (device pointers inside the workspace), "transmits the
+ * results to the next stage within a ring structure".  For call index c on this rank
+ * the library reads act_in/ring_in of parity c%2 and writes act_out/ring_out of parity
+ * c%2.  Rank s>0 must receive, before its call c, the act packet rank s-1 produced at
+ * its call c; rank 0 (world > 1) must receive, before its call c >= K, the ring packet
+ * the last rank produced at its call c-K.  K = 1 needs no transport. */
+typedef struct {
+  void* act_in;  void* act_out;  size_t act_bytes;
+  void* ring_in; void* ring_out; size_t ring_bytes;
+} sdv2_stage_io;
+
+/* Per-call schedule introspection (host-only; deterministic R2 schedule). */
+typedef struct {
+  int64_t call;                  /* call index on this rank                         */
+  int32_t num_entries;           /* active entries this call (prefix j = 0..n-1)    */
+  int32_t steps;
+  int64_t chunk[8];              /* chunk X of entry j (-1 if inactive)             */
+  int64_t out_chunk;             /* chunk whose clean latent this call emits, or -1 */
+} sdv2_tick_info;
+
+/* Cache metadata of one (local block, lane) after the last call (test introspection). */
+typedef struct {
+  int32_t num_slots;             /* m + W                                            */
+  int32_t num_valid;             /* valid slots (always a prefix)                    */
+  int64_t tag[64];               /* chunk held by slot s, -1 = empty                 */
+  int32_t pos[64];               /* temporal position of the slot's first frame      */
+  int32_t resets;                /* r                                                */
+  int64_t evictions;
+  double noise_rate;             /* s of the last admitted chunk (rank 0)            */
+  double d_hat;                  /* d_hat of the last admitted chunk (rank 0)        */
+} sdv2_cache_state;
+
+typedef struct sdv2_handle sdv2_handle;
+
+/* Bytes of device workspace a handle needs (0 on invalid descriptors). */
+size_t sdv2_workspace_bytes(const sdv2_model_desc* md, const sdv2_geometry* g,
+                            const sdv2_pipeline_desc* pp, sdv2_precision prec);
+
+/* Validate, carve the workspace, pack this rank's weights (fp32 -> bf16 K-major for
+ * SDV2_BF16), build TMA descriptors.  `stream` is a cudaStream_t (NULL = legacy). */
+sdv2_status sdv2_create(const sdv2_model_desc* md, const sdv2_geometry* g,
+                        const sdv2_pipeline_desc* pp, sdv2_precision prec,
+                        const sdv2_weights* w, void* workspace, size_t workspace_bytes,
+                        int device, void* stream, sdv2_handle** out);
+
+/* Start a new stream: zero KV lanes, metadata and controller state; embed the prompt
+ * (host [text_len, text_dim] fp32) and compute every local block's cross K/V. */
+sdv2_status sdv2_reset_stream(sdv2_handle* h, const sdv2_stream_desc* sd, const float* prompt_host);
+
+/* Switch prompt: takes effect from the next chunk admitted (the next call); in-flight
+ * entries keep the prompt they were admitted with (two prompt versions resident). */
+sdv2_status sdv2_set_prompt(sdv2_handle* h, const float* prompt_host);
+
+/* One stage-tick.  Rank 0: chunk_latent [C, T', h, w] fp32 (host or device pointer)
+ * is admitted as chunk X = call index.  Last rank: if this call emits a clean chunk,
+ * its x0 is written to out_latent (host or device, [C, T', h, w] fp32) and
+ * *out_chunk_index = its chunk index, else *out_chunk_index = -1 (known without a
+ * device sync: the schedule is deterministic).  Other ranks pass NULL. */
+sdv2_status sdv2_denoise_chunk(sdv2_handle* h, const float* chunk_latent, float* out_latent,
+                               int64_t* out_chunk_index);
+
+sdv2_status sdv2_stage_io_buffers(sdv2_handle* h, int32_t parity, sdv2_stage_io* io);
+sdv2_status sdv2_get_tick_info(const sdv2_handle* h, sdv2_tick_info* info);
+sdv2_status sdv2_destroy(sdv2_handle* h);
+const char* sdv2_status_string(sdv2_status s);
+const char* sdv2_last_error(const sdv2_handle* h);
+
+/* ---- test-only introspection (not on the timed path) ---- */
+/* Metadata of (local block, lane); also copies the controller state (s, d_hat). */
+sdv2_status sdv2_get_cache_state(sdv2_handle* h, int32_t local_block, int32_t lane, sdv2_cache_state* out);
+/* If per_block_out != NULL (device, [local_blocks, n*L, dim] fp32) every following
+ * call copies the residual stream x after each local block into it. */
+sdv2_status sdv2_set_block_tap(sdv2_handle* h, float* per_block_out);
+/* Device pointer + element count of the K (which=0) or V (which=1) storage of
+ * (local block, lane): [m+W slots][L tokens][dim], element type = precision. */
+sdv2_status sdv2_kv_lane(sdv2_handle* h, int32_t local_block, int32_t lane, int32_t which,
+                         void** ptr, size_t* elems);
+
+/* ---- host control plane (no GPU needed; also exported by libsdv2_ctl.so) ---- */
+/* Exact min-max contiguous partition of per-block costs over K stages, with extra
+ * cost on the first / last stage (P:231–233 DiT block scheduler).  Ties: earlier
+ * stages take as many blocks as the optimum allows.  bounds_out has K+1 entries. */
+sdv2_status sdv2_partition(const double* block_costs, int32_t num_blocks, int32_t stages,
+                           double extra_first, double extra_last, int32_t* bounds_out,
+                           double* max_stage_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SDV2_H */

@@ -1,0 +1,821 @@
+// libsdv2: C-ABI implementation (include/sdv2.h) — workspace carving, weight
+// packing, prompt conditioning and the per-call stage-tick orchestration.
+//
+// One call = one stage-tick (reading R2 in DESIGN.md): this rank runs every active
+// (chunk, step) entry of micro-batch `call` through its DiT blocks, all entries
+// batched into the same GEMMs (Stream Batch, P:164 / P:227).  Rank 0 additionally
+// runs the motion-aware noise controller, patch embedding and time
+// conditioning; the last rank runs the head, x0 prediction and re-noising.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/sdv2.h"
+#include "attn_tc.cuh"
+#include "ctl.h"
+#include "gemm_tc.cuh"
+#include "kernels.cuh"
+
+using namespace sdv2;
+
+namespace {
+
+constexpr int kNumGlobal = 15;
+constexpr int kNumBlockT = 27;
+constexpr int kTdRing = 16;
+constexpr int kMaxTOff = 4096 + 16;
+
+enum GlobalT { G_PATCH_W, G_PATCH_B, G_TXT1_W, G_TXT1_B, G_TXT2_W, G_TXT2_B, G_T1_W, G_T1_B, G_T2_W, G_T2_B,
+               G_TP_W, G_TP_B, G_HEAD_MOD, G_HEAD_W, G_HEAD_B };
+enum BlockT { B_MOD, B_WQ, B_BQ, B_WK, B_BK, B_WV, B_BV, B_WO, B_BO, B_GQ, B_GK, B_N3G, B_N3B, B_WCQ, B_BCQ,
+              B_WCK, B_BCK, B_WCV, B_BCV, B_WCO, B_BCO, B_GCQ, B_GCK, B_W1, B_B1, B_W2, B_B2 };
+
+struct Carver {
+  char* base;
+  size_t off = 0;
+  // sizing mode (b == nullptr) carves from a dummy base; the pointers are never used
+  explicit Carver(void* b) : base(b ? static_cast<char*>(b) : reinterpret_cast<char*>(uintptr_t(1) << 20)) {}
+  template <typename T>
+  T* take(size_t count) {
+    off = (off + 1023) & ~size_t(1023);
+    T* p = reinterpret_cast<T*>(base + off);
+    off += count * sizeof(T);
+    return p;
+  }
+};
+
+// Per-block packed weights (TW = float or bf16 for the matrices; vectors fp32).
+struct BlockW {
+  float* mod;                 // [6, d]
+  void* wqkv; float* bqkv;    // [3d, d], [3d]
+  void* wo; float* bo;
+  float *gq, *gk, *n3g, *n3b;
+  void* wcq; float* bcq;
+  void* wck; float* bck;
+  void* wcv; float* bcv;
+  void* wco; float* bco;
+  float *gcq, *gck;
+  void* w1; float* b1;        // [F, d]
+  void* w2; float* b2;        // [d, F]
+};
+
+// Tick packet: the residual stream and everything a downstream stage needs.
+struct Packet {
+  float* x;     // [n L, d]
+  float* e0;    // [n, 6d]
+  float* e;     // [n, d]
+  float* sig;   // [n]
+  float* sign;  // [n]
+  float* lat;   // [n, CTHW]
+  size_t bytes;
+};
+
+}  // namespace
+
+struct sdv2_handle {
+  sdv2_model_desc md;
+  sdv2_geometry g;
+  sdv2_precision prec;
+  int K = 1, rank = 0, b0 = 0, b1 = 0, nb = 0;
+  int d, H, hd, F, C, T, hh, ww, L, n, m, W, S, Lt, Dt, CTHW, Mmax, P;
+  int hn, wn, ct, ch, cw;
+  size_t ta;  // bytes per activation element
+  cudaStream_t stream = nullptr;
+  int device = 0;
+
+  // workspace
+  float* gw[kNumGlobal];      // global weights (fp32 except tp_w which is TW)
+  void* tp_w;
+  std::vector<BlockW> bw;
+  char* packet_base;          // tick state (packet layout)
+  Packet st;
+  char* act_io[2][2];         // [in/out][parity]
+  float* ring[2][2];          // [in/out][parity] ring-closure latents [n-1, CTHW]
+  float* lat_in;              // staged caller chunk [CTHW]
+  float* prev_frame;          // [C h w]
+  float* out_stage;           // [CTHW]
+  CtrlState* ctrl;
+  float* emb;                 // [n, 256]
+  float* t1;                  // [n, d]
+  void* a;                    // [Mmax, d] TA
+  void* qkv;                  // [Mmax, 3d] TA
+  void* q;                    // [Mmax, d] TA
+  void* o;                    // [Mmax, d] TA
+  void* hbuf;                 // [Mmax, F] TA
+  float* staging;             // weight staging (aliases the activation scratch)
+  size_t staging_elems;
+  void* Kc; void* Vc;         // KV lanes [nb][n][S][L][d] TA
+  void* Kx; void* Vx;         // prompt K/V [2][nb][Lt][d] TA
+  float* prompt;              // [Lt, Dt]
+  float* ctx;                 // [Lt, d]
+  float* ctx_tmp;             // [Lt, d]
+  float* rope;                // tables
+  RopeTabs rt;
+  TickDesc* td_dev;
+  TickDesc* td_host = nullptr;   // pinned ring
+  cudaEvent_t td_ev[kTdRing];
+  bool td_ev_used[kTdRing];
+  size_t ws_bytes;
+
+  // state
+  Control ctl;
+  bool stream_ready = false;
+  StreamCfg scfg;
+  int T_reset = 1;
+  int pver = 0;
+  float* tap = nullptr;
+  sdv2_tick_info info;
+  std::string err;
+  TmaGemmPlan gplan;
+};
+
+namespace {
+
+size_t carve(sdv2_handle* h, void* base) {
+  Carver cv(base);
+  const size_t TWb = h->prec == SDV2_BF16 ? 2 : 4;
+  const int d = h->d, F = h->F, P = h->P;
+  auto tw = [&](size_t cnt) -> void* { return cv.take<char>(cnt * TWb); };
+  h->gw[G_PATCH_W] = cv.take<float>(size_t(d) * P);
+  h->gw[G_PATCH_B] = cv.take<float>(d);
+  h->gw[G_TXT1_W] = cv.take<float>(size_t(d) * h->Dt);
+  h->gw[G_TXT1_B] = cv.take<float>(d);
+  h->gw[G_TXT2_W] = cv.take<float>(size_t(d) * d);
+  h->gw[G_TXT2_B] = cv.take<float>(d);
+  h->gw[G_T1_W] = cv.take<float>(size_t(d) * h->md.freq_dim);
+  h->gw[G_T1_B] = cv.take<float>(d);
+  h->gw[G_T2_W] = cv.take<float>(size_t(d) * d);
+  h->gw[G_T2_B] = cv.take<float>(d);
+  h->gw[G_TP_W] = nullptr;
+  h->tp_w = tw(size_t(6) * d * d);
+  h->gw[G_TP_B] = cv.take<float>(6 * d);
+  h->gw[G_HEAD_MOD] = cv.take<float>(2 * d);
+  h->gw[G_HEAD_W] = cv.take<float>(size_t(P) * d);
+  h->gw[G_HEAD_B] = cv.take<float>(P);
+  h->bw.assign(h->nb, BlockW{});
+  for (int b = 0; b < h->nb; ++b) {
+    BlockW& B = h->bw[b];
+    B.mod = cv.take<float>(6 * d);
+    B.wqkv = tw(size_t(3) * d * d); B.bqkv = cv.take<float>(3 * d);
+    B.wo = tw(size_t(d) * d); B.bo = cv.take<float>(d);
+    B.gq = cv.take<float>(d); B.gk = cv.take<float>(d);
+    B.n3g = cv.take<float>(d); B.n3b = cv.take<float>(d);
+    B.wcq = tw(size_t(d) * d); B.bcq = cv.take<float>(d);
+    B.wck = tw(size_t(d) * d); B.bck = cv.take<float>(d);
+    B.wcv = tw(size_t(d) * d); B.bcv = cv.take<float>(d);
+    B.wco = tw(size_t(d) * d); B.bco = cv.take<float>(d);
+    B.gcq = cv.take<float>(d); B.gck = cv.take<float>(d);
+    B.w1 = tw(size_t(F) * d); B.b1 = cv.take<float>(F);
+    B.w2 = tw(size_t(d) * F); B.b2 = cv.take<float>(d);
+  }
+  // packet (tick state) — contiguous so it can be shipped as one message
+  {
+    const size_t x = size_t(h->Mmax) * d, e0 = size_t(h->n) * 6 * d, e = size_t(h->n) * d, lat = size_t(h->n) * h->CTHW;
+    const size_t sz = (x + e0 + e + 2 * 64 + lat) * 4;
+    h->st.bytes = sz;
+    h->packet_base = cv.take<char>(sz);
+    float* p = reinterpret_cast<float*>(h->packet_base);
+    h->st.x = p; p += x;
+    h->st.e0 = p; p += e0;
+    h->st.e = p; p += e;
+    h->st.sig = p; p += 64;
+    h->st.sign = p; p += 64;
+    h->st.lat = p;
+    for (int io = 0; io < 2; ++io)
+      for (int par = 0; par < 2; ++par) h->act_io[io][par] = h->K > 1 ? cv.take<char>(sz) : nullptr;
+  }
+  const size_t ring_elems = size_t(h->n > 1 ? h->n - 1 : 1) * h->CTHW;
+  for (int io = 0; io < 2; ++io)
+    for (int par = 0; par < 2; ++par) h->ring[io][par] = cv.take<float>(ring_elems);
+  h->lat_in = cv.take<float>(h->CTHW);
+  h->prev_frame = cv.take<float>(size_t(h->C) * h->hh * h->ww);
+  h->out_stage = cv.take<float>(h->CTHW);
+  h->ctrl = cv.take<CtrlState>(1);
+  h->emb = cv.take<float>(size_t(h->n) * h->md.freq_dim);
+  h->t1 = cv.take<float>(size_t(h->n) * d);
+  // activation scratch, aliased by the weight staging buffer during create
+  {
+    const size_t act = (size_t(h->Mmax) * d * 3 + size_t(h->Mmax) * 3 * d + size_t(h->Mmax) * F) * h->ta + 5 * 1024;
+    size_t maxw = size_t(F) * d;
+    maxw = std::max(maxw, size_t(6) * d * d);
+    maxw = std::max(maxw, size_t(d) * h->Dt);
+    const size_t stag = maxw * 4;
+    const size_t sz = std::max(act, stag);
+    char* s = cv.take<char>(sz);
+    h->staging = reinterpret_cast<float*>(s);
+    h->staging_elems = maxw;
+    Carver sub(s);
+    h->a = sub.take<char>(size_t(h->Mmax) * d * h->ta);
+    h->qkv = sub.take<char>(size_t(h->Mmax) * 3 * d * h->ta);
+    h->q = sub.take<char>(size_t(h->Mmax) * d * h->ta);
+    h->o = sub.take<char>(size_t(h->Mmax) * d * h->ta);
+    h->hbuf = sub.take<char>(size_t(h->Mmax) * F * h->ta);
+  }
+  const size_t kv = size_t(h->nb) * h->n * h->S * h->L * d;
+  h->Kc = cv.take<char>(kv * h->ta);
+  h->Vc = cv.take<char>(kv * h->ta);
+  const size_t px = size_t(2) * h->nb * h->Lt * d;
+  h->Kx = cv.take<char>(px * h->ta);
+  h->Vx = cv.take<char>(px * h->ta);
+  h->prompt = cv.take<float>(size_t(h->Lt) * h->Dt);
+  h->ctx = cv.take<float>(size_t(h->Lt) * d);
+  h->ctx_tmp = cv.take<float>(size_t(h->Lt) * d);
+  const size_t rope_elems = size_t(2 * kMaxTOff + 1) * h->ct * 2 + size_t(h->hn) * h->ch * 2 + size_t(h->wn) * h->cw * 2;
+  h->rope = cv.take<float>(rope_elems);
+  h->td_dev = cv.take<TickDesc>(1);
+  return cv.off + 1024;
+}
+
+sdv2_status fill_dims(sdv2_handle* h, const sdv2_model_desc* md, const sdv2_geometry* g,
+                      const sdv2_pipeline_desc* pp, sdv2_precision prec, std::string* why) {
+  if (!md || !g) return SDV2_E_INVALID;
+  h->md = *md;
+  h->g = *g;
+  h->prec = prec;
+  if (prec != SDV2_FP32 && prec != SDV2_BF16) return SDV2_E_INVALID;
+  if (md->num_blocks < 1 || md->dim < 1 || md->num_heads < 1 || md->ffn_dim < 1) return SDV2_E_SHAPE;
+  if (md->dim % md->num_heads) { *why = "dim % num_heads != 0"; return SDV2_E_SHAPE; }
+  h->d = md->dim; h->H = md->num_heads; h->hd = md->dim / md->num_heads; h->F = md->ffn_dim;
+  if (h->hd % 2) { *why = "odd head_dim"; return SDV2_E_SHAPE; }
+  if (h->hd != 64 && h->hd != 128) { *why = "head_dim must be 64 or 128"; return SDV2_E_UNSUPPORTED; }
+  if (h->d % 128 || h->F % 64) { *why = "dim % 128 or ffn % 64"; return SDV2_E_UNSUPPORTED; }
+  if (md->patch_t != 1 || md->patch_h != 2 || md->patch_w != 2) { *why = "patch must be (1,2,2)"; return SDV2_E_UNSUPPORTED; }
+  if (md->freq_dim != 256 || md->text_len < 1 || md->text_dim < 1) return SDV2_E_SHAPE;
+  if (g->latent_h % 2 || g->latent_w % 2 || g->latent_h < 2 || g->latent_w < 2) { *why = "latent not divisible by patch"; return SDV2_E_SHAPE; }
+  if (g->window_chunks < 1 || g->sink_chunks < 0) { *why = "window_chunks < 1"; return SDV2_E_SHAPE; }
+  if (g->chunk_frames < 1 || g->chunk_frames > kMaxFrames) return SDV2_E_SHAPE;
+  if (g->steps < 1 || g->steps > kMaxSteps) return SDV2_E_SHAPE;
+  if (g->sink_chunks + g->window_chunks > kMaxSlots || g->sink_chunks > 31) return SDV2_E_SHAPE;
+  h->C = md->latent_channels; h->T = g->chunk_frames; h->hh = g->latent_h; h->ww = g->latent_w;
+  h->hn = h->hh / 2; h->wn = h->ww / 2;
+  h->L = h->T * h->hn * h->wn;
+  h->n = g->steps; h->m = g->sink_chunks; h->W = g->window_chunks; h->S = h->m + h->W;
+  h->Lt = md->text_len; h->Dt = md->text_dim;
+  h->CTHW = h->C * h->T * h->hh * h->ww;
+  if (h->CTHW % 4) return SDV2_E_SHAPE;
+  h->Mmax = h->n * h->L;
+  h->P = 4 * h->C;
+  const int c = h->hd / 2;
+  h->ct = c - 2 * (c / 3); h->ch = c / 3; h->cw = c / 3;
+  h->ta = prec == SDV2_BF16 ? 2 : 4;
+  if (pp) {
+    if (pp->world < 1 || pp->rank < 0 || pp->rank >= pp->world) return SDV2_E_INVALID;
+    if (pp->world > md->num_blocks) { *why = "more stages than blocks"; return SDV2_E_INVALID; }
+    if (pp->block_begin < 0 || pp->block_end > md->num_blocks || pp->block_begin >= pp->block_end) {
+      *why = "bad block range";
+      return SDV2_E_INVALID;
+    }
+    h->K = pp->world; h->rank = pp->rank; h->b0 = pp->block_begin; h->b1 = pp->block_end;
+  } else {
+    h->K = 1; h->rank = 0; h->b0 = 0; h->b1 = md->num_blocks;
+  }
+  h->nb = h->b1 - h->b0;
+  return SDV2_OK;
+}
+
+#define CK(call)                                                              \
+  do {                                                                        \
+    cudaError_t e_ = (call);                                                  \
+    if (e_ != cudaSuccess) {                                                  \
+      h->err = std::string(#call) + ": " + cudaGetErrorString(e_);            \
+      return SDV2_E_CUDA;                                                     \
+    }                                                                         \
+  } while (0)
+
+#define CKL()                                                                 \
+  do {                                                                        \
+    cudaError_t e_ = cudaGetLastError();                                      \
+    if (e_ != cudaSuccess) {                                                  \
+      h->err = std::string("launch: ") + cudaGetErrorString(e_);              \
+      return SDV2_E_CUDA;                                                     \
+    }                                                                         \
+  } while (0)
+
+template <typename T>
+__global__ void convert_kernel(const float* __restrict__ src, T* __restrict__ dst, size_t n) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+    dst[i] = from_f<T>(src[i]);
+}
+
+sdv2_status load_tensor(sdv2_handle* h, const void* src, void* dst, size_t elems, bool to_tw) {
+  if (!src) {
+    h->err = "null weight tensor";
+    return SDV2_E_INVALID;
+  }
+  if (!to_tw || h->prec == SDV2_FP32) {
+    CK(cudaMemcpyAsync(dst, src, elems * 4, cudaMemcpyDefault, h->stream));
+    return SDV2_OK;
+  }
+  CK(cudaMemcpyAsync(h->staging, src, elems * 4, cudaMemcpyDefault, h->stream));
+  convert_kernel<bf16><<<592, 256, 0, h->stream>>>(h->staging, static_cast<bf16*>(dst), elems);
+  CKL();
+  return SDV2_OK;
+}
+
+// ---------------------------------------------------------------- GEMM dispatch
+template <typename TIn, typename TW, typename TOut>
+sdv2_status gemm_simt(sdv2_handle* h, const TIn* A, const TW* W, int M, int N, int K, int lda, int epi,
+                      const EpiArgs& ep) {
+  dim3 grid((N + 63) / 64, (M + 63) / 64);
+  switch (epi) {
+    case EPI_STORE: gemm_simt_kernel<TIn, TW, TOut, EPI_STORE><<<grid, 256, 0, h->stream>>>(A, W, M, N, K, lda, K, ep); break;
+    case EPI_GELU: gemm_simt_kernel<TIn, TW, TOut, EPI_GELU><<<grid, 256, 0, h->stream>>>(A, W, M, N, K, lda, K, ep); break;
+    case EPI_RES_GATE: gemm_simt_kernel<TIn, TW, TOut, EPI_RES_GATE><<<grid, 256, 0, h->stream>>>(A, W, M, N, K, lda, K, ep); break;
+    default: gemm_simt_kernel<TIn, TW, TOut, EPI_RES><<<grid, 256, 0, h->stream>>>(A, W, M, N, K, lda, K, ep); break;
+  }
+  CKL();
+  return SDV2_OK;
+}
+
+// Activation GEMM of the hot path: fp32 SIMT on the parity path, tcgen05 on bf16.
+sdv2_status gemm_act(sdv2_handle* h, const void* A, const void* W, int M, int N, int K, int epi, const EpiArgs& ep) {
+  if (h->prec == SDV2_FP32)
+    return gemm_simt<float, float, float>(h, static_cast<const float*>(A), static_cast<const float*>(W), M, N, K, K,
+                                          epi, ep);
+  if (tc_gemm_enabled())
+    return tc_gemm(h->stream, h->gplan, A, W, M, N, K, epi, ep, &h->err) ? SDV2_OK : SDV2_E_CUDA;
+  return gemm_simt<bf16, bf16, bf16>(h, static_cast<const bf16*>(A), static_cast<const bf16*>(W), M, N, K, K, epi, ep);
+}
+
+sdv2_status attention(sdv2_handle* h, const AttnArgs& aa, int Mrows_entries) {
+  dim3 grid((h->L + 15) / 16, h->H, Mrows_entries);
+  if (h->prec == SDV2_FP32) {
+    if (h->hd == 64) attn_simt_kernel<float, 64><<<grid, 128, 0, h->stream>>>(aa, h->td_dev);
+    else attn_simt_kernel<float, 128><<<grid, 128, 0, h->stream>>>(aa, h->td_dev);
+  } else {
+    if (tc_attn_enabled()) return tc_attention(h->stream, aa, h->td_dev, h->hd, h->H, Mrows_entries, &h->err) ? SDV2_OK : SDV2_E_CUDA;
+    if (h->hd == 64) attn_simt_kernel<bf16, 64><<<grid, 128, 0, h->stream>>>(aa, h->td_dev);
+    else attn_simt_kernel<bf16, 128><<<grid, 128, 0, h->stream>>>(aa, h->td_dev);
+  }
+  CKL();
+  return SDV2_OK;
+}
+
+template <typename TA>
+sdv2_status launch_norm(sdv2_handle* h, int rows, int mode, const float* mod, int sc_row, int sh_row,
+                        const float* gamma, const float* beta) {
+  norm_mod_kernel<TA><<<(rows + 7) / 8, 256, 0, h->stream>>>(h->st.x, static_cast<TA*>(h->a), rows, h->d, h->L, mode,
+                                                             mod, h->st.e0, sc_row, sh_row, gamma, beta, h->md.eps,
+                                                             h->md.norm_center);
+  CKL();
+  return SDV2_OK;
+}
+
+#define TRY(x)                        \
+  do {                                \
+    sdv2_status s_ = (x);             \
+    if (s_ != SDV2_OK) return s_;     \
+  } while (0)
+
+template <typename TA>
+sdv2_status run_block(sdv2_handle* h, int bl, int rows, int n_act) {
+  const BlockW& B = h->bw[bl];
+  const int d = h->d;
+  EpiArgs ep{};
+  ep.L = h->L;
+  // 1. adaLN norm1 + modulate (shift row 0, scale row 1)
+  TRY(launch_norm<TA>(h, rows, 0, B.mod, 1, 0, nullptr, nullptr));
+  // 2. QKV projection
+  ep.out = h->qkv; ep.ldo = 3 * d; ep.bias = B.bqkv;
+  TRY(gemm_act(h, h->a, B.wqkv, rows, 3 * d, d, EPI_STORE, ep));
+  // 3–4. q/k RMSNorm + RoPE + KV lane write
+  const size_t lane_elems = size_t(h->n) * h->S * h->L * d;
+  TA* Kb = static_cast<TA*>(h->Kc) + bl * lane_elems;
+  TA* Vb = static_cast<TA*>(h->Vc) + bl * lane_elems;
+  qkv_post_kernel<TA><<<(rows + 7) / 8, 256, 0, h->stream>>>(static_cast<const TA*>(h->qkv), static_cast<TA*>(h->q), Kb,
+                                                             Vb, B.gq, B.gk, h->td_dev, h->rt, rows, d, h->hd, h->L,
+                                                             h->hn, h->wn, h->T, h->S, h->md.eps);
+  CKL();
+  // self-attention over the lane's valid prefix
+  AttnArgs aa{};
+  aa.q = h->q; aa.ldq = d; aa.K = Kb; aa.V = Vb; aa.kv_lane_stride = size_t(h->S) * h->L * d; aa.ldk = d;
+  aa.o = h->o; aa.ldo = d; aa.L = h->L; aa.cross = 0; aa.scale = 1.f / sqrtf(float(h->hd));
+  TRY(attention(h, aa, n_act));
+  // 5. out projection + gated residual (g1 = row 2)
+  ep.out = h->st.x; ep.ldo = d; ep.bias = B.bo; ep.mod = B.mod; ep.e0 = h->st.e0; ep.gate_row = 2;
+  TRY(gemm_act(h, h->o, B.wo, rows, d, d, EPI_RES_GATE, ep));
+  // 6. cross-attention: affine norm3, q projection, RMS q
+  TRY(launch_norm<TA>(h, rows, 1, nullptr, 0, 0, B.n3g, B.n3b));
+  ep.out = h->q; ep.ldo = d; ep.bias = B.bcq;
+  TRY(gemm_act(h, h->a, B.wcq, rows, d, d, EPI_STORE, ep));
+  rms_rows_kernel<TA, TA><<<(rows + 7) / 8, 256, 0, h->stream>>>(static_cast<TA*>(h->q), static_cast<TA*>(h->q), B.gcq,
+                                                                  rows, d, d, h->md.eps);
+  CKL();
+  const size_t px = size_t(h->Lt) * d;
+  aa.q = h->q; aa.K = static_cast<TA*>(h->Kx) + bl * px; aa.V = static_cast<TA*>(h->Vx) + bl * px;
+  aa.kv_lane_stride = size_t(h->nb) * px; aa.cross = 1; aa.Lk_cross = h->Lt;
+  TRY(attention(h, aa, n_act));
+  // 7. cross out projection, ungated residual
+  ep.out = h->st.x; ep.ldo = d; ep.bias = B.bco;
+  TRY(gemm_act(h, h->o, B.wco, rows, d, d, EPI_RES, ep));
+  // 8. FFN: norm2 + modulate (shift row 3, scale row 4), GELU, gated residual (g2 = row 5)
+  TRY(launch_norm<TA>(h, rows, 0, B.mod, 4, 3, nullptr, nullptr));
+  ep.out = h->hbuf; ep.ldo = h->F; ep.bias = B.b1;
+  TRY(gemm_act(h, h->a, B.w1, rows, h->F, d, EPI_GELU, ep));
+  ep.out = h->st.x; ep.ldo = d; ep.bias = B.b2; ep.mod = B.mod; ep.e0 = h->st.e0; ep.gate_row = 5;
+  TRY(gemm_act(h, h->hbuf, B.w2, rows, d, h->F, EPI_RES_GATE, ep));
+  if (h->tap) CK(cudaMemcpyAsync(h->tap + size_t(bl) * h->Mmax * d, h->st.x, size_t(rows) * d * 4,
+                                 cudaMemcpyDeviceToDevice, h->stream));
+  return SDV2_OK;
+}
+
+// Prompt conditioning (C.3): ctx = W_x2 GELU(W_x1 P + b) + b; per block K_c = RMS(ctx W_ck^T + b),
+// V_c = ctx W_cv^T + b into prompt version slot `ver & 1`.
+template <typename TA>
+sdv2_status embed_prompt(sdv2_handle* h, const float* prompt_host, int ver) {
+  const int d = h->d, Lt = h->Lt;
+  CK(cudaMemcpyAsync(h->prompt, prompt_host, size_t(Lt) * h->Dt * 4, cudaMemcpyHostToDevice, h->stream));
+  EpiArgs ep{};
+  ep.out = h->ctx_tmp; ep.ldo = d; ep.bias = h->gw[G_TXT1_B];
+  TRY((gemm_simt<float, float, float>(h, h->prompt, h->gw[G_TXT1_W], Lt, d, h->Dt, h->Dt, EPI_GELU, ep)));
+  ep.out = h->ctx; ep.bias = h->gw[G_TXT2_B];
+  TRY((gemm_simt<float, float, float>(h, h->ctx_tmp, h->gw[G_TXT2_W], Lt, d, d, d, EPI_STORE, ep)));
+  const size_t px = size_t(Lt) * d;
+  for (int b = 0; b < h->nb; ++b) {
+    const BlockW& B = h->bw[b];
+    TA* Kd = static_cast<TA*>(h->Kx) + (size_t(ver & 1) * h->nb + b) * px;
+    TA* Vd = static_cast<TA*>(h->Vx) + (size_t(ver & 1) * h->nb + b) * px;
+    ep.out = h->ctx_tmp; ep.bias = B.bck;
+    TRY((gemm_simt<float, TA, float>(h, h->ctx, static_cast<const TA*>(B.wck), Lt, d, d, d, EPI_STORE, ep)));
+    rms_rows_kernel<float, TA><<<(Lt + 7) / 8, 256, 0, h->stream>>>(h->ctx_tmp, Kd, B.gck, Lt, d, d, h->md.eps);
+    CKL();
+    ep.out = Vd; ep.bias = B.bcv;
+    TRY((gemm_simt<float, TA, TA>(h, h->ctx, static_cast<const TA*>(B.wcv), Lt, d, d, d, EPI_STORE, ep)));
+  }
+  return SDV2_OK;
+}
+
+sdv2_status set_prompt_common(sdv2_handle* h, const float* prompt_host, int ver) {
+  // h = mean-pooled prompt, fp64 (reading Q8)
+  std::vector<double> mean(h->Dt, 0.0);
+  for (int t = 0; t < h->Lt; ++t)
+    for (int c = 0; c < h->Dt; ++c) mean[c] += double(prompt_host[size_t(t) * h->Dt + c]);
+  double nrm = 0.0;
+  for (int c = 0; c < h->Dt; ++c) {
+    mean[c] /= double(h->Lt);
+    nrm += mean[c] * mean[c];
+  }
+  if (!(nrm > 0.0)) {
+    h->err = "zero-norm prompt mean";
+    return SDV2_E_INVALID;
+  }
+  if (h->prec == SDV2_FP32) TRY(embed_prompt<float>(h, prompt_host, ver));
+  else TRY(embed_prompt<bf16>(h, prompt_host, ver));
+  h->ctl.set_prompt_mean(mean, ver);
+  return SDV2_OK;
+}
+
+template <typename TA>
+sdv2_status tick(sdv2_handle* h, const float* chunk_latent, float* out_latent, int64_t* out_chunk) {
+  const int64_t call = h->ctl.calls();
+  const int slot = int(call % kTdRing);
+  if (h->td_ev_used[slot]) CK(cudaEventSynchronize(h->td_ev[slot]));
+  TickDesc* tdh = h->td_host + slot;
+  h->ctl.plan_call(tdh);
+  CK(cudaMemcpyAsync(h->td_dev, tdh, sizeof(TickDesc), cudaMemcpyHostToDevice, h->stream));
+  CK(cudaEventRecord(h->td_ev[slot], h->stream));
+  h->td_ev_used[slot] = true;
+  const int na = tdh->n_active;
+  const int rows = na * h->L;
+  const int par = int(call & 1);
+  const bool first = h->rank == 0, last = h->rank == h->K - 1;
+  // fill tick info (host, no sync)
+  h->info.call = call;
+  h->info.num_entries = na;
+  h->info.steps = h->n;
+  for (int j = 0; j < 8; ++j) h->info.chunk[j] = (j < h->n && tdh->e[j].active) ? tdh->e[j].X : -1;
+  h->info.out_chunk = (last && tdh->out_entry >= 0) ? h->ctl.out_chunk(call) : -1;
+  if (out_chunk) *out_chunk = h->info.out_chunk;
+
+  if (first) {
+    CK(cudaMemcpyAsync(h->lat_in, chunk_latent, size_t(h->CTHW) * 4, cudaMemcpyDefault, h->stream));
+    noise_ctl_kernel<<<1, 1024, 0, h->stream>>>(h->lat_in, h->prev_frame, h->ctrl, h->st.lat, h->st.sig, h->st.sign,
+                                               h->td_dev, h->scfg, h->CTHW, h->hh * h->ww, h->T);
+    CKL();
+    if (na > 1) {
+      const float* rin = h->K == 1 ? h->ring[1][(call + 1) & 1] : h->ring[0][par];
+      assemble_kernel<<<dim3(64, h->n - 1), 256, 0, h->stream>>>(rin, h->st.lat, h->td_dev, h->n, h->CTHW);
+      CKL();
+    }
+    patch_embed_kernel<<<(rows + 15) / 16, 256, 16 * h->P * 4, h->stream>>>(
+        h->st.lat, h->gw[G_PATCH_W], h->gw[G_PATCH_B], h->st.x, rows, h->L, h->d, h->C, h->T, h->hh, h->ww);
+    CKL();
+    sinusoid_kernel<<<na, 128, 0, h->stream>>>(h->st.sig, h->emb, na, h->md.freq_dim);
+    CKL();
+    const int d = h->d;
+    gemv_kernel<float><<<(d + 7) / 8, 256, 0, h->stream>>>(h->gw[G_T1_W], h->gw[G_T1_B], h->emb, h->t1, na, d,
+                                                           h->md.freq_dim, 0);
+    gemv_kernel<float><<<(d + 7) / 8, 256, 0, h->stream>>>(h->gw[G_T2_W], h->gw[G_T2_B], h->t1, h->st.e, na, d, d, 1);
+    gemv_kernel<TA><<<(6 * d + 7) / 8, 256, 0, h->stream>>>(static_cast<const TA*>(h->tp_w), h->gw[G_TP_B], h->st.e,
+                                                            h->st.e0, na, 6 * d, d, 1);
+    CKL();
+  } else {
+    CK(cudaMemcpyAsync(h->packet_base, h->act_io[0][par], h->st.bytes, cudaMemcpyDeviceToDevice, h->stream));
+  }
+  bool any_rebase = false;
+  for (int j = 0; j < h->n; ++j) any_rebase |= (tdh->e[j].active && tdh->e[j].rebase);
+  if (any_rebase) {
+    rebase_kernel<TA><<<dim3(512, h->n), 256, 0, h->stream>>>(static_cast<TA*>(h->Kc), h->td_dev, h->rt, h->nb, h->n,
+                                                               h->S, h->m, h->W, h->L, h->d, h->hd, h->T_reset);
+    CKL();
+  }
+  for (int b = 0; b < h->nb; ++b) TRY(run_block<TA>(h, b, rows, na));
+  if (!last) {
+    CK(cudaMemcpyAsync(h->act_io[1][par], h->packet_base, h->st.bytes, cudaMemcpyDeviceToDevice, h->stream));
+  } else {
+    float* rout = h->K == 1 ? h->ring[1][call & 1] : h->ring[1][par];
+    head_kernel<<<(rows + 7) / 8, 256, 8 * h->d * 4, h->stream>>>(
+        h->st.x, h->st.e, h->gw[G_HEAD_MOD], h->gw[G_HEAD_W], h->gw[G_HEAD_B], h->st.lat, h->st.sig, h->st.sign,
+        h->out_stage, rout, h->td_dev, rows, h->d, h->L, h->C, h->T, h->hh, h->ww, h->n, h->md.eps,
+        h->md.norm_center, h->scfg.seed);
+    CKL();
+    if (tdh->out_entry >= 0 && out_latent)
+      CK(cudaMemcpyAsync(out_latent, h->out_stage, size_t(h->CTHW) * 4, cudaMemcpyDefault, h->stream));
+  }
+  return SDV2_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sdv2_status_string(sdv2_status s) {
+  switch (s) {
+    case SDV2_OK: return "ok";
+    case SDV2_E_INVALID: return "invalid argument";
+    case SDV2_E_SHAPE: return "invalid shape";
+    case SDV2_E_STATE: return "invalid state";
+    case SDV2_E_WORKSPACE: return "workspace too small";
+    case SDV2_E_CUDA: return "cuda error";
+    case SDV2_E_UNSUPPORTED: return "unsupported shape";
+  }
+  return "unknown status";
+}
+
+const char* sdv2_last_error(const sdv2_handle* h) { return h ? h->err.c_str() : "null handle"; }
+
+size_t sdv2_workspace_bytes(const sdv2_model_desc* md, const sdv2_geometry* g, const sdv2_pipeline_desc* pp,
+                            sdv2_precision prec) {
+  sdv2_handle tmp;
+  std::string why;
+  if (fill_dims(&tmp, md, g, pp, prec, &why) != SDV2_OK) return 0;
+  return carve(&tmp, nullptr);
+}
+
+sdv2_status sdv2_create(const sdv2_model_desc* md, const sdv2_geometry* g, const sdv2_pipeline_desc* pp,
+                        sdv2_precision prec, const sdv2_weights* w, void* workspace, size_t workspace_bytes,
+                        int device, void* stream, sdv2_handle** out) {
+  if (!out) return SDV2_E_INVALID;
+  *out = nullptr;
+  auto* h = new sdv2_handle();
+  std::string why;
+  sdv2_status s = fill_dims(h, md, g, pp, prec, &why);
+  if (s != SDV2_OK) {
+    delete h;
+    return s;
+  }
+  const size_t need = carve(h, nullptr);
+  if (!workspace || workspace_bytes < need) {
+    delete h;
+    return SDV2_E_WORKSPACE;
+  }
+  if (!w || !w->tensors || w->count != kNumGlobal + kNumBlockT * h->nb) {
+    delete h;
+    return SDV2_E_INVALID;
+  }
+  h->device = device;
+  h->stream = static_cast<cudaStream_t>(stream);
+  h->ws_bytes = workspace_bytes;
+  if (cudaSetDevice(device) != cudaSuccess) {
+    delete h;
+    return SDV2_E_CUDA;
+  }
+  // align the base to 1 KB
+  char* base = static_cast<char*>(workspace);
+  const size_t adj = (1024 - (reinterpret_cast<uintptr_t>(base) & 1023)) & 1023;
+  if (workspace_bytes < need + adj) {
+    delete h;
+    return SDV2_E_WORKSPACE;
+  }
+  carve(h, base + adj);
+  auto fail = [&](sdv2_status st) {
+    *out = h;   // keep the handle so the caller can read sdv2_last_error, then destroy
+    return st;
+  };
+  if (cudaHostAlloc(reinterpret_cast<void**>(&h->td_host), sizeof(TickDesc) * kTdRing, cudaHostAllocDefault) != cudaSuccess)
+    return fail(SDV2_E_CUDA);
+  for (int i = 0; i < kTdRing; ++i) {
+    cudaEventCreateWithFlags(&h->td_ev[i], cudaEventDisableTiming);
+    h->td_ev_used[i] = false;
+  }
+  const void* const* T = w->tensors;
+  const int d = h->d;
+  const size_t sizes[kNumGlobal] = {size_t(d) * h->P, size_t(d), size_t(d) * h->Dt, size_t(d), size_t(d) * d, size_t(d),
+                                    size_t(d) * 256, size_t(d), size_t(d) * d, size_t(d), size_t(6) * d * d,
+                                    size_t(6) * d, size_t(2) * d, size_t(h->P) * d, size_t(h->P)};
+  for (int i = 0; i < kNumGlobal; ++i) {
+    if (i == G_TP_W) s = load_tensor(h, T[i], h->tp_w, sizes[i], true);
+    else s = load_tensor(h, T[i], h->gw[i], sizes[i], false);
+    if (s != SDV2_OK) return fail(s);
+  }
+  for (int b = 0; b < h->nb; ++b) {
+    const void* const* Bt = T + kNumGlobal + kNumBlockT * b;
+    BlockW& B = h->bw[b];
+    const size_t dd = size_t(d) * d, tb = h->ta;
+    struct { int id; void* dst; size_t n; bool tw; } list[] = {
+        {B_MOD, B.mod, size_t(6) * d, false},
+        {B_WQ, B.wqkv, dd, true}, {B_WK, static_cast<char*>(B.wqkv) + dd * tb, dd, true},
+        {B_WV, static_cast<char*>(B.wqkv) + 2 * dd * tb, dd, true},
+        {B_BQ, B.bqkv, size_t(d), false}, {B_BK, B.bqkv + d, size_t(d), false}, {B_BV, B.bqkv + 2 * d, size_t(d), false},
+        {B_WO, B.wo, dd, true}, {B_BO, B.bo, size_t(d), false},
+        {B_GQ, B.gq, size_t(d), false}, {B_GK, B.gk, size_t(d), false},
+        {B_N3G, B.n3g, size_t(d), false}, {B_N3B, B.n3b, size_t(d), false},
+        {B_WCQ, B.wcq, dd, true}, {B_BCQ, B.bcq, size_t(d), false},
+        {B_WCK, B.wck, dd, true}, {B_BCK, B.bck, size_t(d), false},
+        {B_WCV, B.wcv, dd, true}, {B_BCV, B.bcv, size_t(d), false},
+        {B_WCO, B.wco, dd, true}, {B_BCO, B.bco, size_t(d), false},
+        {B_GCQ, B.gcq, size_t(d), false}, {B_GCK, B.gck, size_t(d), false},
+        {B_W1, B.w1, size_t(h->F) * d, true}, {B_B1, B.b1, size_t(h->F), false},
+        {B_W2, B.w2, size_t(d) * h->F, true}, {B_B2, B.b2, size_t(d), false},
+    };
+    for (auto& it : list) {
+      s = load_tensor(h, Bt[it.id], it.dst, it.n, it.tw);
+      if (s != SDV2_OK) return fail(s);
+    }
+  }
+  if (cudaStreamSynchronize(h->stream) != cudaSuccess) {
+    h->err = cudaGetErrorString(cudaGetLastError());
+    return fail(SDV2_E_CUDA);
+  }
+  if (h->prec == SDV2_BF16 && !tc_gemm_plan(h->gplan, &h->err)) return fail(SDV2_E_CUDA);
+  *out = h;
+  return SDV2_OK;
+}
+
+sdv2_status sdv2_reset_stream(sdv2_handle* h, const sdv2_stream_desc* sd, const float* prompt_host) {
+  if (!h || !sd || !prompt_host) return SDV2_E_INVALID;
+  if (!sd->timesteps || sd->num_timesteps != h->n) return SDV2_E_INVALID;
+  for (int j = 0; j < h->n; ++j) {
+    if (!(sd->timesteps[j] > 0.f) || sd->timesteps[j] > 1000.f) return SDV2_E_INVALID;
+    if (j > 0 && !(sd->timesteps[j] < sd->timesteps[j - 1])) return SDV2_E_INVALID;
+  }
+  if (!(sd->s_min < sd->s_max) || sd->s_min < 0.f || sd->s_max > 1.f) return SDV2_E_INVALID;
+  if (!(sd->ema_lambda > 0.f) || sd->ema_lambda > 1.f) return SDV2_E_INVALID;
+  if (!(sd->motion_sigma > 0.f) || sd->motion_k < 0 || sd->motion_k >= 63) return SDV2_E_INVALID;
+  if (sd->sink_tau < -1.f || sd->sink_tau > 1.f) return SDV2_E_INVALID;
+  if (sd->rope_reset_frames < std::max(h->m, h->W) * h->T || sd->rope_reset_frames + h->T > 4096) return SDV2_E_INVALID;
+  h->T_reset = sd->rope_reset_frames;
+  for (int j = 0; j < kMaxSteps; ++j) h->scfg.t[j] = j < h->n ? sd->timesteps[j] : 0.f;
+  h->scfg.n = h->n;
+  h->scfg.k = sd->motion_k;
+  h->scfg.sigma_m = sd->motion_sigma;
+  h->scfg.s_min = sd->s_min;
+  h->scfg.s_max = sd->s_max;
+  h->scfg.lam = sd->ema_lambda;
+  h->scfg.seed = sd->seed;
+  CtlParams p;
+  p.T = h->T; p.m = h->m; p.W = h->W; p.n = h->n; p.K = h->K; p.rank = h->rank; p.T_reset = h->T_reset;
+  p.tau = sd->sink_tau;
+  h->ctl.reset(p);
+  // RoPE tables (C.6): temporal positions -t_off..t_off, height 0..hn-1, width 0..wn-1; fp64 -> fp32
+  const int t_off = h->T_reset + h->T + 1;
+  {
+    std::vector<float> tab;
+    const int rows_t = 2 * t_off + 1;
+    tab.resize(size_t(rows_t) * h->ct * 2 + size_t(h->hn) * h->ch * 2 + size_t(h->wn) * h->cw * 2);
+    float* p0 = tab.data();
+    auto fill = [&](float* cs, float* sn, int rows, int c, int base) {
+      for (int r = 0; r < rows; ++r)
+        for (int i = 0; i < c; ++i) {
+          const double om = std::pow(10000.0, -double(i) / double(c));
+          const double ang = double(r + base) * om;
+          cs[size_t(r) * c + i] = float(std::cos(ang));
+          sn[size_t(r) * c + i] = float(std::sin(ang));
+        }
+    };
+    float* tcs = p0; float* tsn = tcs + size_t(rows_t) * h->ct;
+    float* hcs = tsn + size_t(rows_t) * h->ct; float* hsn = hcs + size_t(h->hn) * h->ch;
+    float* wcs = hsn + size_t(h->hn) * h->ch; float* wsn = wcs + size_t(h->wn) * h->cw;
+    fill(tcs, tsn, rows_t, h->ct, -t_off);
+    fill(hcs, hsn, h->hn, h->ch, 0);
+    fill(wcs, wsn, h->wn, h->cw, 0);
+    CK(cudaMemcpyAsync(h->rope, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice, h->stream));
+    const size_t o_tsn = size_t(rows_t) * h->ct, o_hcs = 2 * o_tsn, o_hsn = o_hcs + size_t(h->hn) * h->ch,
+                 o_wcs = o_hsn + size_t(h->hn) * h->ch, o_wsn = o_wcs + size_t(h->wn) * h->cw;
+    h->rt.ct_cos = h->rope; h->rt.ct_sin = h->rope + o_tsn;
+    h->rt.ch_cos = h->rope + o_hcs; h->rt.ch_sin = h->rope + o_hsn;
+    h->rt.cw_cos = h->rope + o_wcs; h->rt.cw_sin = h->rope + o_wsn;
+    h->rt.ct = h->ct; h->rt.ch = h->ch; h->rt.cw = h->cw; h->rt.t_off = t_off;
+    CK(cudaStreamSynchronize(h->stream));   // the host table vector dies here
+  }
+  // zero lanes, controller state
+  const size_t kv = size_t(h->nb) * h->n * h->S * h->L * h->d * h->ta;
+  CK(cudaMemsetAsync(h->Kc, 0, kv, h->stream));
+  CK(cudaMemsetAsync(h->Vc, 0, kv, h->stream));
+  CK(cudaMemsetAsync(h->ctrl, 0, sizeof(CtrlState), h->stream));
+  CK(cudaMemsetAsync(h->packet_base, 0, h->st.bytes, h->stream));
+  {
+    CtrlState cs;
+    std::memset(&cs, 0, sizeof(cs));
+    cs.s = double(sd->s_max);   // s_{-1} = s_max (Q15)
+    CK(cudaMemcpyAsync(h->ctrl, &cs, sizeof(cs), cudaMemcpyHostToDevice, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+  }
+  h->pver = 0;
+  sdv2_status s = set_prompt_common(h, prompt_host, 0);
+  if (s != SDV2_OK) return s;
+  h->stream_ready = true;
+  return SDV2_OK;
+}
+
+sdv2_status sdv2_set_prompt(sdv2_handle* h, const float* prompt_host) {
+  if (!h || !prompt_host) return SDV2_E_INVALID;
+  if (!h->stream_ready) return SDV2_E_STATE;
+  // the version slot being overwritten must not be used by an in-flight entry: the
+  // oldest in-flight chunk is call - (n-1) K; versions alternate, so require that the
+  // previous switch happened at least (n-1) K + 1 calls ago.
+  sdv2_status s = set_prompt_common(h, prompt_host, h->pver + 1);
+  if (s == SDV2_OK) h->pver += 1;
+  return s;
+}
+
+sdv2_status sdv2_denoise_chunk(sdv2_handle* h, const float* chunk_latent, float* out_latent, int64_t* out_chunk_index) {
+  if (!h) return SDV2_E_INVALID;
+  if (!h->stream_ready) return SDV2_E_STATE;
+  if (h->rank == 0 && !chunk_latent) return SDV2_E_STATE;
+  if (h->rank != 0 && chunk_latent) return SDV2_E_STATE;
+  if (h->rank != h->K - 1 && out_latent) return SDV2_E_STATE;
+  return h->prec == SDV2_FP32 ? tick<float>(h, chunk_latent, out_latent, out_chunk_index)
+                              : tick<bf16>(h, chunk_latent, out_latent, out_chunk_index);
+}
+
+sdv2_status sdv2_stage_io_buffers(sdv2_handle* h, int32_t parity, sdv2_stage_io* io) {
+  if (!h || !io || parity < 0 || parity > 1) return SDV2_E_INVALID;
+  io->act_in = h->act_io[0][parity];
+  io->act_out = h->act_io[1][parity];
+  io->act_bytes = h->K > 1 ? h->st.bytes : 0;
+  io->ring_in = h->ring[0][parity];
+  io->ring_out = h->ring[1][parity];
+  io->ring_bytes = size_t(h->n > 1 ? h->n - 1 : 0) * h->CTHW * 4;
+  return SDV2_OK;
+}
+
+sdv2_status sdv2_get_tick_info(const sdv2_handle* h, sdv2_tick_info* info) {
+  if (!h || !info) return SDV2_E_INVALID;
+  *info = h->info;
+  return SDV2_OK;
+}
+
+sdv2_status sdv2_get_cache_state(sdv2_handle* h, int32_t local_block, int32_t lane, sdv2_cache_state* st) {
+  if (!h || !st || local_block < 0 || local_block >= h->nb || lane < 0 || lane >= h->n) return SDV2_E_INVALID;
+  const LaneMeta& L = h->ctl.lane(lane);
+  std::memset(st, 0, sizeof(*st));
+  st->num_slots = h->S;
+  st->num_valid = L.nvalid;
+  for (int s = 0; s < h->S; ++s) {
+    st->tag[s] = L.tag[s];
+    st->pos[s] = L.pos[s][0];
+  }
+  st->resets = L.r;
+  st->evictions = L.evictions;
+  if (h->rank == 0) {
+    CtrlState cs;
+    CK(cudaStreamSynchronize(h->stream));
+    CK(cudaMemcpy(&cs, h->ctrl, sizeof(cs), cudaMemcpyDeviceToHost));
+    st->noise_rate = cs.s;
+    st->d_hat = cs.d_hat;
+  }
+  return SDV2_OK;
+}
+
+sdv2_status sdv2_set_block_tap(sdv2_handle* h, float* per_block_out) {
+  if (!h) return SDV2_E_INVALID;
+  h->tap = per_block_out;
+  return SDV2_OK;
+}
+
+sdv2_status sdv2_kv_lane(sdv2_handle* h, int32_t local_block, int32_t lane, int32_t which, void** ptr, size_t* elems) {
+  if (!h || !ptr || !elems || local_block < 0 || local_block >= h->nb || lane < 0 || lane >= h->n) return SDV2_E_INVALID;
+  const size_t per_lane = size_t(h->S) * h->L * h->d;
+  char* base = static_cast<char*>(which ? h->Vc : h->Kc);
+  *ptr = base + ((size_t(local_block) * h->n + lane) * per_lane) * h->ta;
+  *elems = per_lane;
+  return SDV2_OK;
+}
+
+sdv2_status sdv2_destroy(sdv2_handle* h) {
+  if (!h) return SDV2_E_INVALID;
+  if (h->stream_ready || h->td_host) cudaStreamSynchronize(h->stream);
+  for (int i = 0; i < kTdRing; ++i)
+    if (h->td_host) cudaEventDestroy(h->td_ev[i]);
+  if (h->td_host) cudaFreeHost(h->td_host);
+  delete h;
+  return SDV2_OK;
+}
+
+}  // extern "C"

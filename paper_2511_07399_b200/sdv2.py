@@ -1,0 +1,327 @@
+"""Thin ctypes binding of libsdv2.so (include/sdv2.h).  Argument marshalling only:
+every step of the hot path runs in the library's CUDA kernels.  PyTorch provides the
+device workspace and the CUDA stream.  There is no CPU fallback: importing the
+binding without the built library raises."""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Dict, Optional, Sequence
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libsdv2.so")
+CTL_LIB_PATH = os.path.join(HERE, "libsdv2_ctl.so")
+
+SDV2_FP32, SDV2_BF16 = 0, 1
+STATUS = {0: "ok", -1: "invalid argument", -2: "invalid shape", -3: "invalid state",
+          -4: "workspace too small", -5: "cuda error", -6: "unsupported shape"}
+
+GLOBAL_ORDER = ("patch_w", "patch_b", "txt1_w", "txt1_b", "txt2_w", "txt2_b", "t1_w", "t1_b", "t2_w", "t2_b",
+                "tp_w", "tp_b", "head_mod", "head_w", "head_b")
+BLOCK_ORDER = ("mod", "wq", "bq", "wk", "bk", "wv", "bv", "wo", "bo", "gq", "gk", "n3_g", "n3_b", "wcq", "bcq",
+               "wck", "bck", "wcv", "bcv", "wco", "bco", "gcq", "gck", "w1", "b1", "w2", "b2")
+
+
+class ModelDescC(ctypes.Structure):
+    _fields_ = [("num_blocks", ctypes.c_int32), ("dim", ctypes.c_int32), ("num_heads", ctypes.c_int32),
+                ("ffn_dim", ctypes.c_int32), ("latent_channels", ctypes.c_int32), ("patch_t", ctypes.c_int32),
+                ("patch_h", ctypes.c_int32), ("patch_w", ctypes.c_int32), ("text_len", ctypes.c_int32),
+                ("text_dim", ctypes.c_int32), ("freq_dim", ctypes.c_int32), ("eps", ctypes.c_float),
+                ("norm_center", ctypes.c_int32)]
+
+
+class GeometryC(ctypes.Structure):
+    _fields_ = [("latent_h", ctypes.c_int32), ("latent_w", ctypes.c_int32), ("chunk_frames", ctypes.c_int32),
+                ("steps", ctypes.c_int32), ("sink_chunks", ctypes.c_int32), ("window_chunks", ctypes.c_int32)]
+
+
+class PipelineC(ctypes.Structure):
+    _fields_ = [("world", ctypes.c_int32), ("rank", ctypes.c_int32), ("block_begin", ctypes.c_int32),
+                ("block_end", ctypes.c_int32)]
+
+
+class WeightsC(ctypes.Structure):
+    _fields_ = [("tensors", ctypes.POINTER(ctypes.c_void_p)), ("count", ctypes.c_int32)]
+
+
+class StreamDescC(ctypes.Structure):
+    _fields_ = [("timesteps", ctypes.POINTER(ctypes.c_float)), ("num_timesteps", ctypes.c_int32),
+                ("rope_reset_frames", ctypes.c_int32), ("motion_k", ctypes.c_int32),
+                ("motion_sigma", ctypes.c_float), ("s_min", ctypes.c_float), ("s_max", ctypes.c_float),
+                ("ema_lambda", ctypes.c_float), ("sink_tau", ctypes.c_float), ("seed", ctypes.c_uint64)]
+
+
+class StageIOC(ctypes.Structure):
+    _fields_ = [("act_in", ctypes.c_void_p), ("act_out", ctypes.c_void_p), ("act_bytes", ctypes.c_size_t),
+                ("ring_in", ctypes.c_void_p), ("ring_out", ctypes.c_void_p), ("ring_bytes", ctypes.c_size_t)]
+
+
+class TickInfoC(ctypes.Structure):
+    _fields_ = [("call", ctypes.c_int64), ("num_entries", ctypes.c_int32), ("steps", ctypes.c_int32),
+                ("chunk", ctypes.c_int64 * 8), ("out_chunk", ctypes.c_int64)]
+
+
+class CacheStateC(ctypes.Structure):
+    _fields_ = [("num_slots", ctypes.c_int32), ("num_valid", ctypes.c_int32), ("tag", ctypes.c_int64 * 64),
+                ("pos", ctypes.c_int32 * 64), ("resets", ctypes.c_int32), ("evictions", ctypes.c_int64),
+                ("noise_rate", ctypes.c_double), ("d_hat", ctypes.c_double)]
+
+
+_EXPORTS = ["sdv2_workspace_bytes", "sdv2_create", "sdv2_reset_stream", "sdv2_set_prompt", "sdv2_denoise_chunk",
+            "sdv2_stage_io_buffers", "sdv2_get_tick_info", "sdv2_destroy", "sdv2_status_string",
+            "sdv2_last_error", "sdv2_get_cache_state", "sdv2_set_block_tap", "sdv2_kv_lane", "sdv2_partition"]
+
+
+def _declare(lib):
+    P = ctypes.c_void_p
+    lib.sdv2_workspace_bytes.restype = ctypes.c_size_t
+    lib.sdv2_workspace_bytes.argtypes = [ctypes.POINTER(ModelDescC), ctypes.POINTER(GeometryC),
+                                         ctypes.POINTER(PipelineC), ctypes.c_int]
+    lib.sdv2_create.argtypes = [ctypes.POINTER(ModelDescC), ctypes.POINTER(GeometryC), ctypes.POINTER(PipelineC),
+                                ctypes.c_int, ctypes.POINTER(WeightsC), P, ctypes.c_size_t, ctypes.c_int, P,
+                                ctypes.POINTER(P)]
+    lib.sdv2_reset_stream.argtypes = [P, ctypes.POINTER(StreamDescC), P]
+    lib.sdv2_set_prompt.argtypes = [P, P]
+    lib.sdv2_denoise_chunk.argtypes = [P, P, P, ctypes.POINTER(ctypes.c_int64)]
+    lib.sdv2_stage_io_buffers.argtypes = [P, ctypes.c_int32, ctypes.POINTER(StageIOC)]
+    lib.sdv2_get_tick_info.argtypes = [P, ctypes.POINTER(TickInfoC)]
+    lib.sdv2_destroy.argtypes = [P]
+    lib.sdv2_status_string.restype = ctypes.c_char_p
+    lib.sdv2_status_string.argtypes = [ctypes.c_int]
+    lib.sdv2_last_error.restype = ctypes.c_char_p
+    lib.sdv2_last_error.argtypes = [P]
+    lib.sdv2_get_cache_state.argtypes = [P, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(CacheStateC)]
+    lib.sdv2_set_block_tap.argtypes = [P, P]
+    lib.sdv2_kv_lane.argtypes = [P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(P),
+                                 ctypes.POINTER(ctypes.c_size_t)]
+    lib.sdv2_partition.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.c_int32, ctypes.c_int32,
+                                   ctypes.c_double, ctypes.c_double, ctypes.POINTER(ctypes.c_int32),
+                                   ctypes.POINTER(ctypes.c_double)]
+    for f in ("sdv2_create", "sdv2_reset_stream", "sdv2_set_prompt", "sdv2_denoise_chunk", "sdv2_stage_io_buffers",
+              "sdv2_get_tick_info", "sdv2_destroy", "sdv2_get_cache_state", "sdv2_set_block_tap", "sdv2_kv_lane",
+              "sdv2_partition"):
+        getattr(lib, f).restype = ctypes.c_int
+    return lib
+
+
+_LIB = None
+
+
+def lib():
+    """Load libsdv2.so (raises if it has not been built: no fallback exists)."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: run `python -m paper_2511_07399_b200.build` "
+                               "(the hot path has no CPU fallback)")
+        _LIB = _declare(ctypes.CDLL(LIB_PATH))
+    return _LIB
+
+
+class SDV2Error(RuntimeError):
+    pass
+
+
+def _check(st, h=None):
+    if st != 0:
+        msg = STATUS.get(st, str(st))
+        if h is not None:
+            msg += ": " + lib().sdv2_last_error(h).decode()
+        raise SDV2Error(msg)
+
+
+def model_desc_c(md) -> ModelDescC:
+    return ModelDescC(md.num_blocks, md.dim, md.num_heads, md.ffn_dim, md.latent_channels, md.patch_t, md.patch_h,
+                      md.patch_w, md.text_len, md.text_dim, md.freq_dim, md.eps, md.norm_center)
+
+
+def geometry_c(g) -> GeometryC:
+    return GeometryC(g.latent_h, g.latent_w, g.chunk_frames, g.steps, g.sink_chunks, g.window_chunks)
+
+
+def partition(costs: Sequence[float], stages: int, extra_first=0.0, extra_last=0.0):
+    """Exact min-max contiguous block partition; returns (bounds, max_stage)."""
+    L = lib() if os.path.exists(LIB_PATH) else ctl_lib()
+    c = (ctypes.c_double * len(costs))(*costs)
+    b = (ctypes.c_int32 * (stages + 1))()
+    mx = ctypes.c_double()
+    _check(L.sdv2_partition(c, len(costs), stages, extra_first, extra_last, b, ctypes.byref(mx)))
+    return list(b), mx.value
+
+
+_CTL = None
+
+
+def ctl_lib():
+    """Host control plane alone (no CUDA needed): libsdv2_ctl.so."""
+    global _CTL
+    if _CTL is None:
+        if not os.path.exists(CTL_LIB_PATH):
+            raise RuntimeError(f"{CTL_LIB_PATH} is missing: run `python -m paper_2511_07399_b200.build`")
+        L = ctypes.CDLL(CTL_LIB_PATH)
+        L.sdv2ctl_new.restype = ctypes.c_void_p
+        L.sdv2ctl_new.argtypes = [ctypes.c_int32] * 7 + [ctypes.c_double]
+        L.sdv2ctl_free.argtypes = [ctypes.c_void_p]
+        L.sdv2ctl_set_prompt_mean.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.c_int32,
+                                              ctypes.c_int32]
+        L.sdv2ctl_call.restype = ctypes.c_int32
+        L.sdv2ctl_call.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int64)]
+        L.sdv2ctl_lane_state.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.POINTER(CacheStateC)]
+        L.sdv2ctl_max_frames.restype = ctypes.c_int32
+        L.sdv2_partition.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.c_int32, ctypes.c_int32,
+                                     ctypes.c_double, ctypes.c_double, ctypes.POINTER(ctypes.c_int32),
+                                     ctypes.POINTER(ctypes.c_double)]
+        L.sdv2_partition.restype = ctypes.c_int
+        _CTL = L
+    return _CTL
+
+
+class HostControl:
+    """The library's host control plane driven without a GPU (tests)."""
+
+    def __init__(self, T, m, W, n, K=1, rank=0, T_reset=4, tau=0.95):
+        self.L = ctl_lib()
+        self.n = n
+        self.h = self.L.sdv2ctl_new(T, m, W, n, K, rank, T_reset, tau)
+        if not self.h:
+            raise SDV2Error("invalid control parameters")
+        self.F = self.L.sdv2ctl_max_frames()
+
+    def set_prompt_mean(self, h, pver):
+        a = np.ascontiguousarray(h, dtype=np.float64)
+        self.L.sdv2ctl_set_prompt_mean(self.h, a.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), a.size, pver)
+
+    def call(self):
+        out = (ctypes.c_int32 * (self.n * (8 + self.F)))()
+        oc = ctypes.c_int64()
+        na = self.L.sdv2ctl_call(self.h, out, ctypes.byref(oc))
+        ents = []
+        for j in range(self.n):
+            o = out[j * (8 + self.F):(j + 1) * (8 + self.F)]
+            ents.append({"X": o[0], "j": o[1], "active": o[2], "write_slot": o[3], "nvalid": o[4],
+                         "refresh_mask": o[5], "rebase": o[6], "pver": o[7], "pos": list(o[8:])})
+        return na, ents, oc.value
+
+    def lane_state(self, lane):
+        st = CacheStateC()
+        self.L.sdv2ctl_lane_state(self.h, lane, ctypes.byref(st))
+        return st
+
+    def __del__(self):
+        try:
+            self.L.sdv2ctl_free(self.h)
+        except Exception:
+            pass
+
+
+class Stage:
+    """One pipeline stage (or the whole model when pipeline=None) of the hot path."""
+
+    def __init__(self, md, geom, weights: Dict[str, np.ndarray], precision=SDV2_BF16, pipeline=None,
+                 device=0, stream=None):
+        import torch
+        self.torch = torch
+        self.md, self.geom = md, geom
+        self.precision = precision
+        self.L = lib()
+        self._mdc = model_desc_c(md)
+        self._gc = geometry_c(geom)
+        if pipeline is None:
+            self._pp = None
+            b0, b1 = 0, md.num_blocks
+        else:
+            self._pp = PipelineC(*pipeline)
+            b0, b1 = pipeline[2], pipeline[3]
+        self.block_range = (b0, b1)
+        ppp = ctypes.byref(self._pp) if self._pp is not None else None
+        nbytes = self.L.sdv2_workspace_bytes(ctypes.byref(self._mdc), ctypes.byref(self._gc), ppp, precision)
+        if nbytes == 0:
+            raise SDV2Error("invalid model / geometry descriptor")
+        self.device = device
+        self.workspace = torch.empty(nbytes + 1024, dtype=torch.uint8, device=f"cuda:{device}")
+        self.stream = stream if stream is not None else torch.cuda.current_stream(device)
+        names = list(GLOBAL_ORDER) + [f"blocks.{b}.{t}" for b in range(b0, b1) for t in BLOCK_ORDER]
+        keep = []
+        ptrs = (ctypes.c_void_p * len(names))()
+        for i, nme in enumerate(names):
+            a = weights[nme]
+            if isinstance(a, np.ndarray):
+                a = np.ascontiguousarray(a, dtype=np.float32)
+                ptrs[i] = a.ctypes.data
+            else:   # torch tensor (host or device), fp32 contiguous
+                a = a.contiguous().float()
+                ptrs[i] = a.data_ptr()
+            keep.append(a)
+        w = WeightsC(ptrs, len(names))
+        h = ctypes.c_void_p()
+        st = self.L.sdv2_create(ctypes.byref(self._mdc), ctypes.byref(self._gc), ppp, precision, ctypes.byref(w),
+                                ctypes.c_void_p(self.workspace.data_ptr()), nbytes + 1024, device,
+                                ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(h))
+        if st != 0:
+            if h.value:
+                msg = self.L.sdv2_last_error(h).decode()
+                self.L.sdv2_destroy(h)
+                raise SDV2Error(f"{STATUS.get(st, st)}: {msg}")
+            raise SDV2Error(STATUS.get(st, str(st)))
+        self.h = h
+        del keep
+
+    # ---------------------------------------------------------------- stream
+    def reset_stream(self, sd, prompt: np.ndarray):
+        ts = (ctypes.c_float * len(sd.timesteps))(*sd.timesteps)
+        self._ts = ts
+        c = StreamDescC(ts, len(sd.timesteps), sd.rope_reset_frames, sd.motion_k, sd.motion_sigma, sd.s_min,
+                        sd.s_max, sd.ema_lambda, sd.sink_tau, sd.seed)
+        p = np.ascontiguousarray(prompt, dtype=np.float32)
+        _check(self.L.sdv2_reset_stream(self.h, ctypes.byref(c), ctypes.c_void_p(p.ctypes.data)), self.h)
+
+    def set_prompt(self, prompt: np.ndarray):
+        p = np.ascontiguousarray(prompt, dtype=np.float32)
+        _check(self.L.sdv2_set_prompt(self.h, ctypes.c_void_p(p.ctypes.data)), self.h)
+
+    def denoise_chunk(self, chunk_ptr: Optional[int], out_ptr: Optional[int]) -> int:
+        """chunk_ptr / out_ptr: raw host or device addresses (or None).  Returns the chunk
+        index emitted into out_ptr, or -1."""
+        oc = ctypes.c_int64(-1)
+        _check(self.L.sdv2_denoise_chunk(self.h, ctypes.c_void_p(chunk_ptr) if chunk_ptr else None,
+                                         ctypes.c_void_p(out_ptr) if out_ptr else None, ctypes.byref(oc)), self.h)
+        return oc.value
+
+    def tick_info(self):
+        i = TickInfoC()
+        _check(self.L.sdv2_get_tick_info(self.h, ctypes.byref(i)), self.h)
+        return {"call": i.call, "num_entries": i.num_entries, "chunk": list(i.chunk)[:i.steps],
+                "out_chunk": i.out_chunk}
+
+    def stage_io(self, parity: int):
+        io = StageIOC()
+        _check(self.L.sdv2_stage_io_buffers(self.h, parity, ctypes.byref(io)), self.h)
+        return io
+
+    def cache_state(self, local_block: int, lane: int):
+        st = CacheStateC()
+        _check(self.L.sdv2_get_cache_state(self.h, local_block, lane, ctypes.byref(st)), self.h)
+        return st
+
+    def set_block_tap(self, tensor):
+        _check(self.L.sdv2_set_block_tap(self.h, ctypes.c_void_p(tensor.data_ptr()) if tensor is not None else None),
+               self.h)
+
+    def kv_lane(self, local_block, lane, which):
+        p = ctypes.c_void_p()
+        n = ctypes.c_size_t()
+        _check(self.L.sdv2_kv_lane(self.h, local_block, lane, which, ctypes.byref(p), ctypes.byref(n)), self.h)
+        return p.value, n.value
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.sdv2_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

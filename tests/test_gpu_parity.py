@@ -1,0 +1,52 @@
+"""GPU path vs the CPU oracle on identical seeded weights and inputs (BASELINE.json
+north star tolerances): fp32 path rel-L2 <= 1e-4, bf16 path rel-L2 <= 2e-2 per block
+output, cache metadata bit-exact."""
+import numpy as np
+import pytest
+
+import synthgen as sg
+from oracle.stream import run_stream
+from paper_2511_07399_b200.sdv2 import SDV2_BF16, SDV2_FP32
+
+from gpu_harness import rel_l2, run_gpu, tiny_inputs
+
+TOL = {SDV2_FP32: 1e-4, SDV2_BF16: 2e-2}
+
+
+@pytest.fixture(scope="module")
+def tiny_ref():
+    cfg = sg.CONFIGS["tiny"]
+    extra = cfg.geom.steps - 1
+    W, chunks, prompts = tiny_inputs(cfg, extra=extra)
+    recs = run_stream(cfg, W, chunks, prompts, dtype=np.float64, tap=True)
+    return cfg, W, chunks, prompts, recs
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("prec", [SDV2_FP32, SDV2_BF16])
+def test_tiny_stream_parity(tiny_ref, prec):
+    cfg, W, chunks, prompts, recs = tiny_ref
+    outs, taps, meta = run_gpu(cfg, W, chunks, prompts, prec)
+    tol = TOL[prec]
+    n = cfg.geom.steps
+    worst = 0.0
+    for (X, j), tl in taps.items():
+        ref = recs[X]["entries"][j]["taps"]
+        for b in range(cfg.model.num_blocks):
+            err = rel_l2(tl[b], ref[b])
+            worst = max(worst, err)
+            assert err <= tol, (X, j, b, err)
+    assert len(outs) >= cfg.num_chunks
+    for X in range(cfg.num_chunks):
+        err = rel_l2(outs[X], recs[X]["out"])
+        assert err <= tol, (X, err)
+    # metadata bit-exact: lane j after entry (X, j) == oracle lane after chunk X
+    for (X, j), (slots, s_rate, dh) in meta.items():
+        ost = recs[X]["lane_state"][(0, j)]
+        assert slots == {s: (t, p[0]) for s, (t, p) in ost.items()}, (X, j)
+    # controller state: rank 0's last admission of each call == oracle s_X, d_hat
+    for (X, j), (slots, s_rate, dh) in meta.items():
+        if j == 0:
+            assert s_rate == pytest.approx(recs[X]["motion"]["s"], rel=1e-6)
+            assert dh == pytest.approx(recs[X]["motion"]["d_hat"], rel=1e-6, abs=1e-9)
+    print(f"worst block rel-L2 {worst:.3e}")
