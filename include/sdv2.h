@@ -180,6 +180,14 @@ sdv2_status sdv2_set_block_tap(sdv2_handle* h, float* per_block_out);
 sdv2_status sdv2_kv_lane(sdv2_handle* h, int32_t local_block, int32_t lane, int32_t which,
                          void** ptr, size_t* elems);
 
+/* Kernel-level test hook: one tensor-core GEMM C = A W^T + b on device pointers
+ * (A [M,K] bf16, W [N,K] bf16, bias [N] fp32), epilogue epi = 0 store bf16 to out
+ * [M,N], 1 GELU-tanh store bf16, 2 out (fp32 [M,N]) += (mod[gate_row] + e0[r/L][gate_row]) *
+ * (AW^T + b), 3 out += AW^T + b.  Enqueued on `stream`. */
+sdv2_status sdv2_debug_gemm(const void* A, const void* W, const float* bias, void* out, int32_t M, int32_t N,
+                            int32_t K, int32_t epi, const float* mod, const float* e0, int32_t gate_row, int32_t L,
+                            void* stream);
+
 /* ---- host control plane (no GPU needed; also exported by libsdv2_ctl.so) ---- */
 /* Exact min-max contiguous partition of per-block costs over K stages, with extra
  * cost on the first / last stage (P:231–233 DiT block scheduler).  Ties: earlier

@@ -1,11 +1,325 @@
-// tcgen05 GEMM (placeholder until the tensor-core kernel lands).
+// tcgen05 GEMM for the DiT projections:
+//   C[M, N] = A[M, K] . W[N, K]^T + b, bf16 operands, fp32 accumulation in TMEM,
+// fused epilogues (bf16 store / GELU-tanh / gated fp32 residual / fp32 residual).
+//
+// Design (B200-first): persistent CTAs (one per SM), warp-specialised:
+//   warp 0      TMA producer (A box 64x128, W box 64xBN, 128-byte swizzle, 4-stage ring)
+//   warp 1      MMA issuer: one thread issues tcgen05.mma M=128, N=BN, K=16
+//   warp 2      TMEM allocator (2 accumulator buffers x BN columns)
+//   warps 4..7  epilogue: tcgen05.ld 32 lanes x 32 columns -> epilogue -> global
+// The accumulator is double-buffered in TMEM so the epilogue of tile i overlaps the
+// MMAs of tile i+1.  BN is a runtime parameter (multiple of 32, <= 256) chosen per
+// GEMM shape by the host to balance tiles over the 148 SMs (M = 1560 is awkward).
+// The K reduction order is fixed (64-wide blocks, ascending), independent of M and
+// of the tile shape, so results are batch invariant.
 #pragma once
 #include <string>
+#include <unordered_map>
+
 #include "kernels.cuh"
+#include "tc_common.cuh"
+
 namespace sdv2 {
-struct TmaGemmPlan { int unused = 0; };
-inline bool tc_gemm_enabled() { return false; }
-inline bool tc_gemm_plan(TmaGemmPlan&, std::string*) { return true; }
-inline bool tc_gemm(cudaStream_t, const TmaGemmPlan&, const void*, const void*, int, int, int, int, const EpiArgs&,
-                    std::string* err) { *err = "tc gemm not built"; return false; }
+
+constexpr int kGemmBM = 128, kGemmBK = 64, kGemmStages = 4, kGemmMaxBN = 256;
+constexpr int kGemmSmemA = kGemmBM * kGemmBK * 2;        // 16 KB
+constexpr int kGemmSmemB = kGemmMaxBN * kGemmBK * 2;     // 32 KB
+constexpr int kGemmSmem = kGemmStages * (kGemmSmemA + kGemmSmemB) + 1024 + 256;
+
+template <int EPI, typename TOut>
+__device__ __forceinline__ void gemm_epilogue_chunk(const EpiArgs& ep, int r, int c0, int N, const uint32_t (&v)[32]) {
+  if (c0 + 32 <= N) {
+    float acc[32];
+#pragma unroll
+    for (int i = 0; i < 32; i += 4) {
+      const float4 b = *reinterpret_cast<const float4*>(ep.bias + c0 + i);
+      acc[i] = __uint_as_float(v[i]) + b.x;
+      acc[i + 1] = __uint_as_float(v[i + 1]) + b.y;
+      acc[i + 2] = __uint_as_float(v[i + 2]) + b.z;
+      acc[i + 3] = __uint_as_float(v[i + 3]) + b.w;
+    }
+    if (EPI == EPI_STORE || EPI == EPI_GELU) {
+      TOut* o = reinterpret_cast<TOut*>(ep.out) + size_t(r) * ep.ldo + c0;
+      if constexpr (sizeof(TOut) == 2) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          float a0 = acc[2 * i], a1 = acc[2 * i + 1];
+          if (EPI == EPI_GELU) {
+            a0 = gelu_tanh(a0);
+            a1 = gelu_tanh(a1);
+          }
+          __nv_bfloat162 h2 = __floats2bfloat162_rn(a0, a1);
+          pk[i] = *reinterpret_cast<uint32_t*>(&h2);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          reinterpret_cast<uint4*>(o)[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) o[i] = from_f<TOut>(EPI == EPI_GELU ? gelu_tanh(acc[i]) : acc[i]);
+      }
+    } else {
+      float* x = reinterpret_cast<float*>(ep.out) + size_t(r) * ep.ldo + c0;
+      if (EPI == EPI_RES_GATE) {
+        const int e = r / ep.L;
+        const float* gm = ep.mod + ep.gate_row * N + c0;
+        const float* ge = ep.e0 + size_t(e) * 6 * N + ep.gate_row * N + c0;
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+          const float4 a = *reinterpret_cast<const float4*>(gm + i);
+          const float4 b = *reinterpret_cast<const float4*>(ge + i);
+          float4 xv = *reinterpret_cast<float4*>(x + i);
+          xv.x += (a.x + b.x) * acc[i];
+          xv.y += (a.y + b.y) * acc[i + 1];
+          xv.z += (a.z + b.z) * acc[i + 2];
+          xv.w += (a.w + b.w) * acc[i + 3];
+          *reinterpret_cast<float4*>(x + i) = xv;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+          float4 xv = *reinterpret_cast<float4*>(x + i);
+          xv.x += acc[i];
+          xv.y += acc[i + 1];
+          xv.z += acc[i + 2];
+          xv.w += acc[i + 3];
+          *reinterpret_cast<float4*>(x + i) = xv;
+        }
+      }
+    }
+  } else {
+    for (int i = 0; i < 32; ++i)
+      if (c0 + i < N) epi_store<TOut, EPI>(ep, r, c0 + i, N, __uint_as_float(v[i]));
+  }
+}
+
+template <int EPI, typename TOut>
+__global__ void __launch_bounds__(256, 1) gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA,
+                                                         const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
+                                                         int BN, EpiArgs ep) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kGemmStages * kGemmSmemA;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + kGemmStages * kGemmSmemB);
+  uint64_t* empty = full + kGemmStages;
+  uint64_t* tfull = empty + kGemmStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int num_m = (M + kGemmBM - 1) / kGemmBM, num_n = (N + BN - 1) / BN;
+  const int tiles = num_m * num_n;
+  const int kblocks = K / kGemmBK;
+
+  if (warp == 0 && lane == 0) {
+    tc::tma_prefetch_desc(&tmA);
+    tc::tma_prefetch_desc(&tmB);
+    for (int s = 0; s < kGemmStages; ++s) {
+      tc::mbar_init(full + s, 1);
+      tc::mbar_init(empty + s, 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      tc::mbar_init(tfull + s, 1);
+      tc::mbar_init(tempty + s, 4);
+    }
+    tc::fence_barrier_init();
+  }
+  if (warp == 2) tc::tmem_alloc(tmem_slot, 512);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      const uint32_t bytes = uint32_t(kGemmSmemA) + uint32_t(BN) * kGemmBK * 2;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int mb = t % num_m, nb = t / num_m;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          tc::mbar_wait(empty + stage, phase ^ 1);
+          tc::mbar_expect_tx(full + stage, bytes);
+          tc::tma_load_2d(sA + stage * kGemmSmemA, &tmA, full + stage, kb * kGemmBK, mb * kGemmBM);
+          tc::tma_load_2d(sB + stage * kGemmSmemB, &tmB, full + stage, kb * kGemmBK, nb * BN);
+          if (++stage == kGemmStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = tc::idesc_bf16(kGemmBM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        tc::mbar_wait(tempty + acc, acc_phase ^ 1);
+        tc::tc_fence_after();
+        const uint32_t d_tmem = tmem + uint32_t(acc * BN);
+        for (int kb = 0; kb < kblocks; ++kb) {
+          tc::mbar_wait(full + stage, phase);
+          tc::tc_fence_after();
+          const uint32_t a0 = tc::smem_u32(sA + stage * kGemmSmemA);
+          const uint32_t b0 = tc::smem_u32(sB + stage * kGemmSmemB);
+#pragma unroll
+          for (int k = 0; k < kGemmBK / 16; ++k) {
+            tc::mma_bf16(d_tmem, tc::sw128_kmajor_desc(a0 + k * 32), tc::sw128_kmajor_desc(b0 + k * 32), idesc,
+                         (kb | k) != 0);
+          }
+          tc::mma_commit(empty + stage);
+          if (++stage == kGemmStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc::mma_commit(tfull + acc);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp - 4;   // TMEM lane quarter accessible by this warp
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      const int mb = t % num_m, nb = t / num_m;
+      tc::mbar_wait(tfull + acc, acc_phase);
+      tc::tc_fence_after();
+      const int r = mb * kGemmBM + q * 32 + lane;
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t v[32];
+        tc::tmem_ld32(tmem + (uint32_t(q * 32) << 16) + uint32_t(acc * BN + c), v);
+        tc::tmem_ld_wait();
+        const int c0 = nb * BN + c;
+        if (r < M && c0 < N) gemm_epilogue_chunk<EPI, TOut>(ep, r, c0, N, v);
+      }
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(tempty + acc);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc(tmem, 512);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+struct TmaGemmPlan {
+  PFN_encodeTiled encode = nullptr;
+  int num_sms = 148;
+  std::unordered_map<std::string, CUtensorMap> maps;
+};
+
+inline bool tc_gemm_enabled() { return true; }
+
+inline bool tc_gemm_plan(TmaGemmPlan& p, std::string* err) {
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) {
+    *err = "cuTensorMapEncodeTiled unavailable";
+    return false;
+  }
+  p.encode = reinterpret_cast<PFN_encodeTiled>(fn);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&p.num_sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaFuncSetAttribute(gemm_tc_kernel<EPI_STORE, bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmem);
+  cudaFuncSetAttribute(gemm_tc_kernel<EPI_GELU, bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmem);
+  cudaFuncSetAttribute(gemm_tc_kernel<EPI_RES_GATE, bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmem);
+  cudaFuncSetAttribute(gemm_tc_kernel<EPI_RES, bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmem);
+  return true;
+}
+
+// 2D bf16 K-major tensor map [rows, K] with a (64 x box_rows) box, 128-byte swizzle.
+inline bool tc_make_map(TmaGemmPlan& p, CUtensorMap* m, const void* ptr, int rows, int K, int box_rows,
+                        std::string* err) {
+  const cuuint64_t dims[2] = {cuuint64_t(K), cuuint64_t(rows)};
+  const cuuint64_t strides[1] = {cuuint64_t(K) * 2};
+  const cuuint32_t box[2] = {64, cuuint32_t(box_rows)};
+  const cuuint32_t es[2] = {1, 1};
+  CUresult r = p.encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    *err = "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")";
+    return false;
+  }
+  return true;
+}
+
+inline const CUtensorMap* tc_map(TmaGemmPlan& p, const void* ptr, int rows, int K, int box_rows, std::string* err) {
+  const std::string key = std::to_string(reinterpret_cast<uintptr_t>(ptr)) + ":" + std::to_string(rows) + ":" +
+                          std::to_string(K) + ":" + std::to_string(box_rows);
+  auto it = p.maps.find(key);
+  if (it != p.maps.end()) return &it->second;
+  CUtensorMap m;
+  if (!tc_make_map(p, &m, ptr, rows, K, box_rows, err)) return nullptr;
+  return &(p.maps.emplace(key, m).first->second);
+}
+
+// Tile width N chosen to balance (M/128) x (N/BN) tiles over the SMs: maximise
+// useful-column fraction x wave efficiency.
+inline int tc_pick_bn(int M, int N, int sms) {
+  const int num_m = (M + kGemmBM - 1) / kGemmBM;
+  int best = 256;
+  double best_eff = -1.0;
+  for (int bn = 256; bn >= 64; bn -= 32) {
+    const int num_n = (N + bn - 1) / bn;
+    const int tiles = num_m * num_n;
+    const int waves = (tiles + sms - 1) / sms;
+    const double eff = double(N) / double(num_n * bn) * double(tiles) / double(waves * sms);
+    // prefer wider tiles on ties (fewer, larger MMAs; less A re-read)
+    if (eff > best_eff + 1e-3) {
+      best_eff = eff;
+      best = bn;
+    }
+  }
+  return best;
+}
+
+inline bool tc_gemm(cudaStream_t s, TmaGemmPlan& p, const void* A, const void* W, int M, int N, int K, int epi,
+                    const EpiArgs& ep, std::string* err, int a_rows_alloc = 0) {
+  if (K % kGemmBK != 0 || N % 16 != 0) {
+    *err = "tc_gemm: K % 64 or N % 16";
+    return false;
+  }
+  const int BN = tc_pick_bn(M, N, p.num_sms);
+  const CUtensorMap* ma = tc_map(p, A, a_rows_alloc > 0 ? a_rows_alloc : M, K, kGemmBM, err);
+  const CUtensorMap* mb = tc_map(p, W, N, K, BN, err);
+  if (!ma || !mb) return false;
+  const int tiles = ((M + kGemmBM - 1) / kGemmBM) * ((N + BN - 1) / BN);
+  const int grid = tiles < p.num_sms ? tiles : p.num_sms;
+  switch (epi) {
+    case EPI_STORE: gemm_tc_kernel<EPI_STORE, bf16><<<grid, 256, kGemmSmem, s>>>(*ma, *mb, M, N, K, BN, ep); break;
+    case EPI_GELU: gemm_tc_kernel<EPI_GELU, bf16><<<grid, 256, kGemmSmem, s>>>(*ma, *mb, M, N, K, BN, ep); break;
+    case EPI_RES_GATE: gemm_tc_kernel<EPI_RES_GATE, bf16><<<grid, 256, kGemmSmem, s>>>(*ma, *mb, M, N, K, BN, ep); break;
+    default: gemm_tc_kernel<EPI_RES, bf16><<<grid, 256, kGemmSmem, s>>>(*ma, *mb, M, N, K, BN, ep); break;
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    *err = std::string("gemm_tc launch: ") + cudaGetErrorString(e);
+    return false;
+  }
+  return true;
+}
+
 }  // namespace sdv2

@@ -819,3 +819,28 @@ sdv2_status sdv2_destroy(sdv2_handle* h) {
 }
 
 }  // extern "C"
+
+extern "C" sdv2_status sdv2_debug_gemm(const void* A, const void* W, const float* bias, void* out, int32_t M, int32_t N,
+                                       int32_t K, int32_t epi, const float* mod, const float* e0, int32_t gate_row,
+                                       int32_t L, void* stream) {
+  static TmaGemmPlan plan;
+  static bool ready = false;
+  std::string err;
+  if (!ready) {
+    if (!tc_gemm_plan(plan, &err)) return SDV2_E_CUDA;
+    ready = true;
+  }
+  EpiArgs ep{};
+  ep.out = out;
+  ep.ldo = N;
+  ep.bias = bias;
+  ep.mod = mod;
+  ep.e0 = e0;
+  ep.gate_row = gate_row;
+  ep.L = L > 0 ? L : 1;
+  if (!tc_gemm(static_cast<cudaStream_t>(stream), plan, A, W, M, N, K, epi, ep, &err)) {
+    fprintf(stderr, "sdv2_debug_gemm: %s\n", err.c_str());
+    return SDV2_E_CUDA;
+  }
+  return SDV2_OK;
+}
