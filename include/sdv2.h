@@ -120,7 +120,17 @@ typedef struct {
   int32_t steps;
   int64_t chunk[8];              /* chunk X of entry j (-1 if inactive)             */
   int64_t out_chunk;             /* chunk whose clean latent this call emits, or -1 */
+  int64_t kernel_launches;       /* cumulative kernels this handle has launched      */
 } sdv2_tick_info;
+
+/* Per-kernel-class device time (CUDA events around each launch on the handle's
+ * stream) and algorithmic work, accumulated while profiling is enabled.
+ * Classes: 0 projection GEMMs, 1 self-attention, 2 cross-attention, 3 other. */
+typedef struct {
+  int64_t launches[4];
+  double ms[4];
+  double flops[4];
+} sdv2_profile;
 
 /* Cache metadata of one (local block, lane) after the last call (test introspection). */
 typedef struct {
@@ -179,6 +189,11 @@ sdv2_status sdv2_set_block_tap(sdv2_handle* h, float* per_block_out);
  * (local block, lane): [m+W slots][L tokens][dim], element type = precision. */
 sdv2_status sdv2_kv_lane(sdv2_handle* h, int32_t local_block, int32_t lane, int32_t which,
                          void** ptr, size_t* elems);
+
+/* Enable (1, resets the accumulators) or disable (0) per-class event timing. */
+sdv2_status sdv2_profile_enable(sdv2_handle* h, int32_t enable);
+/* Synchronises the stream and returns the accumulated per-class times. */
+sdv2_status sdv2_profile_read(sdv2_handle* h, sdv2_profile* out);
 
 /* Kernel-level test hook: one tensor-core GEMM C = A W^T + b on device pointers
  * (A [M,K] bf16, W [N,K] bf16, bias [N] fp32), epilogue epi = 0 store bf16 to out

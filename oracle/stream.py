@@ -70,12 +70,14 @@ class StreamOracle:
         # 4. cache update (re-base, write/refresh) then attention over all valid entries
         lane.apply(act, k, v, self.g.chunk_frames)
         pt_q, ph_q, pw_q = M.token_positions(md, self.g, act["pos"])
-        phi_q = M.rope_angles(hd, pt_q, ph_q, pw_q)
+        R = x.shape[0]          # a chunk, or a row prefix of one (bench sample only)
+        phi_q = M.rope_angles(hd, pt_q[:R], ph_q[:R], pw_q[:R])
         ents = lane.attended()
         keys, vals = [], []
         for e in ents:
             pt, ph, pw = M.token_positions(md, self.g, e.pos)
-            phi = M.rope_angles(hd, pt, ph, pw)
+            nk = e.k.shape[0]
+            phi = M.rope_angles(hd, pt[:nk], ph[:nk], pw[:nk])
             keys.append((e.k, phi))
             vals.append(e.v)
         o = np.zeros_like(x)

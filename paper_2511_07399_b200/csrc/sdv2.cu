@@ -132,7 +132,44 @@ struct sdv2_handle {
   sdv2_tick_info info;
   std::string err;
   TmaGemmPlan gplan;
+  int64_t launches = 0;
+  TickDesc* td_host_cur = nullptr;
+  // profiling (sdv2_profile_enable): event pairs around each launch, per class
+  bool prof = false;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_next = 0;
+  struct ProfRec { int cls; double flops; cudaEvent_t a, b; };
+  std::vector<ProfRec> prof_recs;
+  sdv2_profile prof_acc;
 };
+
+namespace {
+// Profiling scope: records an event pair around the launches of one kernel class.
+struct ProfScope {
+  sdv2_handle* h;
+  int cls;
+  double flops;
+  cudaEvent_t a = nullptr;
+  ProfScope(sdv2_handle* h_, int c, double f) : h(h_), cls(c), flops(f) {
+    if (!h->prof) return;
+    if (h->ev_next + 2 > h->ev_pool.size()) {
+      for (int i = 0; i < 256; ++i) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        h->ev_pool.push_back(e);
+      }
+    }
+    a = h->ev_pool[h->ev_next++];
+    cudaEventRecord(a, h->stream);
+  }
+  ~ProfScope() {
+    if (!h->prof || !a) return;
+    cudaEvent_t b = h->ev_pool[h->ev_next++];
+    cudaEventRecord(b, h->stream);
+    h->prof_recs.push_back({cls, flops, a, b});
+  }
+};
+}  // namespace
 
 namespace {
 
@@ -289,6 +326,7 @@ sdv2_status fill_dims(sdv2_handle* h, const sdv2_model_desc* md, const sdv2_geom
 
 #define CKL()                                                                 \
   do {                                                                        \
+    ++h->launches;                                                            \
     cudaError_t e_ = cudaGetLastError();                                      \
     if (e_ != cudaSuccess) {                                                  \
       h->err = std::string("launch: ") + cudaGetErrorString(e_);              \
@@ -334,21 +372,25 @@ sdv2_status gemm_simt(sdv2_handle* h, const TIn* A, const TW* W, int M, int N, i
 
 // Activation GEMM of the hot path: fp32 SIMT on the parity path, tcgen05 on bf16.
 sdv2_status gemm_act(sdv2_handle* h, const void* A, const void* W, int M, int N, int K, int epi, const EpiArgs& ep) {
+  ProfScope ps(h, 0, 2.0 * M * N * K);
   if (h->prec == SDV2_FP32)
     return gemm_simt<float, float, float>(h, static_cast<const float*>(A), static_cast<const float*>(W), M, N, K, K,
                                           epi, ep);
-  if (tc_gemm_enabled())
+  if (tc_gemm_enabled()) {
+    ++h->launches;
     return tc_gemm(h->stream, h->gplan, A, W, M, N, K, epi, ep, &h->err) ? SDV2_OK : SDV2_E_CUDA;
+  }
   return gemm_simt<bf16, bf16, bf16>(h, static_cast<const bf16*>(A), static_cast<const bf16*>(W), M, N, K, K, epi, ep);
 }
 
-sdv2_status attention(sdv2_handle* h, const AttnArgs& aa, int Mrows_entries) {
+sdv2_status attention(sdv2_handle* h, const AttnArgs& aa, int Mrows_entries, double flops) {
+  ProfScope ps(h, aa.cross ? 2 : 1, flops);
   dim3 grid((h->L + 15) / 16, h->H, Mrows_entries);
   if (h->prec == SDV2_FP32) {
     if (h->hd == 64) attn_simt_kernel<float, 64><<<grid, 128, 0, h->stream>>>(aa, h->td_dev);
     else attn_simt_kernel<float, 128><<<grid, 128, 0, h->stream>>>(aa, h->td_dev);
   } else {
-    if (tc_attn_enabled()) return tc_attention(h->stream, aa, h->td_dev, h->hd, h->H, Mrows_entries, &h->err) ? SDV2_OK : SDV2_E_CUDA;
+    if (tc_attn_enabled() && ++h->launches) return tc_attention(h->stream, aa, h->td_dev, h->hd, h->H, Mrows_entries, &h->err) ? SDV2_OK : SDV2_E_CUDA;
     if (h->hd == 64) attn_simt_kernel<bf16, 64><<<grid, 128, 0, h->stream>>>(aa, h->td_dev);
     else attn_simt_kernel<bf16, 128><<<grid, 128, 0, h->stream>>>(aa, h->td_dev);
   }
@@ -395,7 +437,9 @@ sdv2_status run_block(sdv2_handle* h, int bl, int rows, int n_act) {
   AttnArgs aa{};
   aa.q = h->q; aa.ldq = d; aa.K = Kb; aa.V = Vb; aa.kv_lane_stride = size_t(h->S) * h->L * d; aa.ldk = d;
   aa.o = h->o; aa.ldo = d; aa.L = h->L; aa.cross = 0; aa.scale = 1.f / sqrtf(float(h->hd));
-  TRY(attention(h, aa, n_act));
+  double fl_self = 0.0;
+  for (int j = 0; j < n_act; ++j) fl_self += 4.0 * h->L * double(h->td_host_cur->e[j].nvalid) * h->L * d;
+  TRY(attention(h, aa, n_act, fl_self));
   // 5. out projection + gated residual (g1 = row 2)
   ep.out = h->st.x; ep.ldo = d; ep.bias = B.bo; ep.mod = B.mod; ep.e0 = h->st.e0; ep.gate_row = 2;
   TRY(gemm_act(h, h->o, B.wo, rows, d, d, EPI_RES_GATE, ep));
@@ -409,7 +453,7 @@ sdv2_status run_block(sdv2_handle* h, int bl, int rows, int n_act) {
   const size_t px = size_t(h->Lt) * d;
   aa.q = h->q; aa.K = static_cast<TA*>(h->Kx) + bl * px; aa.V = static_cast<TA*>(h->Vx) + bl * px;
   aa.kv_lane_stride = size_t(h->nb) * px; aa.cross = 1; aa.Lk_cross = h->Lt;
-  TRY(attention(h, aa, n_act));
+  TRY(attention(h, aa, n_act, 4.0 * double(rows) * h->Lt * d));
   // 7. cross out projection, ungated residual
   ep.out = h->st.x; ep.ldo = d; ep.bias = B.bco;
   TRY(gemm_act(h, h->o, B.wco, rows, d, d, EPI_RES, ep));
@@ -477,6 +521,7 @@ sdv2_status tick(sdv2_handle* h, const float* chunk_latent, float* out_latent, i
   if (h->td_ev_used[slot]) CK(cudaEventSynchronize(h->td_ev[slot]));
   TickDesc* tdh = h->td_host + slot;
   h->ctl.plan_call(tdh);
+  h->td_host_cur = tdh;
   CK(cudaMemcpyAsync(h->td_dev, tdh, sizeof(TickDesc), cudaMemcpyHostToDevice, h->stream));
   CK(cudaEventRecord(h->td_ev[slot], h->stream));
   h->td_ev_used[slot] = true;
@@ -490,6 +535,7 @@ sdv2_status tick(sdv2_handle* h, const float* chunk_latent, float* out_latent, i
   h->info.steps = h->n;
   for (int j = 0; j < 8; ++j) h->info.chunk[j] = (j < h->n && tdh->e[j].active) ? tdh->e[j].X : -1;
   h->info.out_chunk = (last && tdh->out_entry >= 0) ? h->ctl.out_chunk(call) : -1;
+  h->info.kernel_launches = h->launches;
   if (out_chunk) *out_chunk = h->info.out_chunk;
 
   if (first) {
@@ -511,6 +557,7 @@ sdv2_status tick(sdv2_handle* h, const float* chunk_latent, float* out_latent, i
     gemv_kernel<float><<<(d + 7) / 8, 256, 0, h->stream>>>(h->gw[G_T1_W], h->gw[G_T1_B], h->emb, h->t1, na, d,
                                                            h->md.freq_dim, 0);
     gemv_kernel<float><<<(d + 7) / 8, 256, 0, h->stream>>>(h->gw[G_T2_W], h->gw[G_T2_B], h->t1, h->st.e, na, d, d, 1);
+    h->launches += 2;
     gemv_kernel<TA><<<(6 * d + 7) / 8, 256, 0, h->stream>>>(static_cast<const TA*>(h->tp_w), h->gw[G_TP_B], h->st.e,
                                                             h->st.e0, na, 6 * d, d, 1);
     CKL();
@@ -768,6 +815,7 @@ sdv2_status sdv2_stage_io_buffers(sdv2_handle* h, int32_t parity, sdv2_stage_io*
 sdv2_status sdv2_get_tick_info(const sdv2_handle* h, sdv2_tick_info* info) {
   if (!h || !info) return SDV2_E_INVALID;
   *info = h->info;
+  info->kernel_launches = h->launches;
   return SDV2_OK;
 }
 
@@ -808,12 +856,39 @@ sdv2_status sdv2_kv_lane(sdv2_handle* h, int32_t local_block, int32_t lane, int3
   return SDV2_OK;
 }
 
+sdv2_status sdv2_profile_enable(sdv2_handle* h, int32_t enable) {
+  if (!h) return SDV2_E_INVALID;
+  CK(cudaStreamSynchronize(h->stream));
+  h->prof = enable != 0;
+  h->prof_recs.clear();
+  h->ev_next = 0;
+  std::memset(&h->prof_acc, 0, sizeof(h->prof_acc));
+  return SDV2_OK;
+}
+
+sdv2_status sdv2_profile_read(sdv2_handle* h, sdv2_profile* out) {
+  if (!h || !out) return SDV2_E_INVALID;
+  CK(cudaStreamSynchronize(h->stream));
+  for (auto& r : h->prof_recs) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, r.a, r.b));
+    h->prof_acc.launches[r.cls] += 1;
+    h->prof_acc.ms[r.cls] += ms;
+    h->prof_acc.flops[r.cls] += r.flops;
+  }
+  h->prof_recs.clear();
+  h->ev_next = 0;
+  *out = h->prof_acc;
+  return SDV2_OK;
+}
+
 sdv2_status sdv2_destroy(sdv2_handle* h) {
   if (!h) return SDV2_E_INVALID;
   if (h->stream_ready || h->td_host) cudaStreamSynchronize(h->stream);
   for (int i = 0; i < kTdRing; ++i)
     if (h->td_host) cudaEventDestroy(h->td_ev[i]);
   if (h->td_host) cudaFreeHost(h->td_host);
+  for (auto e : h->ev_pool) cudaEventDestroy(e);
   delete h;
   return SDV2_OK;
 }

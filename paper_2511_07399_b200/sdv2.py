@@ -60,7 +60,11 @@ class StageIOC(ctypes.Structure):
 
 class TickInfoC(ctypes.Structure):
     _fields_ = [("call", ctypes.c_int64), ("num_entries", ctypes.c_int32), ("steps", ctypes.c_int32),
-                ("chunk", ctypes.c_int64 * 8), ("out_chunk", ctypes.c_int64)]
+                ("chunk", ctypes.c_int64 * 8), ("out_chunk", ctypes.c_int64), ("kernel_launches", ctypes.c_int64)]
+
+
+class ProfileC(ctypes.Structure):
+    _fields_ = [("launches", ctypes.c_int64 * 4), ("ms", ctypes.c_double * 4), ("flops", ctypes.c_double * 4)]
 
 
 class CacheStateC(ctypes.Structure):
@@ -99,7 +103,9 @@ def _declare(lib):
     lib.sdv2_partition.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.c_int32, ctypes.c_int32,
                                    ctypes.c_double, ctypes.c_double, ctypes.POINTER(ctypes.c_int32),
                                    ctypes.POINTER(ctypes.c_double)]
-    for f in ("sdv2_create", "sdv2_reset_stream", "sdv2_set_prompt", "sdv2_denoise_chunk", "sdv2_stage_io_buffers",
+    lib.sdv2_profile_enable.argtypes = [P, ctypes.c_int32]
+    lib.sdv2_profile_read.argtypes = [P, ctypes.POINTER(ProfileC)]
+    for f in ("sdv2_profile_enable", "sdv2_profile_read", "sdv2_create", "sdv2_reset_stream", "sdv2_set_prompt", "sdv2_denoise_chunk", "sdv2_stage_io_buffers",
               "sdv2_get_tick_info", "sdv2_destroy", "sdv2_get_cache_state", "sdv2_set_block_tap", "sdv2_kv_lane",
               "sdv2_partition"):
         getattr(lib, f).restype = ctypes.c_int
@@ -293,7 +299,16 @@ class Stage:
         i = TickInfoC()
         _check(self.L.sdv2_get_tick_info(self.h, ctypes.byref(i)), self.h)
         return {"call": i.call, "num_entries": i.num_entries, "chunk": list(i.chunk)[:i.steps],
-                "out_chunk": i.out_chunk}
+                "out_chunk": i.out_chunk, "kernel_launches": i.kernel_launches}
+
+    def profile_enable(self, on: bool):
+        _check(self.L.sdv2_profile_enable(self.h, 1 if on else 0), self.h)
+
+    def profile_read(self):
+        p = ProfileC()
+        _check(self.L.sdv2_profile_read(self.h, ctypes.byref(p)), self.h)
+        names = ("gemm", "self_attn", "cross_attn", "other")
+        return {names[i]: {"launches": p.launches[i], "ms": p.ms[i], "flops": p.flops[i]} for i in range(4)}
 
     def stage_io(self, parity: int):
         io = StageIOC()
