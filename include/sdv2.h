@@ -203,6 +203,12 @@ sdv2_status sdv2_debug_gemm(const void* A, const void* W, const float* bias, voi
                             int32_t K, int32_t epi, const float* mod, const float* e0, int32_t gate_row, int32_t L,
                             void* stream);
 
+/* Kernel-level test hook: tensor-core attention softmax(q K^T / sqrt(hd)) V for one
+ * query block q [Lq, H*hd] over keys K/V [Lk, H*hd] (bf16, device) -> o [Lq, H*hd]
+ * bf16.  `scratch` is >= 1 KB of device memory.  Synchronises `stream`. */
+sdv2_status sdv2_debug_attention(const void* q, const void* K, const void* V, void* o, int32_t Lq, int32_t Lk,
+                                 int32_t H, int32_t hd, void* scratch, void* stream);
+
 /* ---- host control plane (no GPU needed; also exported by libsdv2_ctl.so) ---- */
 /* Exact min-max contiguous partition of per-block costs over K stages, with extra
  * cost on the first / last stage (P:231–233 DiT block scheduler).  Ties: earlier

@@ -16,9 +16,9 @@
 #include <vector>
 
 #include "../../include/sdv2.h"
-#include "attn_tc.cuh"
 #include "ctl.h"
 #include "gemm_tc.cuh"
+#include "attn_tc.cuh"
 #include "kernels.cuh"
 
 using namespace sdv2;
@@ -132,6 +132,7 @@ struct sdv2_handle {
   sdv2_tick_info info;
   std::string err;
   TmaGemmPlan gplan;
+  AttnPlan aplan;
   int64_t launches = 0;
   TickDesc* td_host_cur = nullptr;
   // profiling (sdv2_profile_enable): event pairs around each launch, per class
@@ -383,14 +384,38 @@ sdv2_status gemm_act(sdv2_handle* h, const void* A, const void* W, int M, int N,
   return gemm_simt<bf16, bf16, bf16>(h, static_cast<const bf16*>(A), static_cast<const bf16*>(W), M, N, K, K, epi, ep);
 }
 
-sdv2_status attention(sdv2_handle* h, const AttnArgs& aa, int Mrows_entries, double flops) {
+sdv2_status attention(sdv2_handle* h, const AttnArgs& aa, int Mrows_entries, double flops, int bl) {
   ProfScope ps(h, aa.cross ? 2 : 1, flops);
   dim3 grid((h->L + 15) / 16, h->H, Mrows_entries);
   if (h->prec == SDV2_FP32) {
     if (h->hd == 64) attn_simt_kernel<float, 64><<<grid, 128, 0, h->stream>>>(aa, h->td_dev);
     else attn_simt_kernel<float, 128><<<grid, 128, 0, h->stream>>>(aa, h->td_dev);
   } else {
-    if (tc_attn_enabled() && ++h->launches) return tc_attention(h->stream, aa, h->td_dev, h->hd, h->H, Mrows_entries, &h->err) ? SDV2_OK : SDV2_E_CUDA;
+    if (tc_attn_enabled()) {
+      ++h->launches;
+      AttnTcArgs ta{};
+      ta.L = h->L;
+      ta.cross = aa.cross;
+      ta.Lk_cross = aa.Lk_cross;
+      ta.scale_log2 = 1.4426950408889634f / sqrtf(float(h->hd));
+      ta.o = aa.o;
+      ta.ldo = aa.ldo;
+      const void *Kb, *Vb;
+      long long kv_rows;
+      if (aa.cross) {
+        Kb = h->Kx; Vb = h->Vx;
+        kv_rows = 2LL * h->nb * h->Lt;
+        ta.kv_row0 = bl * h->Lt;
+        ta.kv_lane_rows = h->nb * h->Lt;
+      } else {
+        Kb = h->Kc; Vb = h->Vc;
+        kv_rows = (long long)h->nb * h->n * h->S * h->L;
+        ta.kv_row0 = bl * h->n * h->S * h->L;
+        ta.kv_lane_rows = h->S * h->L;
+      }
+      return tc_attention(h->stream, h->aplan, aa.q, h->Mmax, Kb, Vb, kv_rows, h->d, h->hd, h->H, Mrows_entries, ta,
+                          h->td_dev, &h->err) ? SDV2_OK : SDV2_E_CUDA;
+    }
     if (h->hd == 64) attn_simt_kernel<bf16, 64><<<grid, 128, 0, h->stream>>>(aa, h->td_dev);
     else attn_simt_kernel<bf16, 128><<<grid, 128, 0, h->stream>>>(aa, h->td_dev);
   }
@@ -439,7 +464,7 @@ sdv2_status run_block(sdv2_handle* h, int bl, int rows, int n_act) {
   aa.o = h->o; aa.ldo = d; aa.L = h->L; aa.cross = 0; aa.scale = 1.f / sqrtf(float(h->hd));
   double fl_self = 0.0;
   for (int j = 0; j < n_act; ++j) fl_self += 4.0 * h->L * double(h->td_host_cur->e[j].nvalid) * h->L * d;
-  TRY(attention(h, aa, n_act, fl_self));
+  TRY(attention(h, aa, n_act, fl_self, bl));
   // 5. out projection + gated residual (g1 = row 2)
   ep.out = h->st.x; ep.ldo = d; ep.bias = B.bo; ep.mod = B.mod; ep.e0 = h->st.e0; ep.gate_row = 2;
   TRY(gemm_act(h, h->o, B.wo, rows, d, d, EPI_RES_GATE, ep));
@@ -453,7 +478,7 @@ sdv2_status run_block(sdv2_handle* h, int bl, int rows, int n_act) {
   const size_t px = size_t(h->Lt) * d;
   aa.q = h->q; aa.K = static_cast<TA*>(h->Kx) + bl * px; aa.V = static_cast<TA*>(h->Vx) + bl * px;
   aa.kv_lane_stride = size_t(h->nb) * px; aa.cross = 1; aa.Lk_cross = h->Lt;
-  TRY(attention(h, aa, n_act, 4.0 * double(rows) * h->Lt * d));
+  TRY(attention(h, aa, n_act, 4.0 * double(rows) * h->Lt * d, bl));
   // 7. cross out projection, ungated residual
   ep.out = h->st.x; ep.ldo = d; ep.bias = B.bco;
   TRY(gemm_act(h, h->o, B.wco, rows, d, d, EPI_RES, ep));
@@ -699,7 +724,10 @@ sdv2_status sdv2_create(const sdv2_model_desc* md, const sdv2_geometry* g, const
     h->err = cudaGetErrorString(cudaGetLastError());
     return fail(SDV2_E_CUDA);
   }
-  if (h->prec == SDV2_BF16 && !tc_gemm_plan(h->gplan, &h->err)) return fail(SDV2_E_CUDA);
+  if (h->prec == SDV2_BF16) {
+    if (!tc_gemm_plan(h->gplan, &h->err)) return fail(SDV2_E_CUDA);
+    attn_plan_init(h->aplan, h->gplan.encode);
+  }
   *out = h;
   return SDV2_OK;
 }
@@ -917,5 +945,40 @@ extern "C" sdv2_status sdv2_debug_gemm(const void* A, const void* W, const float
     fprintf(stderr, "sdv2_debug_gemm: %s\n", err.c_str());
     return SDV2_E_CUDA;
   }
+  return SDV2_OK;
+}
+
+extern "C" sdv2_status sdv2_debug_attention(const void* q, const void* K, const void* V, void* o, int32_t Lq,
+                                            int32_t Lk, int32_t H, int32_t hd, void* scratch, void* stream) {
+  static TmaGemmPlan gp;
+  static AttnPlan ap;
+  static bool ready = false;
+  std::string err;
+  if (!ready) {
+    if (!tc_gemm_plan(gp, &err)) return SDV2_E_CUDA;
+    attn_plan_init(ap, gp.encode);
+    ready = true;
+  }
+  ap.maps.clear();
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  TickDesc tdh;
+  std::memset(&tdh, 0, sizeof(tdh));
+  tdh.n_active = 1;
+  tdh.e[0].active = 1;
+  if (cudaMemcpyAsync(scratch, &tdh, sizeof(tdh), cudaMemcpyHostToDevice, s) != cudaSuccess) return SDV2_E_CUDA;
+  AttnTcArgs ta{};
+  ta.L = Lq;
+  ta.cross = 1;
+  ta.Lk_cross = Lk;
+  ta.scale_log2 = 1.4426950408889634f / sqrtf(float(hd));
+  ta.o = o;
+  ta.ldo = H * hd;
+  ta.kv_row0 = 0;
+  ta.kv_lane_rows = 0;
+  if (!tc_attention(s, ap, q, Lq, K, V, Lk, H * hd, hd, H, 1, ta, static_cast<const TickDesc*>(scratch), &err)) {
+    fprintf(stderr, "sdv2_debug_attention: %s\n", err.c_str());
+    return SDV2_E_CUDA;
+  }
+  cudaStreamSynchronize(s);
   return SDV2_OK;
 }

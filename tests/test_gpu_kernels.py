@@ -57,3 +57,29 @@ def test_tc_gemm(M, N, K, epi):
             ref = x0 + ref
         err = (out - ref).norm() / ref.norm()
         assert err < 1e-5, err
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("Lq,Lk,H,hd", [(16, 48, 2, 64), (1560, 7800, 2, 128), (1560, 512, 3, 128), (128, 128, 1, 128),
+                                        (200, 300, 2, 64), (1024, 5120, 2, 128)])
+def test_tc_attention(Lq, Lk, H, hd):
+    import torch
+    L_ = lib()
+    L_.sdv2_debug_attention.argtypes = [P, P, P, P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                        P, P]
+    L_.sdv2_debug_attention.restype = ctypes.c_int
+    torch.manual_seed(Lq + Lk)
+    q = torch.randn(Lq, H * hd, device="cuda").bfloat16()
+    k = torch.randn(Lk, H * hd, device="cuda").bfloat16()
+    v = torch.randn(Lk, H * hd, device="cuda").bfloat16()
+    o = torch.zeros(Lq, H * hd, device="cuda", dtype=torch.bfloat16)
+    scratch = torch.zeros(4096, dtype=torch.uint8, device="cuda")
+    st = L_.sdv2_debug_attention(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), Lq, Lk, H, hd,
+                                 scratch.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    assert st == 0
+    qh = q.float().view(Lq, H, hd).transpose(0, 1)
+    kh = k.float().view(Lk, H, hd).transpose(0, 1)
+    vh = v.float().view(Lk, H, hd).transpose(0, 1)
+    ref = torch.nn.functional.scaled_dot_product_attention(qh, kh, vh).transpose(0, 1).reshape(Lq, H * hd)
+    err = (o.float() - ref).norm() / ref.norm()
+    assert err < 1.5e-2, err
