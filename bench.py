@@ -228,12 +228,17 @@ def run_ours(args, cfg):
     l0 = stage.tick_info()["kernel_launches"]
     torch.cuda.synchronize()
     outs = 0
+    nvtx = os.environ.get("BENCH_NVTX") == "1"
+    if nvtx:
+        torch.cuda.nvtx.range_push("timed")
     evs[0].record(stream)
     for i in range(args.steps):
         oc = stage.denoise_chunk(dev_chunks[(c + i) % R].data_ptr(), out_dev.data_ptr())
         outs += oc >= 0
         evs[i + 1].record(stream)
     torch.cuda.synchronize()
+    if nvtx:
+        torch.cuda.nvtx.range_pop()
     clocks = clk.stop()
     launches = stage.tick_info()["kernel_launches"] - l0
     c += args.steps

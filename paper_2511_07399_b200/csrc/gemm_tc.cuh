@@ -60,33 +60,41 @@ __device__ __forceinline__ void gemm_epilogue_chunk(const EpiArgs& ep, int r, in
         for (int i = 0; i < 32; ++i) o[i] = from_f<TOut>(EPI == EPI_GELU ? gelu_tanh(acc[i]) : acc[i]);
       }
     } else {
+      // Residual epilogues: issue every load (x row segment, gate vectors through the
+      // read-only path) before the first store, so the 8 x 16 B round trips overlap
+      // instead of serialising on possible aliasing between x and the gate pointers.
       float* x = reinterpret_cast<float*>(ep.out) + size_t(r) * ep.ldo + c0;
+      float4 xv[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) xv[i] = __ldcg(reinterpret_cast<const float4*>(x) + i);
       if (EPI == EPI_RES_GATE) {
         const int e = r / ep.L;
-        const float* gm = ep.mod + ep.gate_row * N + c0;
-        const float* ge = ep.e0 + size_t(e) * 6 * N + ep.gate_row * N + c0;
+        const float4* gm = reinterpret_cast<const float4*>(ep.mod + ep.gate_row * N + c0);
+        const float4* ge = reinterpret_cast<const float4*>(ep.e0 + size_t(e) * 6 * N + ep.gate_row * N + c0);
+        float4 ga[8], gb[8];
 #pragma unroll
-        for (int i = 0; i < 32; i += 4) {
-          const float4 a = *reinterpret_cast<const float4*>(gm + i);
-          const float4 b = *reinterpret_cast<const float4*>(ge + i);
-          float4 xv = *reinterpret_cast<float4*>(x + i);
-          xv.x += (a.x + b.x) * acc[i];
-          xv.y += (a.y + b.y) * acc[i + 1];
-          xv.z += (a.z + b.z) * acc[i + 2];
-          xv.w += (a.w + b.w) * acc[i + 3];
-          *reinterpret_cast<float4*>(x + i) = xv;
+        for (int i = 0; i < 8; ++i) {
+          ga[i] = __ldg(gm + i);
+          gb[i] = __ldg(ge + i);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          xv[i].x += (ga[i].x + gb[i].x) * acc[4 * i];
+          xv[i].y += (ga[i].y + gb[i].y) * acc[4 * i + 1];
+          xv[i].z += (ga[i].z + gb[i].z) * acc[4 * i + 2];
+          xv[i].w += (ga[i].w + gb[i].w) * acc[4 * i + 3];
         }
       } else {
 #pragma unroll
-        for (int i = 0; i < 32; i += 4) {
-          float4 xv = *reinterpret_cast<float4*>(x + i);
-          xv.x += acc[i];
-          xv.y += acc[i + 1];
-          xv.z += acc[i + 2];
-          xv.w += acc[i + 3];
-          *reinterpret_cast<float4*>(x + i) = xv;
+        for (int i = 0; i < 8; ++i) {
+          xv[i].x += acc[4 * i];
+          xv[i].y += acc[4 * i + 1];
+          xv[i].z += acc[4 * i + 2];
+          xv[i].w += acc[4 * i + 3];
         }
       }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) reinterpret_cast<float4*>(x)[i] = xv[i];
     }
   } else {
     for (int i = 0; i < 32; ++i)
