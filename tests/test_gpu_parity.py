@@ -50,3 +50,37 @@ def test_tiny_stream_parity(tiny_ref, prec):
             assert s_rate == pytest.approx(recs[X]["motion"]["s"], rel=1e-6)
             assert dh == pytest.approx(recs[X]["motion"]["d_hat"], rel=1e-6, abs=1e-9)
     print(f"worst block rel-L2 {worst:.3e}")
+
+
+def _truncated(cfg_name, nblocks, num_chunks, prompt_switch=()):
+    """A BASELINE.json config at full width (d, heads, F, latent) truncated to the first
+    `nblocks` DiT blocks (oracle and library both run blocks [0, nblocks) then the head)."""
+    import dataclasses
+    cfg = sg.CONFIGS[cfg_name]
+    md = dataclasses.replace(cfg.model, num_blocks=nblocks)
+    return dataclasses.replace(cfg, model=md, num_chunks=num_chunks, prompt_switch=prompt_switch)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,nblocks,chunks", [("wan13_480p_1step", 2, 6), ("wan13_512_4step", 1, 6)])
+def test_full_width_parity_bf16(name, nblocks, chunks):
+    """1.3B-shaped blocks at 480p (L = 1560, ragged 128-row tiles) and 512x512 with a
+    4-step stream batch: per-block rel-L2 <= 2e-2 vs the fp32 oracle, bit-exact metadata.
+    T_reset is lowered so a RoPE re-base happens inside the run."""
+    import dataclasses
+    cfg = _truncated(name, nblocks, chunks, prompt_switch=(4,))
+    cfg = dataclasses.replace(cfg, stream=dataclasses.replace(cfg.stream, rope_reset_frames=4))
+    W, ch, prompts = tiny_inputs(cfg, extra=cfg.geom.steps - 1, segment=2)
+    recs = run_stream(cfg, W, ch, prompts, dtype=np.float32, tap=True)
+    outs, taps, meta = run_gpu(cfg, W, ch, prompts, SDV2_BF16)
+    worst = 0.0
+    for (X, j), tl in taps.items():
+        for b in range(nblocks):
+            err = rel_l2(tl[b], recs[X]["entries"][j]["taps"][b])
+            worst = max(worst, err)
+            assert err <= 2e-2, (X, j, b, err)
+    for X in range(cfg.num_chunks):
+        assert rel_l2(outs[X], recs[X]["out"]) <= 2e-2
+    for (X, j), (slots, _, _) in meta.items():
+        assert slots == {s: (t, p[0]) for s, (t, p) in recs[X]["lane_state"][(0, j)].items()}
+    print(f"{name}: worst block rel-L2 {worst:.3e}")
