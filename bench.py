@@ -196,6 +196,7 @@ def run_ours(args, cfg):
     t_gen = time.time() - t0
     stage = Stage(md, g, W, precision=SDV2_BF16, device=local)
     stream = stage.stream
+    torch.cuda.set_stream(stream)      # everything below is ordered on the stage's stream
     prompt = sg.gen_prompt(md, 0)
     ls = sg.LatentStream(md.latent_channels, g.latent_h, g.latent_w, seed=1)
     R = 16

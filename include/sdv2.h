@@ -190,6 +190,9 @@ sdv2_status sdv2_set_block_tap(sdv2_handle* h, float* per_block_out);
 sdv2_status sdv2_kv_lane(sdv2_handle* h, int32_t local_block, int32_t lane, int32_t which,
                          void** ptr, size_t* elems);
 
+/* CUDA-graph replay of the per-call device work (default on; keyed by the number of
+ * active entries and the call parity; not used while profiling or tapping). */
+sdv2_status sdv2_set_graphs(sdv2_handle* h, int32_t enable);
 /* Enable (1, resets the accumulators) or disable (0) per-class event timing. */
 sdv2_status sdv2_profile_enable(sdv2_handle* h, int32_t enable);
 /* Synchronises the stream and returns the accumulated per-class times. */

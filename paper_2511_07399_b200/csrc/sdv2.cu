@@ -135,6 +135,10 @@ struct sdv2_handle {
   AttnPlan aplan;
   int64_t launches = 0;
   TickDesc* td_host_cur = nullptr;
+  // CUDA graphs of the call body, keyed by (active entries, call parity)
+  bool graphs = true;
+  cudaGraphExec_t graph_exec[2 * (kMaxSteps + 1)] = {};
+  int64_t graph_launches[2 * (kMaxSteps + 1)] = {};
   // profiling (sdv2_profile_enable): event pairs around each launch, per class
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -539,37 +543,19 @@ sdv2_status set_prompt_common(sdv2_handle* h, const float* prompt_host, int ver)
   return SDV2_OK;
 }
 
+// Device work of one call that depends only on (active entries, call parity): the
+// part replayed from a CUDA graph.
 template <typename TA>
-sdv2_status tick(sdv2_handle* h, const float* chunk_latent, float* out_latent, int64_t* out_chunk) {
-  const int64_t call = h->ctl.calls();
-  const int slot = int(call % kTdRing);
-  if (h->td_ev_used[slot]) CK(cudaEventSynchronize(h->td_ev[slot]));
-  TickDesc* tdh = h->td_host + slot;
-  h->ctl.plan_call(tdh);
-  h->td_host_cur = tdh;
-  CK(cudaMemcpyAsync(h->td_dev, tdh, sizeof(TickDesc), cudaMemcpyHostToDevice, h->stream));
-  CK(cudaEventRecord(h->td_ev[slot], h->stream));
-  h->td_ev_used[slot] = true;
-  const int na = tdh->n_active;
+sdv2_status tick_body(sdv2_handle* h, int na, int par) {
   const int rows = na * h->L;
-  const int par = int(call & 1);
   const bool first = h->rank == 0, last = h->rank == h->K - 1;
-  // fill tick info (host, no sync)
-  h->info.call = call;
-  h->info.num_entries = na;
-  h->info.steps = h->n;
-  for (int j = 0; j < 8; ++j) h->info.chunk[j] = (j < h->n && tdh->e[j].active) ? tdh->e[j].X : -1;
-  h->info.out_chunk = (last && tdh->out_entry >= 0) ? h->ctl.out_chunk(call) : -1;
-  h->info.kernel_launches = h->launches;
-  if (out_chunk) *out_chunk = h->info.out_chunk;
-
   if (first) {
-    CK(cudaMemcpyAsync(h->lat_in, chunk_latent, size_t(h->CTHW) * 4, cudaMemcpyDefault, h->stream));
     noise_ctl_kernel<<<1, 1024, 0, h->stream>>>(h->lat_in, h->prev_frame, h->ctrl, h->st.lat, h->st.sig, h->st.sign,
                                                h->td_dev, h->scfg, h->CTHW, h->hh * h->ww, h->T);
     CKL();
     if (na > 1) {
-      const float* rin = h->K == 1 ? h->ring[1][(call + 1) & 1] : h->ring[0][par];
+      // K = 1: the ring packet of call c-1 was written to ring[1][(c-1)&1] == ring[1][par^1]
+      const float* rin = h->K == 1 ? h->ring[1][par ^ 1] : h->ring[0][par];
       assemble_kernel<<<dim3(64, h->n - 1), 256, 0, h->stream>>>(rin, h->st.lat, h->td_dev, h->n, h->CTHW);
       CKL();
     }
@@ -589,6 +575,44 @@ sdv2_status tick(sdv2_handle* h, const float* chunk_latent, float* out_latent, i
   } else {
     CK(cudaMemcpyAsync(h->packet_base, h->act_io[0][par], h->st.bytes, cudaMemcpyDeviceToDevice, h->stream));
   }
+  for (int b = 0; b < h->nb; ++b) TRY(run_block<TA>(h, b, rows, na));
+  if (!last) {
+    CK(cudaMemcpyAsync(h->act_io[1][par], h->packet_base, h->st.bytes, cudaMemcpyDeviceToDevice, h->stream));
+  } else {
+    head_kernel<<<(rows + 7) / 8, 256, 8 * h->d * 4, h->stream>>>(
+        h->st.x, h->st.e, h->gw[G_HEAD_MOD], h->gw[G_HEAD_W], h->gw[G_HEAD_B], h->st.lat, h->st.sig, h->st.sign,
+        h->out_stage, h->ring[1][par], h->td_dev, rows, h->d, h->L, h->C, h->T, h->hh, h->ww, h->n, h->md.eps,
+        h->md.norm_center, h->scfg.seed);
+    CKL();
+  }
+  return SDV2_OK;
+}
+
+template <typename TA>
+sdv2_status tick(sdv2_handle* h, const float* chunk_latent, float* out_latent, int64_t* out_chunk) {
+  const int64_t call = h->ctl.calls();
+  const int slot = int(call % kTdRing);
+  if (h->td_ev_used[slot]) CK(cudaEventSynchronize(h->td_ev[slot]));
+  TickDesc* tdh = h->td_host + slot;
+  h->ctl.plan_call(tdh);
+  h->td_host_cur = tdh;
+  CK(cudaMemcpyAsync(h->td_dev, tdh, sizeof(TickDesc), cudaMemcpyHostToDevice, h->stream));
+  CK(cudaEventRecord(h->td_ev[slot], h->stream));
+  h->td_ev_used[slot] = true;
+  const int na = tdh->n_active;
+  const int par = int(call & 1);
+  const bool first = h->rank == 0, last = h->rank == h->K - 1;
+  // tick info (host, no sync: the schedule is deterministic)
+  h->info.call = call;
+  h->info.num_entries = na;
+  h->info.steps = h->n;
+  for (int j = 0; j < 8; ++j) h->info.chunk[j] = (j < h->n && tdh->e[j].active) ? tdh->e[j].X : -1;
+  h->info.out_chunk = (last && tdh->out_entry >= 0) ? h->ctl.out_chunk(call) : -1;
+  if (out_chunk) *out_chunk = h->info.out_chunk;
+
+  if (first) CK(cudaMemcpyAsync(h->lat_in, chunk_latent, size_t(h->CTHW) * 4, cudaMemcpyDefault, h->stream));
+  // RoPE re-base (rare: once every T_reset frames) of every local block's ring slots of
+  // the re-basing lanes, before any block of this call writes or attends (R3).
   bool any_rebase = false;
   for (int j = 0; j < h->n; ++j) any_rebase |= (tdh->e[j].active && tdh->e[j].rebase);
   if (any_rebase) {
@@ -596,19 +620,33 @@ sdv2_status tick(sdv2_handle* h, const float* chunk_latent, float* out_latent, i
                                                                h->S, h->m, h->W, h->L, h->d, h->hd, h->T_reset);
     CKL();
   }
-  for (int b = 0; b < h->nb; ++b) TRY(run_block<TA>(h, b, rows, na));
-  if (!last) {
-    CK(cudaMemcpyAsync(h->act_io[1][par], h->packet_base, h->st.bytes, cudaMemcpyDeviceToDevice, h->stream));
+  const bool use_graph = h->graphs && !h->prof && !h->tap && h->stream != nullptr;
+  if (use_graph) {
+    const int key = na * 2 + par;
+    if (!h->graph_exec[key]) {
+      const int64_t l0 = h->launches;
+      CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+      sdv2_status s = tick_body<TA>(h, na, par);
+      cudaGraph_t g = nullptr;
+      cudaError_t e = cudaStreamEndCapture(h->stream, &g);
+      if (s != SDV2_OK) return s;
+      if (e != cudaSuccess) {
+        h->err = std::string("graph capture: ") + cudaGetErrorString(e);
+        return SDV2_E_CUDA;
+      }
+      CK(cudaGraphInstantiate(&h->graph_exec[key], g, 0));
+      cudaGraphDestroy(g);
+      h->graph_launches[key] = h->launches - l0;
+      h->launches = l0;
+    }
+    CK(cudaGraphLaunch(h->graph_exec[key], h->stream));
+    h->launches += h->graph_launches[key];
   } else {
-    float* rout = h->K == 1 ? h->ring[1][call & 1] : h->ring[1][par];
-    head_kernel<<<(rows + 7) / 8, 256, 8 * h->d * 4, h->stream>>>(
-        h->st.x, h->st.e, h->gw[G_HEAD_MOD], h->gw[G_HEAD_W], h->gw[G_HEAD_B], h->st.lat, h->st.sig, h->st.sign,
-        h->out_stage, rout, h->td_dev, rows, h->d, h->L, h->C, h->T, h->hh, h->ww, h->n, h->md.eps,
-        h->md.norm_center, h->scfg.seed);
-    CKL();
-    if (tdh->out_entry >= 0 && out_latent)
-      CK(cudaMemcpyAsync(out_latent, h->out_stage, size_t(h->CTHW) * 4, cudaMemcpyDefault, h->stream));
+    TRY(tick_body<TA>(h, na, par));
   }
+  if (last && tdh->out_entry >= 0 && out_latent)
+    CK(cudaMemcpyAsync(out_latent, h->out_stage, size_t(h->CTHW) * 4, cudaMemcpyDefault, h->stream));
+  h->info.kernel_launches = h->launches;
   return SDV2_OK;
 }
 
@@ -884,6 +922,12 @@ sdv2_status sdv2_kv_lane(sdv2_handle* h, int32_t local_block, int32_t lane, int3
   return SDV2_OK;
 }
 
+sdv2_status sdv2_set_graphs(sdv2_handle* h, int32_t enable) {
+  if (!h) return SDV2_E_INVALID;
+  h->graphs = enable != 0;
+  return SDV2_OK;
+}
+
 sdv2_status sdv2_profile_enable(sdv2_handle* h, int32_t enable) {
   if (!h) return SDV2_E_INVALID;
   CK(cudaStreamSynchronize(h->stream));
@@ -917,6 +961,8 @@ sdv2_status sdv2_destroy(sdv2_handle* h) {
     if (h->td_host) cudaEventDestroy(h->td_ev[i]);
   if (h->td_host) cudaFreeHost(h->td_host);
   for (auto e : h->ev_pool) cudaEventDestroy(e);
+  for (auto& g : h->graph_exec)
+    if (g) cudaGraphExecDestroy(g);
   delete h;
   return SDV2_OK;
 }

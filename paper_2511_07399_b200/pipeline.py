@@ -134,17 +134,21 @@ def stage_io_tensors(stage, workspace):
 def run_pipelined(stage, transport: StageTransport, chunks, out_cb, num_calls: int, on_call=None):
     """Drive num_calls stage-ticks on this rank.  chunks(c) -> device/host pointer of the
     chunk admitted at call c (rank 0 only); out_cb(c) -> output pointer (last rank)."""
-    transport.post(-1, num_calls)
-    outs = []
-    for c in range(num_calls):
+    import contextlib
+    stream = getattr(stage, "stream", None)
+    ctx = transport.torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()
+    with ctx:   # NCCL waits and host-staging copies are ordered on the stage's stream
+        transport.post(-1, num_calls)
+        outs = []
+        for c in range(num_calls):
+            transport.wait()
+            if on_call:
+                on_call(c)
+            oc = stage.denoise_chunk(chunks(c) if transport.rank == 0 else None,
+                                     out_cb(c) if transport.rank == transport.world - 1 else None)
+            outs.append(oc)
+            transport.post(c, num_calls)
         transport.wait()
-        if on_call:
-            on_call(c)
-        oc = stage.denoise_chunk(chunks(c) if transport.rank == 0 else None,
-                                 out_cb(c) if transport.rank == transport.world - 1 else None)
-        outs.append(oc)
-        transport.post(c, num_calls)
-    transport.wait()
     return outs
 
 

@@ -104,6 +104,8 @@ def _declare(lib):
                                    ctypes.c_double, ctypes.c_double, ctypes.POINTER(ctypes.c_int32),
                                    ctypes.POINTER(ctypes.c_double)]
     lib.sdv2_profile_enable.argtypes = [P, ctypes.c_int32]
+    lib.sdv2_set_graphs.argtypes = [P, ctypes.c_int32]
+    lib.sdv2_set_graphs.restype = ctypes.c_int
     lib.sdv2_profile_read.argtypes = [P, ctypes.POINTER(ProfileC)]
     for f in ("sdv2_profile_enable", "sdv2_profile_read", "sdv2_create", "sdv2_reset_stream", "sdv2_set_prompt", "sdv2_denoise_chunk", "sdv2_stage_io_buffers",
               "sdv2_get_tick_info", "sdv2_destroy", "sdv2_get_cache_state", "sdv2_set_block_tap", "sdv2_kv_lane",
@@ -247,7 +249,8 @@ class Stage:
             raise SDV2Error("invalid model / geometry descriptor")
         self.device = device
         self.workspace = torch.empty(nbytes + 1024, dtype=torch.uint8, device=f"cuda:{device}")
-        self.stream = stream if stream is not None else torch.cuda.current_stream(device)
+        # a dedicated (capturable) stream: per-call device work is replayed from CUDA graphs
+        self.stream = stream if stream is not None else torch.cuda.Stream(device)
         names = list(GLOBAL_ORDER) + [f"blocks.{b}.{t}" for b in range(b0, b1) for t in BLOCK_ORDER]
         keep = []
         ptrs = (ctypes.c_void_p * len(names))()
@@ -291,6 +294,9 @@ class Stage:
         """chunk_ptr / out_ptr: raw host or device addresses (or None).  Returns the chunk
         index emitted into out_ptr, or -1."""
         oc = ctypes.c_int64(-1)
+        cur = self.torch.cuda.current_stream(self.device)
+        if cur != self.stream:      # order after the caller's producers on its stream
+            self.stream.wait_stream(cur)
         _check(self.L.sdv2_denoise_chunk(self.h, ctypes.c_void_p(chunk_ptr) if chunk_ptr else None,
                                          ctypes.c_void_p(out_ptr) if out_ptr else None, ctypes.byref(oc)), self.h)
         return oc.value
@@ -300,6 +306,9 @@ class Stage:
         _check(self.L.sdv2_get_tick_info(self.h, ctypes.byref(i)), self.h)
         return {"call": i.call, "num_entries": i.num_entries, "chunk": list(i.chunk)[:i.steps],
                 "out_chunk": i.out_chunk, "kernel_launches": i.kernel_launches}
+
+    def set_graphs(self, on: bool):
+        _check(self.L.sdv2_set_graphs(self.h, 1 if on else 0), self.h)
 
     def profile_enable(self, on: bool):
         _check(self.L.sdv2_profile_enable(self.h, 1 if on else 0), self.h)

@@ -14,10 +14,11 @@ def tiny_inputs(cfg, extra=0, segment=3):
     return W, chunks, prompts
 
 
-def run_gpu(cfg, W, chunks, prompts, prec, tap=True, blocks=None, stream_desc=None):
+def run_gpu(cfg, W, chunks, prompts, prec, tap=True, blocks=None, stream_desc=None, graphs=True):
     import torch
     md, g = cfg.model, cfg.geom
     stage = Stage(md, g, W, precision=prec)
+    stage.set_graphs(graphs)
     sd = stream_desc or cfg.stream
     stage.reset_stream(sd, prompts[0])
     L = g.tokens_per_chunk(md)

@@ -84,3 +84,18 @@ def test_full_width_parity_bf16(name, nblocks, chunks):
     for (X, j), (slots, _, _) in meta.items():
         assert slots == {s: (t, p[0]) for s, (t, p) in recs[X]["lane_state"][(0, j)].items()}
     print(f"{name}: worst block rel-L2 {worst:.3e}")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("prec", [SDV2_FP32, SDV2_BF16])
+def test_graph_replay_equals_eager(tiny_ref, prec):
+    """CUDA-graph replay of the call body (the default, used by bench) is bitwise the
+    eager launch sequence, and matches the oracle."""
+    cfg, W, chunks, prompts, recs = tiny_ref
+    g_outs, _, _ = run_gpu(cfg, W, chunks, prompts, prec, tap=False, graphs=True)
+    e_outs, _, _ = run_gpu(cfg, W, chunks, prompts, prec, tap=False, graphs=False)
+    assert sorted(g_outs) == sorted(e_outs) and len(g_outs) >= cfg.num_chunks
+    for X in g_outs:
+        assert np.array_equal(g_outs[X], e_outs[X]), X
+    for X in range(cfg.num_chunks):
+        assert rel_l2(g_outs[X], recs[X]["out"]) <= TOL[prec]
