@@ -254,6 +254,7 @@ inline bool tc_gemm_plan(TmaGemmPlan& p, std::string* err) {
   cudaFuncSetAttribute(gemm_tc_kernel<EPI_GELU, bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmem);
   cudaFuncSetAttribute(gemm_tc_kernel<EPI_RES_GATE, bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmem);
   cudaFuncSetAttribute(gemm_tc_kernel<EPI_RES, bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmem);
+  cudaFuncSetAttribute(gemm_tc_kernel<EPI_STORE, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmem);
   return true;
 }
 
@@ -320,6 +321,7 @@ inline bool tc_gemm(cudaStream_t s, TmaGemmPlan& p, const void* A, const void* W
     case EPI_STORE: gemm_tc_kernel<EPI_STORE, bf16><<<grid, 256, kGemmSmem, s>>>(*ma, *mb, M, N, K, BN, ep); break;
     case EPI_GELU: gemm_tc_kernel<EPI_GELU, bf16><<<grid, 256, kGemmSmem, s>>>(*ma, *mb, M, N, K, BN, ep); break;
     case EPI_RES_GATE: gemm_tc_kernel<EPI_RES_GATE, bf16><<<grid, 256, kGemmSmem, s>>>(*ma, *mb, M, N, K, BN, ep); break;
+    case EPI_STORE_F32: gemm_tc_kernel<EPI_STORE, float><<<grid, 256, kGemmSmem, s>>>(*ma, *mb, M, N, K, BN, ep); break;
     default: gemm_tc_kernel<EPI_RES, bf16><<<grid, 256, kGemmSmem, s>>>(*ma, *mb, M, N, K, BN, ep); break;
   }
   cudaError_t e = cudaGetLastError();

@@ -19,6 +19,7 @@
 #include "ctl.h"
 #include "gemm_tc.cuh"
 #include "attn_tc.cuh"
+#include "elem.cuh"
 #include "kernels.cuh"
 
 using namespace sdv2;
@@ -101,6 +102,9 @@ struct sdv2_handle {
   float* out_stage;           // [CTHW]
   CtrlState* ctrl;
   float* emb;                 // [n, 256]
+  float* u;                   // patchified tokens [Mmax, 4C] fp32
+  float* yh;                  // head output [Mmax, 4C] fp32
+  void* head_w_tw;            // head weight [4C, d] TW
   float* t1;                  // [n, d]
   void* a;                    // [Mmax, d] TA
   void* qkv;                  // [Mmax, 3d] TA
@@ -199,6 +203,7 @@ size_t carve(sdv2_handle* h, void* base) {
   h->gw[G_HEAD_MOD] = cv.take<float>(2 * d);
   h->gw[G_HEAD_W] = cv.take<float>(size_t(P) * d);
   h->gw[G_HEAD_B] = cv.take<float>(P);
+  h->head_w_tw = tw(size_t(P) * d);
   h->bw.assign(h->nb, BlockW{});
   for (int b = 0; b < h->nb; ++b) {
     BlockW& B = h->bw[b];
@@ -239,6 +244,8 @@ size_t carve(sdv2_handle* h, void* base) {
   h->out_stage = cv.take<float>(h->CTHW);
   h->ctrl = cv.take<CtrlState>(1);
   h->emb = cv.take<float>(size_t(h->n) * h->md.freq_dim);
+  h->u = cv.take<float>(size_t(h->Mmax) * h->P);
+  h->yh = cv.take<float>(size_t(h->Mmax) * h->P);
   h->t1 = cv.take<float>(size_t(h->n) * d);
   // activation scratch, aliased by the weight staging buffer during create
   {
@@ -299,7 +306,7 @@ sdv2_status fill_dims(sdv2_handle* h, const sdv2_model_desc* md, const sdv2_geom
   h->n = g->steps; h->m = g->sink_chunks; h->W = g->window_chunks; h->S = h->m + h->W;
   h->Lt = md->text_len; h->Dt = md->text_dim;
   h->CTHW = h->C * h->T * h->hh * h->ww;
-  if (h->CTHW % 4) return SDV2_E_SHAPE;
+  if (h->CTHW % 4 || (h->hh * h->ww) % 4) return SDV2_E_SHAPE;
   h->Mmax = h->n * h->L;
   h->P = 4 * h->C;
   const int c = h->hd / 2;
@@ -428,13 +435,34 @@ sdv2_status attention(sdv2_handle* h, const AttnArgs& aa, int Mrows_entries, dou
 }
 
 template <typename TA>
-sdv2_status launch_norm(sdv2_handle* h, int rows, int mode, const float* mod, int sc_row, int sh_row,
-                        const float* gamma, const float* beta) {
-  norm_mod_kernel<TA><<<(rows + 7) / 8, 256, 0, h->stream>>>(h->st.x, static_cast<TA*>(h->a), rows, h->d, h->L, mode,
-                                                             mod, h->st.e0, sc_row, sh_row, gamma, beta, h->md.eps,
-                                                             h->md.norm_center);
+sdv2_status launch_norm_args(sdv2_handle* h, int rows, const ModArgs& m) {
+  const int nv = (h->d / 4 + kRowThreads - 1) / kRowThreads;
+  if (nv <= 4)
+    norm_mod2_kernel<TA, 4><<<(rows + 1) / 2, 256, 0, h->stream>>>(h->st.x, static_cast<TA*>(h->a), rows, h->d, h->L,
+                                                                    m, h->md.eps, h->md.norm_center);
+  else
+    norm_mod2_kernel<TA, 16><<<(rows + 1) / 2, 256, 0, h->stream>>>(h->st.x, static_cast<TA*>(h->a), rows, h->d, h->L,
+                                                                     m, h->md.eps, h->md.norm_center);
   CKL();
   return SDV2_OK;
+}
+
+// adaLN (mode 0: shift row sh_row, scale row sc_row of mod + e0[e]) or affine (mode 1).
+template <typename TA>
+sdv2_status launch_norm(sdv2_handle* h, int rows, int mode, const float* mod, int sc_row, int sh_row,
+                        const float* gamma, const float* beta) {
+  ModArgs m{};
+  if (mode == 0) {
+    m.modA = mod; m.sc_off = sc_row * h->d; m.sh_off = sh_row * h->d;
+    m.eA = h->st.e0; m.estride = 6 * h->d; m.esc_off = sc_row * h->d; m.esh_off = sh_row * h->d;
+    m.a0 = 1.f;
+  } else {
+    m.modA = gamma; m.sc_off = 0;
+    m.sh_off = int(beta - gamma);   // beta follows gamma in the workspace (carve order)
+    m.eA = nullptr;
+    m.a0 = 0.f;
+  }
+  return launch_norm_args<TA>(h, rows, m);
 }
 
 #define TRY(x)                        \
@@ -458,10 +486,18 @@ sdv2_status run_block(sdv2_handle* h, int bl, int rows, int n_act) {
   const size_t lane_elems = size_t(h->n) * h->S * h->L * d;
   TA* Kb = static_cast<TA*>(h->Kc) + bl * lane_elems;
   TA* Vb = static_cast<TA*>(h->Vc) + bl * lane_elems;
-  qkv_post_kernel<TA><<<(rows + 7) / 8, 256, 0, h->stream>>>(static_cast<const TA*>(h->qkv), static_cast<TA*>(h->q), Kb,
-                                                             Vb, B.gq, B.gk, h->td_dev, h->rt, rows, d, h->hd, h->L,
-                                                             h->hn, h->wn, h->T, h->S, h->md.eps);
-  CKL();
+  {
+    const int units_pt = (d / (16 / int(sizeof(TA))) + kRowThreads - 1) / kRowThreads;
+    if (units_pt <= 2)
+      qkv_post2_kernel<TA, 2><<<(rows + 1) / 2, 256, 0, h->stream>>>(
+          static_cast<const TA*>(h->qkv), static_cast<TA*>(h->q), Kb, Vb, B.gq, B.gk, h->td_dev, h->rt, rows, d, h->hd,
+          h->L, h->hn, h->wn, h->T, h->S, h->md.eps);
+    else
+      qkv_post2_kernel<TA, 8><<<(rows + 1) / 2, 256, 0, h->stream>>>(
+          static_cast<const TA*>(h->qkv), static_cast<TA*>(h->q), Kb, Vb, B.gq, B.gk, h->td_dev, h->rt, rows, d, h->hd,
+          h->L, h->hn, h->wn, h->T, h->S, h->md.eps);
+    CKL();
+  }
   // self-attention over the lane's valid prefix
   AttnArgs aa{};
   aa.q = h->q; aa.ldq = d; aa.K = Kb; aa.V = Vb; aa.kv_lane_stride = size_t(h->S) * h->L * d; aa.ldk = d;
@@ -476,9 +512,14 @@ sdv2_status run_block(sdv2_handle* h, int bl, int rows, int n_act) {
   TRY(launch_norm<TA>(h, rows, 1, nullptr, 0, 0, B.n3g, B.n3b));
   ep.out = h->q; ep.ldo = d; ep.bias = B.bcq;
   TRY(gemm_act(h, h->a, B.wcq, rows, d, d, EPI_STORE, ep));
-  rms_rows_kernel<TA, TA><<<(rows + 7) / 8, 256, 0, h->stream>>>(static_cast<TA*>(h->q), static_cast<TA*>(h->q), B.gcq,
-                                                                  rows, d, d, h->md.eps);
-  CKL();
+  {
+    const int units_pt = (d / (16 / int(sizeof(TA))) + kRowThreads - 1) / kRowThreads;
+    if (units_pt <= 2)
+      rms_rows2_kernel<TA, 2><<<(rows + 1) / 2, 256, 0, h->stream>>>(static_cast<TA*>(h->q), B.gcq, rows, d, h->md.eps);
+    else
+      rms_rows2_kernel<TA, 8><<<(rows + 1) / 2, 256, 0, h->stream>>>(static_cast<TA*>(h->q), B.gcq, rows, d, h->md.eps);
+    CKL();
+  }
   const size_t px = size_t(h->Lt) * d;
   aa.q = h->q; aa.K = static_cast<TA*>(h->Kx) + bl * px; aa.V = static_cast<TA*>(h->Vx) + bl * px;
   aa.kv_lane_stride = size_t(h->nb) * px; aa.cross = 1; aa.Lk_cross = h->Lt;
@@ -550,8 +591,12 @@ sdv2_status tick_body(sdv2_handle* h, int na, int par) {
   const int rows = na * h->L;
   const bool first = h->rank == 0, last = h->rank == h->K - 1;
   if (first) {
-    noise_ctl_kernel<<<1, 1024, 0, h->stream>>>(h->lat_in, h->prev_frame, h->ctrl, h->st.lat, h->st.sig, h->st.sign,
-                                               h->td_dev, h->scfg, h->CTHW, h->hh * h->ww, h->T);
+    // motion-aware noise controller then the step-0 blend on all SMs
+    motion_kernel<<<1, 1024, 0, h->stream>>>(h->lat_in, h->prev_frame, h->ctrl, h->st.sig, h->st.sign, h->td_dev,
+                                            h->scfg, h->CTHW, h->hh * h->ww, h->T);
+    CKL();
+    blend_kernel<<<(h->CTHW + 255) / 256, 256, 0, h->stream>>>(h->lat_in, h->st.lat, h->st.sig, h->td_dev,
+                                                               h->scfg.seed, h->CTHW);
     CKL();
     if (na > 1) {
       // K = 1: the ring packet of call c-1 was written to ring[1][(c-1)&1] == ring[1][par^1]
@@ -559,18 +604,26 @@ sdv2_status tick_body(sdv2_handle* h, int na, int par) {
       assemble_kernel<<<dim3(64, h->n - 1), 256, 0, h->stream>>>(rin, h->st.lat, h->td_dev, h->n, h->CTHW);
       CKL();
     }
-    patch_embed_kernel<<<(rows + 15) / 16, 256, 16 * h->P * 4, h->stream>>>(
-        h->st.lat, h->gw[G_PATCH_W], h->gw[G_PATCH_B], h->st.x, rows, h->L, h->d, h->C, h->T, h->hh, h->ww);
+    // patchify + patch embedding (C.1): x = u W_pe^T + b_pe, fp32 (K = 4C)
+    patchify_kernel<<<(rows * h->P + 255) / 256, 256, 0, h->stream>>>(h->st.lat, h->u, rows, h->L, h->C, h->T, h->hh,
+                                                                       h->ww);
     CKL();
+    {
+      EpiArgs ep{};
+      ep.out = h->st.x; ep.ldo = h->d; ep.bias = h->gw[G_PATCH_B]; ep.L = h->L;
+      TRY((gemm_simt<float, float, float>(h, h->u, h->gw[G_PATCH_W], rows, h->d, h->P, h->P, EPI_STORE, ep)));
+    }
     sinusoid_kernel<<<na, 128, 0, h->stream>>>(h->st.sig, h->emb, na, h->md.freq_dim);
     CKL();
     const int d = h->d;
-    gemv_kernel<float><<<(d + 7) / 8, 256, 0, h->stream>>>(h->gw[G_T1_W], h->gw[G_T1_B], h->emb, h->t1, na, d,
-                                                           h->md.freq_dim, 0);
-    gemv_kernel<float><<<(d + 7) / 8, 256, 0, h->stream>>>(h->gw[G_T2_W], h->gw[G_T2_B], h->t1, h->st.e, na, d, d, 1);
+    // time MLP (C.2): e = W_t2 SiLU(W_t1 emb + b) + b; e0 = W_tp SiLU(e) + b
+    gemv2_kernel<float><<<(d + 31) / 32, 256, size_t(na) * h->md.freq_dim * 4, h->stream>>>(
+        h->gw[G_T1_W], h->gw[G_T1_B], h->emb, h->t1, na, d, h->md.freq_dim, 0);
+    gemv2_kernel<float><<<(d + 31) / 32, 256, size_t(na) * d * 4, h->stream>>>(h->gw[G_T2_W], h->gw[G_T2_B], h->t1,
+                                                                               h->st.e, na, d, d, 1);
     h->launches += 2;
-    gemv_kernel<TA><<<(6 * d + 7) / 8, 256, 0, h->stream>>>(static_cast<const TA*>(h->tp_w), h->gw[G_TP_B], h->st.e,
-                                                            h->st.e0, na, 6 * d, d, 1);
+    gemv2_kernel<TA><<<(6 * d + 31) / 32, 256, size_t(na) * d * 4, h->stream>>>(
+        static_cast<const TA*>(h->tp_w), h->gw[G_TP_B], h->st.e, h->st.e0, na, 6 * d, d, 1);
     CKL();
   } else {
     CK(cudaMemcpyAsync(h->packet_base, h->act_io[0][par], h->st.bytes, cudaMemcpyDeviceToDevice, h->stream));
@@ -579,10 +632,25 @@ sdv2_status tick_body(sdv2_handle* h, int na, int par) {
   if (!last) {
     CK(cudaMemcpyAsync(h->act_io[1][par], h->packet_base, h->st.bytes, cudaMemcpyDeviceToDevice, h->stream));
   } else {
-    head_kernel<<<(rows + 7) / 8, 256, 8 * h->d * 4, h->stream>>>(
-        h->st.x, h->st.e, h->gw[G_HEAD_MOD], h->gw[G_HEAD_W], h->gw[G_HEAD_B], h->st.lat, h->st.sig, h->st.sign,
-        h->out_stage, h->ring[1][par], h->td_dev, rows, h->d, h->L, h->C, h->T, h->hh, h->ww, h->n, h->md.eps,
-        h->md.norm_center, h->scfg.seed);
+    // head (C.7): a = N(x)(1 + mod_h[1] + e) + mod_h[0] + e; y = a W_h^T + b_h (fp32 out);
+    // then unpatchify + x0 + output / re-noise (C.8, O5)
+    ModArgs m{};
+    m.modA = h->gw[G_HEAD_MOD]; m.sc_off = h->d; m.sh_off = 0;
+    m.eA = h->st.e; m.estride = h->d; m.esc_off = 0; m.esh_off = 0; m.a0 = 1.f;
+    TRY(launch_norm_args<TA>(h, rows, m));
+    EpiArgs ep{};
+    ep.out = h->yh; ep.ldo = h->P; ep.bias = h->gw[G_HEAD_B]; ep.L = h->L;
+    if (h->prec == SDV2_FP32) {
+      TRY((gemm_simt<float, float, float>(h, static_cast<const float*>(h->a), h->gw[G_HEAD_W], rows, h->P, h->d,
+                                          h->d, EPI_STORE, ep)));
+    } else {
+      ++h->launches;
+      if (!tc_gemm(h->stream, h->gplan, h->a, h->head_w_tw, rows, h->P, h->d, EPI_STORE_F32, ep, &h->err))
+        return SDV2_E_CUDA;
+    }
+    flow_kernel<<<(na * h->CTHW + 255) / 256, 256, 0, h->stream>>>(
+        h->yh, h->st.lat, h->st.sig, h->st.sign, h->out_stage, h->ring[1][par], h->td_dev, na, h->L, h->C, h->T,
+        h->hh, h->ww, h->n, h->scfg.seed);
     CKL();
   }
   return SDV2_OK;
@@ -731,6 +799,7 @@ sdv2_status sdv2_create(const sdv2_model_desc* md, const sdv2_geometry* g, const
   for (int i = 0; i < kNumGlobal; ++i) {
     if (i == G_TP_W) s = load_tensor(h, T[i], h->tp_w, sizes[i], true);
     else s = load_tensor(h, T[i], h->gw[i], sizes[i], false);
+    if (s == SDV2_OK && i == G_HEAD_W) s = load_tensor(h, T[i], h->head_w_tw, sizes[i], true);
     if (s != SDV2_OK) return fail(s);
   }
   for (int b = 0; b < h->nb; ++b) {
@@ -766,6 +835,8 @@ sdv2_status sdv2_create(const sdv2_model_desc* md, const sdv2_geometry* g, const
     if (!tc_gemm_plan(h->gplan, &h->err)) return fail(SDV2_E_CUDA);
     attn_plan_init(h->aplan, h->gplan.encode);
   }
+  cudaFuncSetAttribute(gemv2_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(gemv2_kernel<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   *out = h;
   return SDV2_OK;
 }
