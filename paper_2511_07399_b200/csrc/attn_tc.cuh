@@ -2,16 +2,19 @@
 // (SURVEY.md §8(a) a7, P:183 FlashAttention-style O(BT) memory, P:472 rolling cache)
 // and over the prompt K/V (a9 cross-attention).
 //
-// One CTA = (entry e, head h, 128 query rows).  Keys are one contiguous row range
-// of the lane (valid slots are always a prefix, so no gather and no slot mask; only
-// the ragged key tail is masked).  Per 128-key tile j:
-//   S_j = Q K_j^T        tcgen05.mma M=128 N=128 K=hd, A=Q (smem), B=K_j (smem), D in TMEM
-//   softmax              4 warps, one query row per thread (tcgen05.ld S), exp2, running
-//                        max / sum; P_j -> smem (bf16, 128-byte swizzle = UMMA K-major A)
-//   O += P_j V_j         tcgen05.mma M=128 N=hd K=128, B = V_j MN-major, O stays in TMEM
-// S is double-buffered in TMEM so S_{j+1}, S_{j+2} run on the tensor core while the
-// softmax warps work on S_j.  O is rescaled in TMEM only when a row max grows by more
-// than 2^8 (lazy rescale; P <= 256 keeps bf16 and fp32 sums safe).
+// Work unit = (entry e, head h, 128-query tile).  Keys are one contiguous row range of
+// the lane (valid slots are always a prefix, so no gather and no slot mask; only the
+// ragged key tail is masked).  The (unit, 128-key tile) space is split evenly over
+// exactly one CTA per SM ("stream-K"): a CTA walks its contiguous tile range, which
+// covers whole units in the middle and at most one partial unit at each end; partial
+// units leave (unnormalised O, running max, sum) in a scratch slot and are merged by
+// attn_combine_kernel in a fixed CTA order (deterministic).  This removes the wave
+// quantisation of 156 units on 148 SMs (1.3B, 480p, n = 1).
+//
+// Per key tile g:  S_g = Q K_g^T (tcgen05.mma M=128 N=128 K=hd, D in TMEM, double
+// buffered) -> softmax (4 warps, one query row per thread, tcgen05.ld, exp2, lazy
+// rescale of O in TMEM when the row max grows by > 2^8) -> P_g (bf16, 128-byte
+// swizzled smem = UMMA K-major A) -> O += P_g V_g (tcgen05.mma N=hd, V MN-major).
 // Warp roles (192 threads): 0 TMA, 1 MMA issuer, 2..5 softmax / correction / epilogue.
 #pragma once
 #include <string>
@@ -34,24 +37,48 @@ struct AttnSmem {
 
 struct AttnTcArgs {
   int L;               // query rows per entry
-  int q_row_base;      // always 0 (q buffer row e*L)
   int kv_row0;         // row of lane 0 / version 0 of this block in the K/V map
   int kv_lane_rows;    // rows between lanes (self) or prompt versions (cross)
   int cross;
   int Lk_cross;
-  int col0;            // unused
   float scale_log2;    // log2(e) / sqrt(hd)
   void* o;
   int ldo;
+  int H, QT;           // heads, query tiles per entry
+  int n_entries;       // entries covered (active prefix)
+  float* part_o;       // [G][2][128][HD] fp32 partial (unnormalised) O
+  float* part_ml;      // [G][2][128][2] running max (log2 domain), sum
 };
 
-__device__ __forceinline__ void tmem_ld32_f(uint32_t taddr, float (&f)[32]) {
-  uint32_t r[32];
-  tc::tmem_ld32(taddr, r);
-  tc::tmem_ld_wait();
-#pragma unroll
-  for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(r[i]);
-}
+// Stream-K geometry shared by the attention and the combine kernels.
+struct AttnGeo {
+  long long off[kMaxSteps + 1];   // tile offset of entry e's first unit
+  int J[kMaxSteps];               // key tiles per unit of entry e
+  long long T;                    // total tiles
+  __device__ void init(const AttnTcArgs& a, const TickDesc* td) {
+    off[0] = 0;
+    for (int e = 0; e < kMaxSteps; ++e) {
+      int j = 0;
+      if (e < a.n_entries && td->e[e].active) {
+        const int Lk = a.cross ? a.Lk_cross : td->e[e].nvalid * a.L;
+        j = (Lk + kAttnBKV - 1) / kAttnBKV;
+      }
+      J[e] = j;
+      off[e + 1] = off[e] + (long long)a.H * a.QT * j;
+    }
+    T = off[kMaxSteps];
+  }
+  // unit containing global tile g -> (e, unit-in-entry w, tile j)
+  __device__ void locate(long long g, int& e, int& w, int& j) const {
+    e = 0;
+    while (e < kMaxSteps - 1 && g >= off[e + 1]) ++e;
+    const long long r = g - off[e];
+    w = int(r / J[e]);
+    j = int(r % J[e]);
+  }
+  __device__ long long start(int c, int G) const { return (T * c) / G; }
+  __device__ int cta_of(long long g, int G) const { return int(((g + 1) * G + T - 1) / T) - 1; }
+};
 
 template <int HD>
 __global__ void __launch_bounds__(192, 1) attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ,
@@ -76,14 +103,15 @@ __global__ void __launch_bounds__(192, 1) attn_tc_kernel(const __grid_constant__
   uint64_t* s_empty = bar + 11; // [2]
   uint64_t* p_full = bar + 13;
   uint64_t* p_empty = bar + 14;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
+  uint64_t* q_empty = bar + 15;
+  uint64_t* o_empty = bar + 16;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 18);
 
-  const int e = blockIdx.z, h = blockIdx.y, q0 = blockIdx.x * kAttnBQ;
-  const EntryDesc& E = td->e[e];
-  if (!E.active || q0 >= a.L) return;
-  const int Lk = a.cross ? a.Lk_cross : E.nvalid * a.L;
-  const int kv_row = a.kv_row0 + (a.cross ? (E.pver & 1) : e) * a.kv_lane_rows;
-  const int J = (Lk + kAttnBKV - 1) / kAttnBKV;
+  AttnGeo geo;
+  geo.init(a, td);
+  const int G = gridDim.x, c = blockIdx.x;
+  const long long t0 = geo.start(c, G), t1 = geo.start(c + 1, G);
+  if (t0 >= t1) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (warp == 0 && lane == 0) {
@@ -91,6 +119,8 @@ __global__ void __launch_bounds__(192, 1) attn_tc_kernel(const __grid_constant__
     tc::tma_prefetch_desc(&tmK);
     tc::tma_prefetch_desc(&tmV);
     tc::mbar_init(q_full, 1);
+    tc::mbar_init(q_empty, 1);
+    tc::mbar_init(o_empty, 4);
     for (int s = 0; s < 2; ++s) {
       tc::mbar_init(k_full + s, 1);
       tc::mbar_init(k_empty + s, 1);
@@ -111,26 +141,54 @@ __global__ void __launch_bounds__(192, 1) attn_tc_kernel(const __grid_constant__
   const uint32_t tS[2] = {tmem, tmem + 128u};
   const uint32_t tO = tmem + 256u;
 
+  // Segment iteration: [gs, ge) of global tiles inside one unit.
+  struct Seg {
+    int e, h, q0, jb, je, J;
+    long long ge;
+  };
+  auto seg_at = [&](long long g) {
+    Seg s;
+    int w, j;
+    geo.locate(g, s.e, w, j);
+    s.h = w / a.QT;
+    s.q0 = (w % a.QT) * kAttnBQ;
+    s.J = geo.J[s.e];
+    s.jb = j;
+    const long long unit_end = g - j + s.J;
+    s.ge = unit_end < t1 ? unit_end : t1;
+    s.je = j + int(s.ge - g);
+    return s;
+  };
+
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
-      const int col = h * HD;
-      tc::mbar_expect_tx(q_full, SM::Q);
-      for (int c = 0; c < NCH; ++c)
-        tc::tma_load_2d(sQ + c * (kAttnBQ * 128), &tmQ, q_full, col + c * 64, a.q_row_base + e * a.L + q0);
-      for (int j = 0; j < J; ++j) {
-        const int s = j & 1;
-        const uint32_t ph = ((j >> 1) & 1) ^ 1;
-        tc::mbar_wait(k_empty + s, ph);
-        tc::mbar_expect_tx(k_full + s, SM::KV);
-        for (int c = 0; c < NCH; ++c)
-          tc::tma_load_2d(sK + s * SM::KV + c * (kAttnBKV * 128), &tmK, k_full + s, col + c * 64,
-                          kv_row + j * kAttnBKV);
-        tc::mbar_wait(v_empty + s, ph);
-        tc::mbar_expect_tx(v_full + s, SM::KV);
-        for (int c = 0; c < NCH; ++c)
-          tc::tma_load_2d(sV + s * SM::KV + c * (kAttnBKV * 128), &tmV, v_full + s, col + c * 64,
-                          kv_row + j * kAttnBKV);
+      long long g = t0;
+      int gi = 0, sg = 0;   // local tile counter, segment counter
+      while (g < t1) {
+        const Seg s = seg_at(g);
+        const int col = s.h * HD;
+        const int kv_row = a.kv_row0 + (a.cross ? (td->e[s.e].pver & 1) : s.e) * a.kv_lane_rows;
+        if (sg > 0) tc::mbar_wait(q_empty, (sg - 1) & 1);
+        tc::mbar_expect_tx(q_full, SM::Q);
+        for (int ch = 0; ch < NCH; ++ch)
+          tc::tma_load_2d(sQ + ch * (kAttnBQ * 128), &tmQ, q_full, col + ch * 64, s.e * a.L + s.q0);
+        for (int j = s.jb; j < s.je; ++j, ++gi) {
+          const int st = gi & 1;
+          const uint32_t ph = ((gi >> 1) & 1) ^ 1;
+          tc::mbar_wait(k_empty + st, ph);
+          tc::mbar_expect_tx(k_full + st, SM::KV);
+          for (int ch = 0; ch < NCH; ++ch)
+            tc::tma_load_2d(sK + st * SM::KV + ch * (kAttnBKV * 128), &tmK, k_full + st, col + ch * 64,
+                            kv_row + j * kAttnBKV);
+          tc::mbar_wait(v_empty + st, ph);
+          tc::mbar_expect_tx(v_full + st, SM::KV);
+          for (int ch = 0; ch < NCH; ++ch)
+            tc::tma_load_2d(sV + st * SM::KV + ch * (kAttnBKV * 128), &tmV, v_full + st, col + ch * 64,
+                            kv_row + j * kAttnBKV);
+        }
+        g = s.ge;
+        ++sg;
       }
     }
   } else if (warp == 1) {
@@ -139,41 +197,50 @@ __global__ void __launch_bounds__(192, 1) attn_tc_kernel(const __grid_constant__
       const uint32_t idS = tc::idesc_bf16(kAttnBQ, kAttnBKV);
       const uint32_t idO = tc::idesc_bf16(kAttnBQ, HD, true);
       const uint32_t qa = tc::smem_u32(sQ), pa = tc::smem_u32(sP);
-      auto issue_S = [&](int j) {
-        const int s = j & 1;
-        tc::mbar_wait(k_full + s, (j >> 1) & 1);
+      auto issue_S = [&](int gg) {     // gg = local tile counter
+        const int st = gg & 1;
+        tc::mbar_wait(k_full + st, (gg >> 1) & 1);
+        if (gg >= 2) tc::mbar_wait(s_empty + st, ((gg >> 1) - 1) & 1);
         tc::tc_fence_after();
-        const uint32_t ka = tc::smem_u32(sK + s * SM::KV);
+        const uint32_t ka = tc::smem_u32(sK + st * SM::KV);
 #pragma unroll
         for (int k = 0; k < HD / 16; ++k) {
           const uint32_t off = (k >> 2) * (kAttnBQ * 128) + (k & 3) * 32;
           const uint32_t koff = (k >> 2) * (kAttnBKV * 128) + (k & 3) * 32;
-          tc::mma_bf16(tS[s], tc::sw128_kmajor_desc(qa + off), tc::sw128_kmajor_desc(ka + koff), idS, k > 0);
+          tc::mma_bf16(tS[st], tc::sw128_kmajor_desc(qa + off), tc::sw128_kmajor_desc(ka + koff), idS, k > 0);
         }
-        tc::mma_commit(k_empty + s);
-        tc::mma_commit(s_full + s);
+        tc::mma_commit(k_empty + st);
+        tc::mma_commit(s_full + st);
       };
-      tc::mbar_wait(q_full, 0);
-      issue_S(0);
-      if (J > 1) issue_S(1);
-      for (int j = 0; j < J; ++j) {
-        const int s = j & 1;
-        tc::mbar_wait(p_full, j & 1);
-        tc::mbar_wait(v_full + s, (j >> 1) & 1);
-        tc::tc_fence_after();
-        const uint32_t va = tc::smem_u32(sV + s * SM::KV);
+      long long g = t0;
+      int gi = 0, sg = 0;
+      while (g < t1) {
+        const Seg s = seg_at(g);
+        const int nt = s.je - s.jb;
+        tc::mbar_wait(q_full, sg & 1);
+        issue_S(gi);
+        if (nt > 1) issue_S(gi + 1);
+        for (int t = 0; t < nt; ++t) {
+          const int gt = gi + t;
+          tc::mbar_wait(p_full, gt & 1);
+          tc::mbar_wait(v_full + (gt & 1), (gt >> 1) & 1);
+          if (t == 0 && sg > 0) tc::mbar_wait(o_empty, (sg - 1) & 1);
+          tc::tc_fence_after();
+          const uint32_t va = tc::smem_u32(sV + (gt & 1) * SM::KV);
 #pragma unroll
-        for (int k = 0; k < kAttnBKV / 16; ++k) {
-          const uint32_t poff = (k >> 2) * (kAttnBQ * 128) + (k & 3) * 32;
-          tc::mma_bf16(tO, tc::sw128_kmajor_desc(pa + poff),
-                       tc::sw128_mnmajor_desc(va + k * 2048, kAttnBKV * 128), idO, (j | k) != 0);
+          for (int k = 0; k < kAttnBKV / 16; ++k) {
+            const uint32_t poff = (k >> 2) * (kAttnBQ * 128) + (k & 3) * 32;
+            tc::mma_bf16(tO, tc::sw128_kmajor_desc(pa + poff),
+                         tc::sw128_mnmajor_desc(va + k * 2048, kAttnBKV * 128), idO, (t | k) != 0);
+          }
+          tc::mma_commit(v_empty + (gt & 1));
+          tc::mma_commit(p_empty);
+          if (t + 2 < nt) issue_S(gt + 2);
         }
-        tc::mma_commit(v_empty + s);
-        tc::mma_commit(p_empty);
-        if (j + 2 < J) {
-          tc::mbar_wait(s_empty + s, (j >> 1) & 1);
-          issue_S(j + 2);
-        }
+        tc::mma_commit(q_empty);
+        gi += nt;
+        g = s.ge;
+        ++sg;
       }
     }
   } else {
@@ -181,103 +248,136 @@ __global__ void __launch_bounds__(192, 1) attn_tc_kernel(const __grid_constant__
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
     const uint32_t lane_off = uint32_t(quarter * 32) << 16;
-    float m_used = -INFINITY;   // max the current P / O are relative to (log2 domain)
-    float l = 0.f;
-    for (int j = 0; j < J; ++j) {
-      const int s = j & 1;
-      tc::mbar_wait(s_full + s, (j >> 1) & 1);
-      tc::tc_fence_after();
-      float sv[kAttnBKV];
+    long long g = t0;
+    int gi = 0, sg = 0;
+    while (g < t1) {
+      const Seg s = seg_at(g);
+      const int nt = s.je - s.jb;
+      const int Lk = a.cross ? a.Lk_cross : td->e[s.e].nvalid * a.L;
+      float m_used = -INFINITY;   // max the current P / O are relative to (log2 domain)
+      float l = 0.f;
+      for (int t = 0; t < nt; ++t) {
+        const int gt = gi + t;
+        const int st = gt & 1;
+        tc::mbar_wait(s_full + st, (gt >> 1) & 1);
+        tc::tc_fence_after();
+        float sv[kAttnBKV];
 #pragma unroll
-      for (int c = 0; c < kAttnBKV / 32; ++c) {
-        uint32_t r[32];
-        tc::tmem_ld32(tS[s] + lane_off + c * 32, r);
-        tc::tmem_ld_wait();
+        for (int cc = 0; cc < kAttnBKV / 32; ++cc) {
+          uint32_t r[32];
+          tc::tmem_ld32(tS[st] + lane_off + cc * 32, r);
+          tc::tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) sv[c * 32 + i] = __uint_as_float(r[i]);
-      }
-      tc::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(s_empty + s);
-      const int kvalid = Lk - j * kAttnBKV;
-      float mx = -INFINITY;
+          for (int i = 0; i < 32; ++i) sv[cc * 32 + i] = __uint_as_float(r[i]);
+        }
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(s_empty + st);
+        const int kvalid = Lk - (s.jb + t) * kAttnBKV;
+        float mx = -INFINITY;
 #pragma unroll
-      for (int i = 0; i < kAttnBKV; ++i) {
-        sv[i] = (i < kvalid) ? sv[i] * a.scale_log2 : -INFINITY;
-        mx = fmaxf(mx, sv[i]);
-      }
-      // wait until PV_{j-1} finished: P smem free and O stable in TMEM
-      if (j > 0) tc::mbar_wait(p_empty, (j - 1) & 1);
-      tc::tc_fence_after();
-      if (mx > m_used + 8.f) {
-        const float m_new = mx;
-        if (j > 0) {
-          const float alpha = exp2f(m_used - m_new);
-          l *= alpha;
+        for (int i = 0; i < kAttnBKV; ++i) {
+          sv[i] = (i < kvalid) ? sv[i] * a.scale_log2 : -INFINITY;
+          mx = fmaxf(mx, sv[i]);
+        }
+        // PV of the previous tile finished: P smem free and O stable in TMEM
+        if (gt > 0) tc::mbar_wait(p_empty, (gt - 1) & 1);
+        tc::tc_fence_after();
+        if (mx > m_used + 8.f) {
+          const float m_new = mx;
+          if (t > 0) {
+            const float alpha = exp2f(m_used - m_new);
+            l *= alpha;
 #pragma unroll
-          for (int c = 0; c < HD / 16; ++c) {
-            uint32_t r[16];
-            asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-                  "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
-                  "=r"(r[15])
-                : "r"(tO + lane_off + c * 16));
-            tc::tmem_ld_wait();
+            for (int cc = 0; cc < HD / 16; ++cc) {
+              uint32_t r[16];
+              asm volatile(
+                  "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
+                  "[%16];"
+                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                    "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                    "=r"(r[15])
+                  : "r"(tO + lane_off + cc * 16));
+              tc::tmem_ld_wait();
 #pragma unroll
-            for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-            tc::tmem_st16(tO + lane_off + c * 16, r);
+              for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
+              tc::tmem_st16(tO + lane_off + cc * 16, r);
+            }
+            tc::tmem_st_wait();
           }
-          tc::tmem_st_wait();
+          m_used = m_new;
         }
-        m_used = m_new;
-      }
-      // P = exp2(s - m_used) -> bf16, 128-byte swizzled K-major rows
-      float rs = 0.f;
-      uint8_t* prow_base = sP + (row >> 3) * 1024 + (row & 7) * 128;
+        // P = exp2(s - m_used) -> bf16, 128-byte swizzled K-major rows
+        float rs = 0.f;
+        uint8_t* prow_base = sP + (row >> 3) * 1024 + (row & 7) * 128;
 #pragma unroll
-      for (int g = 0; g < kAttnBKV / 8; ++g) {
-        uint32_t pk[4];
+        for (int gq = 0; gq < kAttnBKV / 8; ++gq) {
+          uint32_t pk[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const float p0 = exp2f(sv[g * 8 + 2 * u] - m_used);
-          const float p1 = exp2f(sv[g * 8 + 2 * u + 1] - m_used);
-          rs += p0 + p1;
-          __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
-          pk[u] = *reinterpret_cast<uint32_t*>(&b2);
+          for (int u = 0; u < 4; ++u) {
+            const float p0 = exp2f(sv[gq * 8 + 2 * u] - m_used);
+            const float p1 = exp2f(sv[gq * 8 + 2 * u + 1] - m_used);
+            rs += p0 + p1;
+            __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
+            pk[u] = *reinterpret_cast<uint32_t*>(&b2);
+          }
+          const int chunk = gq >> 3, unit = gq & 7;
+          uint8_t* dst = prow_base + chunk * (kAttnBQ * 128) + ((unit ^ (row & 7)) << 4);
+          *reinterpret_cast<uint4*>(dst) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
         }
-        const int chunk = g >> 3, unit = g & 7;
-        uint8_t* dst = prow_base + chunk * (kAttnBQ * 128) + ((unit ^ (row & 7)) << 4);
-        *reinterpret_cast<uint4*>(dst) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        l += rs;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(p_full);
       }
-      l += rs;
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      // end of segment: last PV done -> read O
+      tc::mbar_wait(p_empty, (gi + nt - 1) & 1);
+      tc::tc_fence_after();
+      const bool full = (s.jb == 0 && s.je == s.J);
+      const int slot = (g == t0) ? 0 : 1;
+      const int qr = s.q0 + row;
+      const float inv = 1.f / l;
+      bf16* orow = reinterpret_cast<bf16*>(a.o) + size_t(s.e * a.L + qr) * a.ldo + s.h * HD;
+      float* prow = a.part_o + ((size_t(c) * 2 + slot) * kAttnBQ + row) * HD;
+#pragma unroll
+      for (int cc = 0; cc < HD / 32; ++cc) {
+        uint32_t r[32];
+        tc::tmem_ld32(tO + lane_off + cc * 32, r);
+        tc::tmem_ld_wait();
+        if (full) {
+          if (qr < a.L) {
+            uint32_t pk[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              __nv_bfloat162 b2 =
+                  __floats2bfloat162_rn(__uint_as_float(r[2 * i]) * inv, __uint_as_float(r[2 * i + 1]) * inv);
+              pk[i] = *reinterpret_cast<uint32_t*>(&b2);
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              reinterpret_cast<uint4*>(orow + cc * 32)[i] =
+                  make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            reinterpret_cast<float4*>(prow + cc * 32)[i] =
+                make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]), __uint_as_float(r[4 * i + 2]),
+                            __uint_as_float(r[4 * i + 3]));
+        }
+      }
+      if (!full) {
+        float* ml = a.part_ml + ((size_t(c) * 2 + slot) * kAttnBQ + row) * 2;
+        ml[0] = m_used;
+        ml[1] = l;
+      }
       tc::tc_fence_before();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(p_full);
-    }
-    // epilogue: wait for the last PV, O / l -> bf16
-    tc::mbar_wait(p_empty, (J - 1) & 1);
-    tc::tc_fence_after();
-    const float inv = 1.f / l;
-    const int qr = q0 + row;
-    bf16* orow = reinterpret_cast<bf16*>(a.o) + size_t(e * a.L + qr) * a.ldo + h * HD;
-#pragma unroll
-    for (int c = 0; c < HD / 32; ++c) {
-      uint32_t r[32];
-      tc::tmem_ld32(tO + lane_off + c * 32, r);
-      tc::tmem_ld_wait();
-      if (qr < a.L) {
-        uint32_t pk[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          __nv_bfloat162 b2 = __floats2bfloat162_rn(__uint_as_float(r[2 * i]) * inv, __uint_as_float(r[2 * i + 1]) * inv);
-          pk[i] = *reinterpret_cast<uint32_t*>(&b2);
-        }
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          reinterpret_cast<uint4*>(orow + c * 32)[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
-      }
+      if (lane == 0) tc::mbar_arrive(o_empty);
+      gi += nt;
+      g = s.ge;
+      ++sg;
     }
   }
   tc::tc_fence_before();
@@ -288,21 +388,83 @@ __global__ void __launch_bounds__(192, 1) attn_tc_kernel(const __grid_constant__
   }
 }
 
+// Merge the partial units (split between consecutive CTAs) in CTA order:
+// O = sum_k 2^(m_k - M) O_k / sum_k 2^(m_k - M) l_k.  One CTA per unit, thread = row.
+template <int HD>
+__global__ void __launch_bounds__(128) attn_combine_kernel(AttnTcArgs a, const TickDesc* __restrict__ td, int G) {
+  AttnGeo geo;
+  geo.init(a, td);
+  const int u = blockIdx.x;
+  const int e = u / (a.H * a.QT), w = u % (a.H * a.QT);
+  if (e >= a.n_entries || geo.J[e] == 0) return;
+  const long long off = geo.off[e] + (long long)w * geo.J[e];
+  const int cf = geo.cta_of(off, G), cl = geo.cta_of(off + geo.J[e] - 1, G);
+  const bool full = (cf == cl) && true;
+  if (full) return;   // one CTA covered the whole unit and wrote the final output
+  const int row = threadIdx.x;
+  const int h = w / a.QT, q0 = (w % a.QT) * kAttnBQ;
+  float M = -INFINITY;
+  for (int cc = cf; cc <= cl; ++cc) {
+    const int slot = (cc == cf && geo.start(cc, G) < off) ? 1 : 0;
+    M = fmaxf(M, a.part_ml[((size_t(cc) * 2 + slot) * kAttnBQ + row) * 2]);
+  }
+  float den = 0.f;
+  float acc[HD];
+#pragma unroll
+  for (int i = 0; i < HD; ++i) acc[i] = 0.f;
+  for (int cc = cf; cc <= cl; ++cc) {
+    const int slot = (cc == cf && geo.start(cc, G) < off) ? 1 : 0;
+    const float* ml = a.part_ml + ((size_t(cc) * 2 + slot) * kAttnBQ + row) * 2;
+    const float wgt = exp2f(ml[0] - M);
+    den += wgt * ml[1];
+    const float4* po = reinterpret_cast<const float4*>(a.part_o + ((size_t(cc) * 2 + slot) * kAttnBQ + row) * HD);
+#pragma unroll
+    for (int i = 0; i < HD / 4; ++i) {
+      const float4 v = po[i];
+      acc[4 * i] += wgt * v.x;
+      acc[4 * i + 1] += wgt * v.y;
+      acc[4 * i + 2] += wgt * v.z;
+      acc[4 * i + 3] += wgt * v.w;
+    }
+  }
+  const int qr = q0 + row;
+  if (qr >= a.L) return;
+  const float inv = 1.f / den;
+  bf16* orow = reinterpret_cast<bf16*>(a.o) + size_t(e * a.L + qr) * a.ldo + h * HD;
+#pragma unroll
+  for (int i = 0; i < HD / 8; ++i) {
+    uint32_t pk[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      __nv_bfloat162 b2 = __floats2bfloat162_rn(acc[8 * i + 2 * k] * inv, acc[8 * i + 2 * k + 1] * inv);
+      pk[k] = *reinterpret_cast<uint32_t*>(&b2);
+    }
+    reinterpret_cast<uint4*>(orow)[i] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+  }
+}
+
 // ------------------------------------------------------------------ host side
 struct AttnPlan {
   PFN_encodeTiled encode = nullptr;
+  int num_sms = 148;
   std::unordered_map<std::string, CUtensorMap> maps;
   bool ready = false;
 };
 
 inline bool tc_attn_enabled() { return true; }
 
-inline bool attn_plan_init(AttnPlan& p, PFN_encodeTiled enc) {
+inline bool attn_plan_init(AttnPlan& p, PFN_encodeTiled enc, int num_sms) {
   p.encode = enc;
+  p.num_sms = num_sms;
   cudaFuncSetAttribute(attn_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, AttnSmem<128>::total);
   cudaFuncSetAttribute(attn_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, AttnSmem<64>::total);
   p.ready = true;
   return true;
+}
+
+// Scratch for the partial units: [num_sms][2][128][hd] fp32 + [num_sms][2][128][2].
+inline size_t attn_scratch_floats(int num_sms, int hd) {
+  return size_t(num_sms) * 2 * kAttnBQ * hd + size_t(num_sms) * 2 * kAttnBQ * 2;
 }
 
 // 2D bf16 map over [rows, ld] with a (64 x box_rows) box, 128-byte swizzle.
@@ -327,20 +489,24 @@ inline const CUtensorMap* attn_map(AttnPlan& p, const void* base, long long rows
   return &(p.maps.emplace(key, m).first->second);
 }
 
-// q: [q_rows, ldq] bf16; K/V maps over whole buffers [kv_rows, ldk]; grid over
-// (q tiles, heads, entries).
+// q: [q_rows, d] bf16; K/V maps over whole buffers [kv_rows, d].  `total_tiles_hint`
+// (host estimate of the unit x key-tile space) only sizes the grid: min(SMs, tiles).
 inline bool tc_attention(cudaStream_t s, AttnPlan& p, const void* q, long long q_rows, const void* Kbase,
-                         const void* Vbase, long long kv_rows, int d, int hd, int H, int n_entries,
+                         const void* Vbase, long long kv_rows, int d, int hd, long long total_tiles_hint,
                          const AttnTcArgs& a, const TickDesc* td, std::string* err) {
   const CUtensorMap* mq = attn_map(p, q, q_rows, d, kAttnBQ, err);
   const CUtensorMap* mk = attn_map(p, Kbase, kv_rows, d, kAttnBKV, err);
   const CUtensorMap* mv = attn_map(p, Vbase, kv_rows, d, kAttnBKV, err);
   if (!mq || !mk || !mv) return false;
-  dim3 grid((a.L + kAttnBQ - 1) / kAttnBQ, H, n_entries);
-  if (hd == 128)
-    attn_tc_kernel<128><<<grid, 192, AttnSmem<128>::total, s>>>(*mq, *mk, *mv, a, td);
-  else
-    attn_tc_kernel<64><<<grid, 192, AttnSmem<64>::total, s>>>(*mq, *mk, *mv, a, td);
+  const int G = int(total_tiles_hint < p.num_sms ? total_tiles_hint : p.num_sms);
+  const int units = a.n_entries * a.H * a.QT;
+  if (hd == 128) {
+    attn_tc_kernel<128><<<G, 192, AttnSmem<128>::total, s>>>(*mq, *mk, *mv, a, td);
+    attn_combine_kernel<128><<<units, 128, 0, s>>>(a, td, G);
+  } else {
+    attn_tc_kernel<64><<<G, 192, AttnSmem<64>::total, s>>>(*mq, *mk, *mv, a, td);
+    attn_combine_kernel<64><<<units, 128, 0, s>>>(a, td, G);
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     *err = std::string("attn_tc launch: ") + cudaGetErrorString(e);

@@ -30,6 +30,7 @@ constexpr int kNumGlobal = 15;
 constexpr int kNumBlockT = 27;
 constexpr int kTdRing = 16;
 constexpr int kMaxTOff = 4096 + 16;
+constexpr int kMaxSMs = 160;
 
 enum GlobalT { G_PATCH_W, G_PATCH_B, G_TXT1_W, G_TXT1_B, G_TXT2_W, G_TXT2_B, G_T1_W, G_T1_B, G_T2_W, G_T2_B,
                G_TP_W, G_TP_B, G_HEAD_MOD, G_HEAD_W, G_HEAD_B };
@@ -104,6 +105,7 @@ struct sdv2_handle {
   float* emb;                 // [n, 256]
   float* u;                   // patchified tokens [Mmax, 4C] fp32
   float* yh;                  // head output [Mmax, 4C] fp32
+  float* attn_part;           // stream-K attention partials
   void* head_w_tw;            // head weight [4C, d] TW
   float* t1;                  // [n, d]
   void* a;                    // [Mmax, d] TA
@@ -246,6 +248,7 @@ size_t carve(sdv2_handle* h, void* base) {
   h->emb = cv.take<float>(size_t(h->n) * h->md.freq_dim);
   h->u = cv.take<float>(size_t(h->Mmax) * h->P);
   h->yh = cv.take<float>(size_t(h->Mmax) * h->P);
+  h->attn_part = cv.take<float>(attn_scratch_floats(kMaxSMs, h->hd));
   h->t1 = cv.take<float>(size_t(h->n) * d);
   // activation scratch, aliased by the weight staging buffer during create
   {
@@ -411,6 +414,16 @@ sdv2_status attention(sdv2_handle* h, const AttnArgs& aa, int Mrows_entries, dou
       ta.scale_log2 = 1.4426950408889634f / sqrtf(float(h->hd));
       ta.o = aa.o;
       ta.ldo = aa.ldo;
+      ta.H = h->H;
+      ta.QT = (h->L + kAttnBQ - 1) / kAttnBQ;
+      ta.n_entries = Mrows_entries;
+      ta.part_o = h->attn_part;
+      ta.part_ml = h->attn_part + size_t(kMaxSMs) * 2 * kAttnBQ * h->hd;
+      long long tiles = 0;
+      for (int e = 0; e < Mrows_entries; ++e) {
+        const int Lk = aa.cross ? aa.Lk_cross : h->td_host_cur->e[e].nvalid * h->L;
+        tiles += (long long)ta.H * ta.QT * ((Lk + kAttnBKV - 1) / kAttnBKV);
+      }
       const void *Kb, *Vb;
       long long kv_rows;
       if (aa.cross) {
@@ -424,8 +437,9 @@ sdv2_status attention(sdv2_handle* h, const AttnArgs& aa, int Mrows_entries, dou
         ta.kv_row0 = bl * h->n * h->S * h->L;
         ta.kv_lane_rows = h->S * h->L;
       }
-      return tc_attention(h->stream, h->aplan, aa.q, h->Mmax, Kb, Vb, kv_rows, h->d, h->hd, h->H, Mrows_entries, ta,
-                          h->td_dev, &h->err) ? SDV2_OK : SDV2_E_CUDA;
+      ++h->launches;   // + the combine kernel
+      return tc_attention(h->stream, h->aplan, aa.q, h->Mmax, Kb, Vb, kv_rows, h->d, h->hd, tiles, ta, h->td_dev,
+                          &h->err) ? SDV2_OK : SDV2_E_CUDA;
     }
     if (h->hd == 64) attn_simt_kernel<bf16, 64><<<grid, 128, 0, h->stream>>>(aa, h->td_dev);
     else attn_simt_kernel<bf16, 128><<<grid, 128, 0, h->stream>>>(aa, h->td_dev);
@@ -833,7 +847,7 @@ sdv2_status sdv2_create(const sdv2_model_desc* md, const sdv2_geometry* g, const
   }
   if (h->prec == SDV2_BF16) {
     if (!tc_gemm_plan(h->gplan, &h->err)) return fail(SDV2_E_CUDA);
-    attn_plan_init(h->aplan, h->gplan.encode);
+    attn_plan_init(h->aplan, h->gplan.encode, std::min(h->gplan.num_sms, kMaxSMs));
   }
   cudaFuncSetAttribute(gemv2_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(gemv2_kernel<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -1073,7 +1087,7 @@ extern "C" sdv2_status sdv2_debug_attention(const void* q, const void* K, const 
   std::string err;
   if (!ready) {
     if (!tc_gemm_plan(gp, &err)) return SDV2_E_CUDA;
-    attn_plan_init(ap, gp.encode);
+    attn_plan_init(ap, gp.encode, std::min(gp.num_sms, kMaxSMs));
     ready = true;
   }
   ap.maps.clear();
@@ -1083,16 +1097,24 @@ extern "C" sdv2_status sdv2_debug_attention(const void* q, const void* K, const 
   tdh.n_active = 1;
   tdh.e[0].active = 1;
   if (cudaMemcpyAsync(scratch, &tdh, sizeof(tdh), cudaMemcpyHostToDevice, s) != cudaSuccess) return SDV2_E_CUDA;
+  static float* part = nullptr;
+  if (!part && cudaMalloc(&part, attn_scratch_floats(kMaxSMs, 128) * 4) != cudaSuccess) return SDV2_E_CUDA;
   AttnTcArgs ta{};
   ta.L = Lq;
   ta.cross = 1;
   ta.Lk_cross = Lk;
+  ta.H = H;
+  ta.QT = (Lq + kAttnBQ - 1) / kAttnBQ;
+  ta.n_entries = 1;
+  ta.part_o = part;
+  ta.part_ml = part + size_t(kMaxSMs) * 2 * kAttnBQ * hd;
   ta.scale_log2 = 1.4426950408889634f / sqrtf(float(hd));
   ta.o = o;
   ta.ldo = H * hd;
   ta.kv_row0 = 0;
   ta.kv_lane_rows = 0;
-  if (!tc_attention(s, ap, q, Lq, K, V, Lk, H * hd, hd, H, 1, ta, static_cast<const TickDesc*>(scratch), &err)) {
+  const long long tiles = (long long)H * ta.QT * ((Lk + kAttnBKV - 1) / kAttnBKV);
+  if (!tc_attention(s, ap, q, Lq, K, V, Lk, H * hd, hd, tiles, ta, static_cast<const TickDesc*>(scratch), &err)) {
     fprintf(stderr, "sdv2_debug_attention: %s\n", err.c_str());
     return SDV2_E_CUDA;
   }
