@@ -915,6 +915,12 @@ sdv2_status sdv2_reset_stream(sdv2_handle* h, const sdv2_stream_desc* sd, const 
   const size_t kv = size_t(h->nb) * h->n * h->S * h->L * h->d * h->ta;
   CK(cudaMemsetAsync(h->Kc, 0, kv, h->stream));
   CK(cudaMemsetAsync(h->Vc, 0, kv, h->stream));
+  // Attention key tiles are 128 rows and may extend past a lane's valid keys into other
+  // slots / blocks / prompt versions: those rows get P = 0, but must hold finite values
+  // (0 x NaN = NaN in the PV MMA), so every K/V buffer starts zeroed.
+  const size_t px = size_t(2) * h->nb * h->Lt * h->d * h->ta;
+  CK(cudaMemsetAsync(h->Kx, 0, px, h->stream));
+  CK(cudaMemsetAsync(h->Vx, 0, px, h->stream));
   CK(cudaMemsetAsync(h->ctrl, 0, sizeof(CtrlState), h->stream));
   CK(cudaMemsetAsync(h->packet_base, 0, h->st.bytes, h->stream));
   {
