@@ -32,7 +32,7 @@ struct AttnSmem {
   static constexpr int Q = kAttnBQ * HD * 2;          // 32 KB (hd 128)
   static constexpr int KV = kAttnBKV * HD * 2;        // one K or V tile
   static constexpr int P = kAttnBQ * kAttnBKV * 2;    // 32 KB
-  static constexpr int total = Q + 4 * KV + P + 1024 + 512;
+  static constexpr int total = Q + 4 * KV + P + 1024 + 256 + 4 * 256 * 4;
 };
 
 struct AttnTcArgs {
@@ -48,6 +48,7 @@ struct AttnTcArgs {
   int n_entries;       // entries covered (active prefix)
   float* part_o;       // [G][2][128][HD] fp32 partial (unnormalised) O
   float* part_ml;      // [G][2][128][2] running max (log2 domain), sum
+  int per_unit;        // 1: one CTA per unit (grid = units, no merge); 0: stream-K
 };
 
 // Stream-K geometry shared by the attention and the combine kernels.
@@ -80,8 +81,16 @@ struct AttnGeo {
   __device__ int cta_of(long long g, int G) const { return int(((g + 1) * G + T - 1) / T) - 1; }
 };
 
+constexpr int kAttnThreads = 320;   // warp 0 TMA, 1 MMA, 2..9 softmax (two column halves)
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 template <int HD>
-__global__ void __launch_bounds__(192, 1) attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ,
+__global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ,
                                                          const __grid_constant__ CUtensorMap tmK,
                                                          const __grid_constant__ CUtensorMap tmV, AttnTcArgs a,
                                                          const TickDesc* __restrict__ td) {
@@ -106,11 +115,21 @@ __global__ void __launch_bounds__(192, 1) attn_tc_kernel(const __grid_constant__
   uint64_t* q_empty = bar + 15;
   uint64_t* o_empty = bar + 16;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 18);
+  float* xch = reinterpret_cast<float*>(bar + 20);   // [2 tiles][2 halves][128] row-max exchange + [2][128] sums
 
   AttnGeo geo;
   geo.init(a, td);
   const int G = gridDim.x, c = blockIdx.x;
-  const long long t0 = geo.start(c, G), t1 = geo.start(c + 1, G);
+  long long t0, t1;
+  if (a.per_unit) {
+    const int e = c / (a.H * a.QT), w = c % (a.H * a.QT);
+    if (e >= kMaxSteps || geo.J[e] == 0) return;
+    t0 = geo.off[e] + (long long)w * geo.J[e];
+    t1 = t0 + geo.J[e];
+  } else {
+    t0 = geo.start(c, G);
+    t1 = geo.start(c + 1, G);
+  }
   if (t0 >= t1) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -120,16 +139,16 @@ __global__ void __launch_bounds__(192, 1) attn_tc_kernel(const __grid_constant__
     tc::tma_prefetch_desc(&tmV);
     tc::mbar_init(q_full, 1);
     tc::mbar_init(q_empty, 1);
-    tc::mbar_init(o_empty, 4);
+    tc::mbar_init(o_empty, 8);
     for (int s = 0; s < 2; ++s) {
       tc::mbar_init(k_full + s, 1);
       tc::mbar_init(k_empty + s, 1);
       tc::mbar_init(v_full + s, 1);
       tc::mbar_init(v_empty + s, 1);
       tc::mbar_init(s_full + s, 1);
-      tc::mbar_init(s_empty + s, 4);
+      tc::mbar_init(s_empty + s, 8);
     }
-    tc::mbar_init(p_full, 4);
+    tc::mbar_init(p_full, 8);
     tc::mbar_init(p_empty, 1);
     tc::fence_barrier_init();
   }
@@ -245,7 +264,11 @@ __global__ void __launch_bounds__(192, 1) attn_tc_kernel(const __grid_constant__
     }
   } else {
     // ------------------------------------------------ softmax / correction / epilogue
+    // 8 warps: TMEM lane quarter = warp & 3 (row), column half = (warp - 2) / 4.
+    constexpr int HC = kAttnBKV / 2;            // S columns per thread
+    constexpr int HO = HD / 2;                  // O columns per thread
     const int quarter = warp & 3;
+    const int half = (warp - 2) >> 2;
     const int row = quarter * 32 + lane;
     const uint32_t lane_off = uint32_t(quarter * 32) << 16;
     long long g = t0;
@@ -255,17 +278,17 @@ __global__ void __launch_bounds__(192, 1) attn_tc_kernel(const __grid_constant__
       const int nt = s.je - s.jb;
       const int Lk = a.cross ? a.Lk_cross : td->e[s.e].nvalid * a.L;
       float m_used = -INFINITY;   // max the current P / O are relative to (log2 domain)
-      float l = 0.f;
+      float l = 0.f;              // this half's share of the row sum
       for (int t = 0; t < nt; ++t) {
         const int gt = gi + t;
         const int st = gt & 1;
         tc::mbar_wait(s_full + st, (gt >> 1) & 1);
         tc::tc_fence_after();
-        float sv[kAttnBKV];
+        float sv[HC];
 #pragma unroll
-        for (int cc = 0; cc < kAttnBKV / 32; ++cc) {
+        for (int cc = 0; cc < HC / 32; ++cc) {
           uint32_t r[32];
-          tc::tmem_ld32(tS[st] + lane_off + cc * 32, r);
+          tc::tmem_ld32(tS[st] + lane_off + half * HC + cc * 32, r);
           tc::tmem_ld_wait();
 #pragma unroll
           for (int i = 0; i < 32; ++i) sv[cc * 32 + i] = __uint_as_float(r[i]);
@@ -273,56 +296,66 @@ __global__ void __launch_bounds__(192, 1) attn_tc_kernel(const __grid_constant__
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(s_empty + st);
-        const int kvalid = Lk - (s.jb + t) * kAttnBKV;
+        const int kvalid = Lk - (s.jb + t) * kAttnBKV - half * HC;
         float mx = -INFINITY;
+        if (kvalid >= HC) {
 #pragma unroll
-        for (int i = 0; i < kAttnBKV; ++i) {
-          sv[i] = (i < kvalid) ? sv[i] * a.scale_log2 : -INFINITY;
-          mx = fmaxf(mx, sv[i]);
+          for (int i = 0; i < HC; ++i) mx = fmaxf(mx, sv[i]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < HC; ++i) {
+            sv[i] = (i < kvalid) ? sv[i] : -INFINITY;
+            mx = fmaxf(mx, sv[i]);
+          }
         }
+        // exchange the row max between the two column halves
+        float* xm = xch + (t & 1) * 256;
+        xm[half * 128 + row] = mx;
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        mx = fmaxf(mx, xm[(half ^ 1) * 128 + row]) * a.scale_log2;
         // PV of the previous tile finished: P smem free and O stable in TMEM
         if (gt > 0) tc::mbar_wait(p_empty, (gt - 1) & 1);
         tc::tc_fence_after();
         if (mx > m_used + 8.f) {
           const float m_new = mx;
           if (t > 0) {
-            const float alpha = exp2f(m_used - m_new);
+            const float alpha = ex2(m_used - m_new);
             l *= alpha;
 #pragma unroll
-            for (int cc = 0; cc < HD / 16; ++cc) {
+            for (int cc = 0; cc < HO / 16; ++cc) {
               uint32_t r[16];
+              const uint32_t ta = tO + lane_off + half * HO + cc * 16;
               asm volatile(
                   "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
                   "[%16];"
                   : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
                     "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
                     "=r"(r[15])
-                  : "r"(tO + lane_off + cc * 16));
+                  : "r"(ta));
               tc::tmem_ld_wait();
 #pragma unroll
               for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-              tc::tmem_st16(tO + lane_off + cc * 16, r);
+              tc::tmem_st16(ta, r);
             }
             tc::tmem_st_wait();
           }
           m_used = m_new;
         }
-        // P = exp2(s - m_used) -> bf16, 128-byte swizzled K-major rows
+        // P = exp2(s * scale - m_used) -> bf16, this half = P chunk `half` (64 keys, 128 B/row)
         float rs = 0.f;
-        uint8_t* prow_base = sP + (row >> 3) * 1024 + (row & 7) * 128;
+        uint8_t* prow_base = sP + half * (kAttnBQ * 128) + (row >> 3) * 1024 + (row & 7) * 128;
 #pragma unroll
-        for (int gq = 0; gq < kAttnBKV / 8; ++gq) {
+        for (int gq = 0; gq < HC / 8; ++gq) {
           uint32_t pk[4];
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            const float p0 = exp2f(sv[gq * 8 + 2 * u] - m_used);
-            const float p1 = exp2f(sv[gq * 8 + 2 * u + 1] - m_used);
+            const float p0 = ex2(fmaf(sv[gq * 8 + 2 * u], a.scale_log2, -m_used));
+            const float p1 = ex2(fmaf(sv[gq * 8 + 2 * u + 1], a.scale_log2, -m_used));
             rs += p0 + p1;
             __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
             pk[u] = *reinterpret_cast<uint32_t*>(&b2);
           }
-          const int chunk = gq >> 3, unit = gq & 7;
-          uint8_t* dst = prow_base + chunk * (kAttnBQ * 128) + ((unit ^ (row & 7)) << 4);
+          uint8_t* dst = prow_base + ((gq ^ (row & 7)) << 4);
           *reinterpret_cast<uint4*>(dst) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
         }
         l += rs;
@@ -331,19 +364,23 @@ __global__ void __launch_bounds__(192, 1) attn_tc_kernel(const __grid_constant__
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(p_full);
       }
-      // end of segment: last PV done -> read O
+      // end of segment: combine the two halves' sums, wait for the last PV, read O
+      float* xl = xch + 512;
+      xl[half * 128 + row] = l;
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      const float lt = l + xl[(half ^ 1) * 128 + row];
       tc::mbar_wait(p_empty, (gi + nt - 1) & 1);
       tc::tc_fence_after();
       const bool full = (s.jb == 0 && s.je == s.J);
       const int slot = (g == t0) ? 0 : 1;
       const int qr = s.q0 + row;
-      const float inv = 1.f / l;
-      bf16* orow = reinterpret_cast<bf16*>(a.o) + size_t(s.e * a.L + qr) * a.ldo + s.h * HD;
-      float* prow = a.part_o + ((size_t(c) * 2 + slot) * kAttnBQ + row) * HD;
+      const float inv = 1.f / lt;
+      bf16* orow = reinterpret_cast<bf16*>(a.o) + size_t(s.e * a.L + qr) * a.ldo + s.h * HD + half * HO;
+      float* prow = a.part_o + ((size_t(c) * 2 + slot) * kAttnBQ + row) * HD + half * HO;
 #pragma unroll
-      for (int cc = 0; cc < HD / 32; ++cc) {
+      for (int cc = 0; cc < HO / 32; ++cc) {
         uint32_t r[32];
-        tc::tmem_ld32(tO + lane_off + cc * 32, r);
+        tc::tmem_ld32(tO + lane_off + half * HO + cc * 32, r);
         tc::tmem_ld_wait();
         if (full) {
           if (qr < a.L) {
@@ -367,10 +404,10 @@ __global__ void __launch_bounds__(192, 1) attn_tc_kernel(const __grid_constant__
                             __uint_as_float(r[4 * i + 3]));
         }
       }
-      if (!full) {
+      if (!full && half == 0) {
         float* ml = a.part_ml + ((size_t(c) * 2 + slot) * kAttnBQ + row) * 2;
         ml[0] = m_used;
-        ml[1] = l;
+        ml[1] = lt;
       }
       tc::tc_fence_before();
       __syncwarp();
@@ -399,8 +436,7 @@ __global__ void __launch_bounds__(128) attn_combine_kernel(AttnTcArgs a, const T
   if (e >= a.n_entries || geo.J[e] == 0) return;
   const long long off = geo.off[e] + (long long)w * geo.J[e];
   const int cf = geo.cta_of(off, G), cl = geo.cta_of(off + geo.J[e] - 1, G);
-  const bool full = (cf == cl) && true;
-  if (full) return;   // one CTA covered the whole unit and wrote the final output
+  if (a.per_unit || cf == cl) return;   // one CTA covered the whole unit and wrote the final output   // one CTA covered the whole unit and wrote the final output
   const int row = threadIdx.x;
   const int h = w / a.QT, q0 = (w % a.QT) * kAttnBQ;
   float M = -INFINITY;
@@ -453,6 +489,15 @@ struct AttnPlan {
 
 inline bool tc_attn_enabled() { return true; }
 
+// Stream-K (even tile split + merge) vs one CTA per unit: compare rounds of tiles,
+// charging each unit boundary / merge about one tile of fixed cost.
+inline int attn_pick_per_unit(long long units, long long tiles, int num_sms) {
+  const long long J = units ? (tiles + units - 1) / units : 1;
+  const double per_unit = double((units + num_sms - 1) / num_sms) * double(J + 1);
+  const double streamk = double((tiles + num_sms - 1) / num_sms) + 3.0;
+  return per_unit <= streamk ? 1 : 0;
+}
+
 inline bool attn_plan_init(AttnPlan& p, PFN_encodeTiled enc, int num_sms) {
   p.encode = enc;
   p.num_sms = num_sms;
@@ -498,14 +543,14 @@ inline bool tc_attention(cudaStream_t s, AttnPlan& p, const void* q, long long q
   const CUtensorMap* mk = attn_map(p, Kbase, kv_rows, d, kAttnBKV, err);
   const CUtensorMap* mv = attn_map(p, Vbase, kv_rows, d, kAttnBKV, err);
   if (!mq || !mk || !mv) return false;
-  const int G = int(total_tiles_hint < p.num_sms ? total_tiles_hint : p.num_sms);
   const int units = a.n_entries * a.H * a.QT;
+  const int G = a.per_unit ? units : int(total_tiles_hint < p.num_sms ? total_tiles_hint : p.num_sms);
   if (hd == 128) {
-    attn_tc_kernel<128><<<G, 192, AttnSmem<128>::total, s>>>(*mq, *mk, *mv, a, td);
-    attn_combine_kernel<128><<<units, 128, 0, s>>>(a, td, G);
+    attn_tc_kernel<128><<<G, kAttnThreads, AttnSmem<128>::total, s>>>(*mq, *mk, *mv, a, td);
+    if (!a.per_unit) attn_combine_kernel<128><<<units, 128, 0, s>>>(a, td, G);
   } else {
-    attn_tc_kernel<64><<<G, 192, AttnSmem<64>::total, s>>>(*mq, *mk, *mv, a, td);
-    attn_combine_kernel<64><<<units, 128, 0, s>>>(a, td, G);
+    attn_tc_kernel<64><<<G, kAttnThreads, AttnSmem<64>::total, s>>>(*mq, *mk, *mv, a, td);
+    if (!a.per_unit) attn_combine_kernel<64><<<units, 128, 0, s>>>(a, td, G);
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {

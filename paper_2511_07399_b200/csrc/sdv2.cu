@@ -424,6 +424,7 @@ sdv2_status attention(sdv2_handle* h, const AttnArgs& aa, int Mrows_entries, dou
         const int Lk = aa.cross ? aa.Lk_cross : h->td_host_cur->e[e].nvalid * h->L;
         tiles += (long long)ta.H * ta.QT * ((Lk + kAttnBKV - 1) / kAttnBKV);
       }
+      ta.per_unit = attn_pick_per_unit((long long)Mrows_entries * ta.H * ta.QT, tiles, h->aplan.num_sms);
       const void *Kb, *Vb;
       long long kv_rows;
       if (aa.cross) {
@@ -1120,6 +1121,7 @@ extern "C" sdv2_status sdv2_debug_attention(const void* q, const void* K, const 
   ta.kv_row0 = 0;
   ta.kv_lane_rows = 0;
   const long long tiles = (long long)H * ta.QT * ((Lk + kAttnBKV - 1) / kAttnBKV);
+  ta.per_unit = getenv("SDV2_ATTN_PER_UNIT") ? atoi(getenv("SDV2_ATTN_PER_UNIT")) : 0;
   if (!tc_attention(s, ap, q, Lq, K, V, Lk, H * hd, hd, tiles, ta, static_cast<const TickDesc*>(scratch), &err)) {
     fprintf(stderr, "sdv2_debug_attention: %s\n", err.c_str());
     return SDV2_E_CUDA;
