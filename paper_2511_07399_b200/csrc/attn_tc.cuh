@@ -426,9 +426,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
 }
 
 // Merge the partial units (split between consecutive CTAs) in CTA order:
-// O = sum_k 2^(m_k - M) O_k / sum_k 2^(m_k - M) l_k.  One CTA per unit, thread = row.
+// O = sum_k 2^(m_k - M) O_k / sum_k 2^(m_k - M) l_k.  One CTA per unit; a warp per row,
+// lanes across the head dim (coalesced 512 B row reads).
 template <int HD>
-__global__ void __launch_bounds__(128) attn_combine_kernel(AttnTcArgs a, const TickDesc* __restrict__ td, int G) {
+__global__ void __launch_bounds__(256) attn_combine_kernel(AttnTcArgs a, const TickDesc* __restrict__ td, int G) {
+  constexpr int PL = HD / 32;   // columns per lane
   AttnGeo geo;
   geo.init(a, td);
   const int u = blockIdx.x;
@@ -436,46 +438,37 @@ __global__ void __launch_bounds__(128) attn_combine_kernel(AttnTcArgs a, const T
   if (e >= a.n_entries || geo.J[e] == 0) return;
   const long long off = geo.off[e] + (long long)w * geo.J[e];
   const int cf = geo.cta_of(off, G), cl = geo.cta_of(off + geo.J[e] - 1, G);
-  if (a.per_unit || cf == cl) return;   // one CTA covered the whole unit and wrote the final output   // one CTA covered the whole unit and wrote the final output
-  const int row = threadIdx.x;
+  if (a.per_unit || cf == cl) return;   // one CTA covered the whole unit and wrote the final output
   const int h = w / a.QT, q0 = (w % a.QT) * kAttnBQ;
-  float M = -INFINITY;
-  for (int cc = cf; cc <= cl; ++cc) {
-    const int slot = (cc == cf && geo.start(cc, G) < off) ? 1 : 0;
-    M = fmaxf(M, a.part_ml[((size_t(cc) * 2 + slot) * kAttnBQ + row) * 2]);
-  }
-  float den = 0.f;
-  float acc[HD];
-#pragma unroll
-  for (int i = 0; i < HD; ++i) acc[i] = 0.f;
-  for (int cc = cf; cc <= cl; ++cc) {
-    const int slot = (cc == cf && geo.start(cc, G) < off) ? 1 : 0;
-    const float* ml = a.part_ml + ((size_t(cc) * 2 + slot) * kAttnBQ + row) * 2;
-    const float wgt = exp2f(ml[0] - M);
-    den += wgt * ml[1];
-    const float4* po = reinterpret_cast<const float4*>(a.part_o + ((size_t(cc) * 2 + slot) * kAttnBQ + row) * HD);
-#pragma unroll
-    for (int i = 0; i < HD / 4; ++i) {
-      const float4 v = po[i];
-      acc[4 * i] += wgt * v.x;
-      acc[4 * i + 1] += wgt * v.y;
-      acc[4 * i + 2] += wgt * v.z;
-      acc[4 * i + 3] += wgt * v.w;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int slot_f = geo.start(cf, G) < off ? 1 : 0;
+  for (int row = warp; row < kAttnBQ; row += 8) {
+    const int qr = q0 + row;
+    if (qr >= a.L) break;
+    float M = -INFINITY;
+    for (int cc = cf; cc <= cl; ++cc) {
+      const int slot = cc == cf ? slot_f : 0;
+      M = fmaxf(M, a.part_ml[((size_t(cc) * 2 + slot) * kAttnBQ + row) * 2]);
     }
-  }
-  const int qr = q0 + row;
-  if (qr >= a.L) return;
-  const float inv = 1.f / den;
-  bf16* orow = reinterpret_cast<bf16*>(a.o) + size_t(e * a.L + qr) * a.ldo + h * HD;
+    float den = 0.f, acc[PL];
 #pragma unroll
-  for (int i = 0; i < HD / 8; ++i) {
-    uint32_t pk[4];
+    for (int i = 0; i < PL; ++i) acc[i] = 0.f;
+    for (int cc = cf; cc <= cl; ++cc) {
+      const int slot = cc == cf ? slot_f : 0;
+      const size_t base = (size_t(cc) * 2 + slot) * kAttnBQ + row;
+      const float wgt = exp2f(a.part_ml[base * 2] - M);
+      den += wgt * a.part_ml[base * 2 + 1];
+      const float* po = a.part_o + base * HD + lane * PL;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      __nv_bfloat162 b2 = __floats2bfloat162_rn(acc[8 * i + 2 * k] * inv, acc[8 * i + 2 * k + 1] * inv);
-      pk[k] = *reinterpret_cast<uint32_t*>(&b2);
+      for (int i = 0; i < PL; ++i) acc[i] += wgt * po[i];
     }
-    reinterpret_cast<uint4*>(orow)[i] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+    const float inv = 1.f / den;
+    bf16* orow = reinterpret_cast<bf16*>(a.o) + size_t(e * a.L + qr) * a.ldo + h * HD + lane * PL;
+#pragma unroll
+    for (int i = 0; i < PL; i += 2) {
+      __nv_bfloat162 b2 = __floats2bfloat162_rn(acc[i] * inv, acc[i + 1] * inv);
+      *reinterpret_cast<__nv_bfloat162*>(orow + i) = b2;
+    }
   }
 }
 
@@ -493,8 +486,9 @@ inline bool tc_attn_enabled() { return true; }
 // charging each unit boundary / merge about one tile of fixed cost.
 inline int attn_pick_per_unit(long long units, long long tiles, int num_sms) {
   const long long J = units ? (tiles + units - 1) / units : 1;
+  if (J <= 8) return 1;     // short key ranges (cross-attention): merge cost dominates
   const double per_unit = double((units + num_sms - 1) / num_sms) * double(J + 1);
-  const double streamk = double((tiles + num_sms - 1) / num_sms) + 3.0;
+  const double streamk = double((tiles + num_sms - 1) / num_sms) + 4.0;
   return per_unit <= streamk ? 1 : 0;
 }
 
@@ -547,10 +541,10 @@ inline bool tc_attention(cudaStream_t s, AttnPlan& p, const void* q, long long q
   const int G = a.per_unit ? units : int(total_tiles_hint < p.num_sms ? total_tiles_hint : p.num_sms);
   if (hd == 128) {
     attn_tc_kernel<128><<<G, kAttnThreads, AttnSmem<128>::total, s>>>(*mq, *mk, *mv, a, td);
-    if (!a.per_unit) attn_combine_kernel<128><<<units, 128, 0, s>>>(a, td, G);
+    if (!a.per_unit) attn_combine_kernel<128><<<units, 256, 0, s>>>(a, td, G);
   } else {
     attn_tc_kernel<64><<<G, kAttnThreads, AttnSmem<64>::total, s>>>(*mq, *mk, *mv, a, td);
-    if (!a.per_unit) attn_combine_kernel<64><<<units, 128, 0, s>>>(a, td, G);
+    if (!a.per_unit) attn_combine_kernel<64><<<units, 256, 0, s>>>(a, td, G);
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {

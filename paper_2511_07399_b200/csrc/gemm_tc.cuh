@@ -21,10 +21,17 @@
 
 namespace sdv2 {
 
-constexpr int kGemmBM = 128, kGemmBK = 64, kGemmStages = 4, kGemmMaxBN = 256;
+constexpr int kGemmBM = 128, kGemmBK = 64, kGemmMaxStages = 8, kGemmMaxBN = 256;
 constexpr int kGemmSmemA = kGemmBM * kGemmBK * 2;        // 16 KB
-constexpr int kGemmSmemB = kGemmMaxBN * kGemmBK * 2;     // 32 KB
-constexpr int kGemmSmem = kGemmStages * (kGemmSmemA + kGemmSmemB) + 1024 + 256;
+constexpr int kGemmSmem = 227 * 1024;                    // whole SM: as many stages as fit
+constexpr int kGemmThreads = 384;                        // 4 control warps + 8 epilogue warps
+
+// Stages of the TMA->MMA ring for a tile width: the ring must cover the L2/HBM latency
+// (about 1-2 us) at the MMA rate, so use all of shared memory.
+__host__ __device__ inline int gemm_stages(int BN) {
+  const int st = (kGemmSmem - 1024 - 512) / (kGemmSmemA + BN * kGemmBK * 2);
+  return st > kGemmMaxStages ? kGemmMaxStages : st;
+}
 
 template <int EPI, typename TOut>
 __device__ __forceinline__ void gemm_epilogue_chunk(const EpiArgs& ep, int r, int c0, int N, const uint32_t (&v)[32]) {
@@ -103,16 +110,18 @@ __device__ __forceinline__ void gemm_epilogue_chunk(const EpiArgs& ep, int r, in
 }
 
 template <int EPI, typename TOut>
-__global__ void __launch_bounds__(256, 1) gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA,
+__global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA,
                                                          const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
                                                          int BN, EpiArgs ep) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int kStages = gemm_stages(BN);
+  const int kSmemB = BN * kGemmBK * 2;      // multiple of 1024 (BN multiple of 32... 8 rows x 128 B)
   uint8_t* sA = smem;
-  uint8_t* sB = smem + kGemmStages * kGemmSmemA;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + kGemmStages * kGemmSmemB);
-  uint64_t* empty = full + kGemmStages;
-  uint64_t* tfull = empty + kGemmStages;
+  uint8_t* sB = smem + kStages * kGemmSmemA;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + kStages * kSmemB);
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -124,13 +133,13 @@ __global__ void __launch_bounds__(256, 1) gemm_tc_kernel(const __grid_constant__
   if (warp == 0 && lane == 0) {
     tc::tma_prefetch_desc(&tmA);
     tc::tma_prefetch_desc(&tmB);
-    for (int s = 0; s < kGemmStages; ++s) {
+    for (int s = 0; s < kStages; ++s) {
       tc::mbar_init(full + s, 1);
       tc::mbar_init(empty + s, 1);
     }
     for (int s = 0; s < 2; ++s) {
       tc::mbar_init(tfull + s, 1);
-      tc::mbar_init(tempty + s, 4);
+      tc::mbar_init(tempty + s, 8);
     }
     tc::fence_barrier_init();
   }
@@ -151,8 +160,8 @@ __global__ void __launch_bounds__(256, 1) gemm_tc_kernel(const __grid_constant__
           tc::mbar_wait(empty + stage, phase ^ 1);
           tc::mbar_expect_tx(full + stage, bytes);
           tc::tma_load_2d(sA + stage * kGemmSmemA, &tmA, full + stage, kb * kGemmBK, mb * kGemmBM);
-          tc::tma_load_2d(sB + stage * kGemmSmemB, &tmB, full + stage, kb * kGemmBK, nb * BN);
-          if (++stage == kGemmStages) {
+          tc::tma_load_2d(sB + stage * kSmemB, &tmB, full + stage, kb * kGemmBK, nb * BN);
+          if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
           }
@@ -174,14 +183,14 @@ __global__ void __launch_bounds__(256, 1) gemm_tc_kernel(const __grid_constant__
           tc::mbar_wait(full + stage, phase);
           tc::tc_fence_after();
           const uint32_t a0 = tc::smem_u32(sA + stage * kGemmSmemA);
-          const uint32_t b0 = tc::smem_u32(sB + stage * kGemmSmemB);
+          const uint32_t b0 = tc::smem_u32(sB + stage * kSmemB);
 #pragma unroll
           for (int k = 0; k < kGemmBK / 16; ++k) {
             tc::mma_bf16(d_tmem, tc::sw128_kmajor_desc(a0 + k * 32), tc::sw128_kmajor_desc(b0 + k * 32), idesc,
                          (kb | k) != 0);
           }
           tc::mma_commit(empty + stage);
-          if (++stage == kGemmStages) {
+          if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
           }
@@ -194,7 +203,8 @@ __global__ void __launch_bounds__(256, 1) gemm_tc_kernel(const __grid_constant__
       }
     }
   } else if (warp >= 4) {
-    const int q = warp - 4;   // TMEM lane quarter accessible by this warp
+    const int q = warp & 3;             // TMEM lane quarter accessible by this warp
+    const int wg = (warp - 4) >> 2;     // epilogue warpgroup: 32-column chunks c % 2 == wg
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
@@ -202,7 +212,7 @@ __global__ void __launch_bounds__(256, 1) gemm_tc_kernel(const __grid_constant__
       tc::mbar_wait(tfull + acc, acc_phase);
       tc::tc_fence_after();
       const int r = mb * kGemmBM + q * 32 + lane;
-      for (int c = 0; c < BN; c += 32) {
+      for (int c = wg * 32; c < BN; c += 64) {
         uint32_t v[32];
         tc::tmem_ld32(tmem + (uint32_t(q * 32) << 16) + uint32_t(acc * BN + c), v);
         tc::tmem_ld_wait();
@@ -318,11 +328,11 @@ inline bool tc_gemm(cudaStream_t s, TmaGemmPlan& p, const void* A, const void* W
   const int tiles = ((M + kGemmBM - 1) / kGemmBM) * ((N + BN - 1) / BN);
   const int grid = tiles < p.num_sms ? tiles : p.num_sms;
   switch (epi) {
-    case EPI_STORE: gemm_tc_kernel<EPI_STORE, bf16><<<grid, 256, kGemmSmem, s>>>(*ma, *mb, M, N, K, BN, ep); break;
-    case EPI_GELU: gemm_tc_kernel<EPI_GELU, bf16><<<grid, 256, kGemmSmem, s>>>(*ma, *mb, M, N, K, BN, ep); break;
-    case EPI_RES_GATE: gemm_tc_kernel<EPI_RES_GATE, bf16><<<grid, 256, kGemmSmem, s>>>(*ma, *mb, M, N, K, BN, ep); break;
-    case EPI_STORE_F32: gemm_tc_kernel<EPI_STORE, float><<<grid, 256, kGemmSmem, s>>>(*ma, *mb, M, N, K, BN, ep); break;
-    default: gemm_tc_kernel<EPI_RES, bf16><<<grid, 256, kGemmSmem, s>>>(*ma, *mb, M, N, K, BN, ep); break;
+    case EPI_STORE: gemm_tc_kernel<EPI_STORE, bf16><<<grid, kGemmThreads, kGemmSmem, s>>>(*ma, *mb, M, N, K, BN, ep); break;
+    case EPI_GELU: gemm_tc_kernel<EPI_GELU, bf16><<<grid, kGemmThreads, kGemmSmem, s>>>(*ma, *mb, M, N, K, BN, ep); break;
+    case EPI_RES_GATE: gemm_tc_kernel<EPI_RES_GATE, bf16><<<grid, kGemmThreads, kGemmSmem, s>>>(*ma, *mb, M, N, K, BN, ep); break;
+    case EPI_STORE_F32: gemm_tc_kernel<EPI_STORE, float><<<grid, kGemmThreads, kGemmSmem, s>>>(*ma, *mb, M, N, K, BN, ep); break;
+    default: gemm_tc_kernel<EPI_RES, bf16><<<grid, kGemmThreads, kGemmSmem, s>>>(*ma, *mb, M, N, K, BN, ep); break;
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
