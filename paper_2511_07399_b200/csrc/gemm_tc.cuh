@@ -109,7 +109,11 @@ __device__ __forceinline__ void gemm_epilogue_chunk(const EpiArgs& ep, int r, in
   }
 }
 
-template <int EPI, typename TOut>
+// MC = CTAs per cluster along M (1 or 2).  With MC = 2 the two CTAs work on
+// consecutive m-blocks of the same n-block: each loads its own A tile and one half of
+// the shared W tile, multicast into both CTAs' shared memory, so every SM pulls
+// 16 KB + BN*64 B per k-block from L2 instead of 16 KB + BN*128 B.
+template <int EPI, typename TOut, int MC>
 __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA,
                                                          const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
                                                          int BN, EpiArgs ep) {
@@ -127,15 +131,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int num_m = (M + kGemmBM - 1) / kGemmBM, num_n = (N + BN - 1) / BN;
-  const int tiles = num_m * num_n;
+  const int num_mg = (num_m + MC - 1) / MC;                 // m-block groups (one per cluster tile)
+  const int tiles = num_mg * num_n;
   const int kblocks = K / kGemmBK;
+  const int cr = MC > 1 ? int(tc::cluster_ctarank()) : 0;
+  const int cid = blockIdx.x / MC, ncl = gridDim.x / MC;
+  const uint16_t mc_mask = uint16_t((1u << MC) - 1);
 
   if (warp == 0 && lane == 0) {
     tc::tma_prefetch_desc(&tmA);
     tc::tma_prefetch_desc(&tmB);
     for (int s = 0; s < kStages; ++s) {
       tc::mbar_init(full + s, 1);
-      tc::mbar_init(empty + s, 1);
+      tc::mbar_init(empty + s, MC);      // both CTAs' MMAs must release a stage (MC = 2)
     }
     for (int s = 0; s < 2; ++s) {
       tc::mbar_init(tfull + s, 1);
@@ -145,7 +153,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
   }
   if (warp == 2) tc::tmem_alloc(tmem_slot, 512);
   tc::tc_fence_before();
-  __syncthreads();
+  if (MC > 1) tc::cluster_sync();   // peer barriers initialised before any multicast
+  else __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -154,13 +163,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
       int stage = 0;
       uint32_t phase = 0;
       const uint32_t bytes = uint32_t(kGemmSmemA) + uint32_t(BN) * kGemmBK * 2;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-        const int mb = t % num_m, nb = t / num_m;
+      const int bh = BN / MC;   // W rows this CTA loads (and multicasts)
+      for (int t = cid; t < tiles; t += ncl) {
+        const int mb = (t % num_mg) * MC + cr, nb = t / num_mg;
         for (int kb = 0; kb < kblocks; ++kb) {
           tc::mbar_wait(empty + stage, phase ^ 1);
           tc::mbar_expect_tx(full + stage, bytes);
           tc::tma_load_2d(sA + stage * kGemmSmemA, &tmA, full + stage, kb * kGemmBK, mb * kGemmBM);
-          tc::tma_load_2d(sB + stage * kSmemB, &tmB, full + stage, kb * kGemmBK, nb * BN);
+          if (MC > 1)
+            tc::tma_load_2d_mc(sB + stage * kSmemB + cr * bh * 128, &tmB, full + stage, kb * kGemmBK,
+                               nb * BN + cr * bh, mc_mask);
+          else
+            tc::tma_load_2d(sB + stage * kSmemB, &tmB, full + stage, kb * kGemmBK, nb * BN);
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
@@ -175,7 +189,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      for (int t = cid; t < tiles; t += ncl) {
         tc::mbar_wait(tempty + acc, acc_phase ^ 1);
         tc::tc_fence_after();
         const uint32_t d_tmem = tmem + uint32_t(acc * BN);
@@ -189,7 +203,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
             tc::mma_bf16(d_tmem, tc::sw128_kmajor_desc(a0 + k * 32), tc::sw128_kmajor_desc(b0 + k * 32), idesc,
                          (kb | k) != 0);
           }
-          tc::mma_commit(empty + stage);
+          if (MC > 1) tc::mma_commit_mc(empty + stage, mc_mask);
+          else tc::mma_commit(empty + stage);
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
@@ -207,8 +222,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
     const int wg = (warp - 4) >> 2;     // epilogue warpgroup: 32-column chunks c % 2 == wg
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-      const int mb = t % num_m, nb = t / num_m;
+    for (int t = cid; t < tiles; t += ncl) {
+      const int mb = (t % num_mg) * MC + cr, nb = t / num_mg;
       tc::mbar_wait(tfull + acc, acc_phase);
       tc::tc_fence_after();
       const int r = mb * kGemmBM + q * 32 + lane;
@@ -229,7 +244,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
     }
   }
   tc::tc_fence_before();
-  __syncthreads();
+  if (MC > 1) tc::cluster_sync();   // no CTA exits while its peer may still multicast into it
+  else __syncthreads();
   if (warp == 2) {
     tc::tc_fence_after();
     tc::tmem_dealloc(tmem, 512);
@@ -249,6 +265,11 @@ struct TmaGemmPlan {
 
 inline bool tc_gemm_enabled() { return true; }
 
+template <int EPI, typename TOut, int MC>
+inline void gemm_set_attr() {
+  cudaFuncSetAttribute(gemm_tc_kernel<EPI, TOut, MC>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmem);
+}
+
 inline bool tc_gemm_plan(TmaGemmPlan& p, std::string* err) {
   void* fn = nullptr;
   cudaDriverEntryPointQueryResult q;
@@ -260,11 +281,11 @@ inline bool tc_gemm_plan(TmaGemmPlan& p, std::string* err) {
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&p.num_sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaFuncSetAttribute(gemm_tc_kernel<EPI_STORE, bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmem);
-  cudaFuncSetAttribute(gemm_tc_kernel<EPI_GELU, bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmem);
-  cudaFuncSetAttribute(gemm_tc_kernel<EPI_RES_GATE, bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmem);
-  cudaFuncSetAttribute(gemm_tc_kernel<EPI_RES, bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmem);
-  cudaFuncSetAttribute(gemm_tc_kernel<EPI_STORE, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmem);
+  gemm_set_attr<EPI_STORE, bf16, 1>(); gemm_set_attr<EPI_STORE, bf16, 2>();
+  gemm_set_attr<EPI_GELU, bf16, 1>(); gemm_set_attr<EPI_GELU, bf16, 2>();
+  gemm_set_attr<EPI_RES_GATE, bf16, 1>(); gemm_set_attr<EPI_RES_GATE, bf16, 2>();
+  gemm_set_attr<EPI_RES, bf16, 1>(); gemm_set_attr<EPI_RES, bf16, 2>();
+  gemm_set_attr<EPI_STORE, float, 1>(); gemm_set_attr<EPI_STORE, float, 2>();
   return true;
 }
 
@@ -295,24 +316,61 @@ inline const CUtensorMap* tc_map(TmaGemmPlan& p, const void* ptr, int rows, int 
   return &(p.maps.emplace(key, m).first->second);
 }
 
-// Tile width N chosen to balance (M/128) x (N/BN) tiles over the SMs: maximise
-// useful-column fraction x wave efficiency.
-inline int tc_pick_bn(int M, int N, int sms) {
+// Tile width N chosen to balance (M/128/MC) x (N/BN) cluster tiles over the SMs:
+// maximise useful-column fraction x useful-row fraction x wave efficiency.
+inline int tc_pick_bn(int M, int N, int sms, int MC) {
   const int num_m = (M + kGemmBM - 1) / kGemmBM;
+  const int num_mg = (num_m + MC - 1) / MC;
+  const int slots = sms / MC;
   int best = 256;
   double best_eff = -1.0;
   for (int bn = 256; bn >= 64; bn -= 32) {
     const int num_n = (N + bn - 1) / bn;
-    const int tiles = num_m * num_n;
-    const int waves = (tiles + sms - 1) / sms;
-    const double eff = double(N) / double(num_n * bn) * double(tiles) / double(waves * sms);
-    // prefer wider tiles on ties (fewer, larger MMAs; less A re-read)
-    if (eff > best_eff + 1e-3) {
+    const int tiles = num_mg * num_n;
+    const int waves = (tiles + slots - 1) / slots;
+    const double eff = double(N) / double(num_n * bn) * double(num_m) / double(num_mg * MC) * double(tiles) /
+                       double(waves * slots);
+    if (eff > best_eff + 1e-3) {   // prefer wider tiles on ties
       best_eff = eff;
       best = bn;
     }
   }
   return best;
+}
+
+template <int EPI, typename TOut, int MC>
+inline cudaError_t gemm_launch(cudaStream_t s, int grid, const CUtensorMap& ma, const CUtensorMap& mb, int M, int N,
+                               int K, int BN, const EpiArgs& ep) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = kGemmSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = MC;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<EPI, TOut, MC>, ma, mb, M, N, K, BN, ep);
+}
+
+template <int MC>
+inline cudaError_t gemm_dispatch(cudaStream_t s, int grid, const CUtensorMap& ma, const CUtensorMap& mb, int M, int N,
+                                 int K, int BN, int epi, const EpiArgs& ep) {
+  switch (epi) {
+    case EPI_STORE: return gemm_launch<EPI_STORE, bf16, MC>(s, grid, ma, mb, M, N, K, BN, ep);
+    case EPI_GELU: return gemm_launch<EPI_GELU, bf16, MC>(s, grid, ma, mb, M, N, K, BN, ep);
+    case EPI_RES_GATE: return gemm_launch<EPI_RES_GATE, bf16, MC>(s, grid, ma, mb, M, N, K, BN, ep);
+    case EPI_STORE_F32: return gemm_launch<EPI_STORE, float, MC>(s, grid, ma, mb, M, N, K, BN, ep);
+    default: return gemm_launch<EPI_RES, bf16, MC>(s, grid, ma, mb, M, N, K, BN, ep);
+  }
+}
+
+inline int tc_gemm_default_mc() {
+  const char* e = getenv("SDV2_GEMM_MC");
+  return e ? atoi(e) : 2;
 }
 
 inline bool tc_gemm(cudaStream_t s, TmaGemmPlan& p, const void* A, const void* W, int M, int N, int K, int epi,
@@ -321,20 +379,18 @@ inline bool tc_gemm(cudaStream_t s, TmaGemmPlan& p, const void* A, const void* W
     *err = "tc_gemm: K % 64 or N % 16";
     return false;
   }
-  const int BN = tc_pick_bn(M, N, p.num_sms);
+  const int num_m = (M + kGemmBM - 1) / kGemmBM;
+  const int MC = (num_m >= 2 && tc_gemm_default_mc() == 2) ? 2 : 1;
+  const int BN = tc_pick_bn(M, N, p.num_sms, MC);
   const CUtensorMap* ma = tc_map(p, A, a_rows_alloc > 0 ? a_rows_alloc : M, K, kGemmBM, err);
-  const CUtensorMap* mb = tc_map(p, W, N, K, BN, err);
+  const CUtensorMap* mb = tc_map(p, W, N, K, BN / MC, err);
   if (!ma || !mb) return false;
-  const int tiles = ((M + kGemmBM - 1) / kGemmBM) * ((N + BN - 1) / BN);
-  const int grid = tiles < p.num_sms ? tiles : p.num_sms;
-  switch (epi) {
-    case EPI_STORE: gemm_tc_kernel<EPI_STORE, bf16><<<grid, kGemmThreads, kGemmSmem, s>>>(*ma, *mb, M, N, K, BN, ep); break;
-    case EPI_GELU: gemm_tc_kernel<EPI_GELU, bf16><<<grid, kGemmThreads, kGemmSmem, s>>>(*ma, *mb, M, N, K, BN, ep); break;
-    case EPI_RES_GATE: gemm_tc_kernel<EPI_RES_GATE, bf16><<<grid, kGemmThreads, kGemmSmem, s>>>(*ma, *mb, M, N, K, BN, ep); break;
-    case EPI_STORE_F32: gemm_tc_kernel<EPI_STORE, float><<<grid, kGemmThreads, kGemmSmem, s>>>(*ma, *mb, M, N, K, BN, ep); break;
-    default: gemm_tc_kernel<EPI_RES, bf16><<<grid, kGemmThreads, kGemmSmem, s>>>(*ma, *mb, M, N, K, BN, ep); break;
-  }
-  cudaError_t e = cudaGetLastError();
+  const int tiles = ((num_m + MC - 1) / MC) * ((N + BN - 1) / BN);
+  const int slots = p.num_sms / MC;
+  const int grid = MC * (tiles < slots ? tiles : slots);
+  cudaError_t e = MC == 2 ? gemm_dispatch<2>(s, grid, *ma, *mb, M, N, K, BN, epi, ep)
+                          : gemm_dispatch<1>(s, grid, *ma, *mb, M, N, K, BN, epi, ep);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     *err = std::string("gemm_tc launch: ") + cudaGetErrorString(e);
     return false;
