@@ -117,6 +117,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 18);
   float* xch = reinterpret_cast<float*>(bar + 20);   // [2 tiles][2 halves][128] row-max exchange + [2][128] sums
 
+  pdl_wait();      // q, K/V lanes and o are produced / consumed by the neighbouring kernels
+  pdl_trigger();
   AttnGeo geo;
   geo.init(a, td);
   const int G = gridDim.x, c = blockIdx.x;
@@ -430,6 +432,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
 // lanes across the head dim (coalesced 512 B row reads).
 template <int HD>
 __global__ void __launch_bounds__(256) attn_combine_kernel(AttnTcArgs a, const TickDesc* __restrict__ td, int G) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int PL = HD / 32;   // columns per lane
   AttnGeo geo;
   geo.init(a, td);
@@ -532,21 +536,34 @@ inline const CUtensorMap* attn_map(AttnPlan& p, const void* base, long long rows
 // (host estimate of the unit x key-tile space) only sizes the grid: min(SMs, tiles).
 inline bool tc_attention(cudaStream_t s, AttnPlan& p, const void* q, long long q_rows, const void* Kbase,
                          const void* Vbase, long long kv_rows, int d, int hd, long long total_tiles_hint,
-                         const AttnTcArgs& a, const TickDesc* td, std::string* err) {
+                         const AttnTcArgs& a, const TickDesc* td, std::string* err, bool pdl = false) {
   const CUtensorMap* mq = attn_map(p, q, q_rows, d, kAttnBQ, err);
   const CUtensorMap* mk = attn_map(p, Kbase, kv_rows, d, kAttnBKV, err);
   const CUtensorMap* mv = attn_map(p, Vbase, kv_rows, d, kAttnBKV, err);
   if (!mq || !mk || !mv) return false;
   const int units = a.n_entries * a.H * a.QT;
   const int G = a.per_unit ? units : int(total_tiles_hint < p.num_sms ? total_tiles_hint : p.num_sms);
-  if (hd == 128) {
-    attn_tc_kernel<128><<<G, kAttnThreads, AttnSmem<128>::total, s>>>(*mq, *mk, *mv, a, td);
-    if (!a.per_unit) attn_combine_kernel<128><<<units, 256, 0, s>>>(a, td, G);
-  } else {
-    attn_tc_kernel<64><<<G, kAttnThreads, AttnSmem<64>::total, s>>>(*mq, *mk, *mv, a, td);
-    if (!a.per_unit) attn_combine_kernel<64><<<units, 256, 0, s>>>(a, td, G);
+  cudaLaunchConfig_t cfg{};
+  cfg.blockDim = dim3(kAttnThreads);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  cudaError_t e;
+  cfg.gridDim = dim3(G);
+  cfg.dynamicSmemBytes = hd == 128 ? AttnSmem<128>::total : AttnSmem<64>::total;
+  e = hd == 128 ? cudaLaunchKernelEx(&cfg, attn_tc_kernel<128>, *mq, *mk, *mv, a, td)
+                : cudaLaunchKernelEx(&cfg, attn_tc_kernel<64>, *mq, *mk, *mv, a, td);
+  if (e == cudaSuccess && !a.per_unit) {
+    cfg.gridDim = dim3(units);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = 0;
+    e = hd == 128 ? cudaLaunchKernelEx(&cfg, attn_combine_kernel<128>, a, td, G)
+                  : cudaLaunchKernelEx(&cfg, attn_combine_kernel<64>, a, td, G);
   }
-  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     *err = std::string("attn_tc launch: ") + cudaGetErrorString(e);
     return false;

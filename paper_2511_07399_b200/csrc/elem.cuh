@@ -59,6 +59,8 @@ struct ModArgs {
 template <typename TA, int NV>
 __global__ void __launch_bounds__(256) norm_mod2_kernel(const float* __restrict__ x, TA* __restrict__ out, int rows,
                                                         int d, int L, ModArgs m, float eps, int center) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float red[2][2][2 * (kRowThreads / 32)];
   const int sub = threadIdx.x / kRowThreads, t = threadIdx.x % kRowThreads;
   const int r = blockIdx.x * 2 + sub;
@@ -165,6 +167,8 @@ __global__ void __launch_bounds__(256) qkv_post2_kernel(const TA* __restrict__ q
                                                         const float* __restrict__ gq, const float* __restrict__ gk,
                                                         const TickDesc* __restrict__ td, RopeTabs R, int rows, int d,
                                                         int hd, int L, int hn, int wn, int T, int S, float eps) {
+  pdl_wait();
+  pdl_trigger();
   using U = Unit<TA>;
   constexpr int UN = U::N;
   __shared__ float red[2][2 * (kRowThreads / 32)];
@@ -248,6 +252,8 @@ __global__ void __launch_bounds__(256) qkv_post2_kernel(const TA* __restrict__ q
 template <typename TA, int kMaxU>
 __global__ void __launch_bounds__(256) rms_rows2_kernel(TA* __restrict__ y, const float* __restrict__ g, int rows, int d,
                                                         float eps) {
+  pdl_wait();
+  pdl_trigger();
   using U = Unit<TA>;
   constexpr int UN = U::N;
   __shared__ float red[2][2 * (kRowThreads / 32)];
@@ -288,6 +294,8 @@ __global__ void __launch_bounds__(256) rms_rows2_kernel(TA* __restrict__ y, cons
 __global__ void __launch_bounds__(1024) motion_kernel(const float* __restrict__ chunk, float* prev, CtrlState* st,
                                                       float* sig, float* sign, const TickDesc* td, StreamCfg cfg,
                                                       int CHW, int HW, int T) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ double red[32];
   const int tid = threadIdx.x, nt = blockDim.x;
   const int C = CHW / (HW * T);
@@ -347,6 +355,8 @@ __global__ void __launch_bounds__(1024) motion_kernel(const float* __restrict__ 
 __global__ void __launch_bounds__(256) blend_kernel(const float* __restrict__ chunk, float* __restrict__ lat0,
                                                     const float* __restrict__ sig, const TickDesc* __restrict__ td,
                                                     unsigned long long seed, int CTHW) {
+  pdl_wait();
+  pdl_trigger();
   const int X = td->e[0].X;
   const float s0 = sig[0];
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < CTHW; i += gridDim.x * blockDim.x) {
@@ -358,6 +368,8 @@ __global__ void __launch_bounds__(256) blend_kernel(const float* __restrict__ ch
 // Patchify (C.1): u[r, c*4 + a*2 + b] = v_e[c, f, 2i+a, 2jj+b], fp32.
 __global__ void patchify_kernel(const float* __restrict__ lat, float* __restrict__ u, int rows, int L, int C, int T,
                                 int h, int w) {
+  pdl_wait();
+  pdl_trigger();
   const int P = 4 * C, hn = h / 2, wn = w / 2;
   const size_t CTHW = size_t(C) * T * h * w;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < rows * P; i += gridDim.x * blockDim.x) {
@@ -377,6 +389,8 @@ __global__ void __launch_bounds__(256) flow_kernel(const float* __restrict__ y, 
                                                    float* __restrict__ out, float* __restrict__ ring_out,
                                                    const TickDesc* __restrict__ td, int n_act, int L, int C, int T,
                                                    int h, int w, int n, unsigned long long seed) {
+  pdl_wait();
+  pdl_trigger();
   const int P = 4 * C, hn = h / 2, wn = w / 2;
   const int CTHW = C * T * h * w;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_act * CTHW; i += gridDim.x * blockDim.x) {
@@ -403,6 +417,8 @@ template <typename TW>
 __global__ void __launch_bounds__(256) gemv2_kernel(const TW* __restrict__ W, const float* __restrict__ b,
                                                     const float* __restrict__ in, float* __restrict__ out, int n,
                                                     int R, int Kd, int pre_silu) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ float xs[];   // [n][Kd]
   for (int i = threadIdx.x; i < n * Kd; i += blockDim.x) {
     float z = in[i];

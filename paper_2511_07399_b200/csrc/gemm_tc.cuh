@@ -137,6 +137,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
   const int cr = MC > 1 ? int(tc::cluster_ctarank()) : 0;
   const int cid = blockIdx.x / MC, ncl = gridDim.x / MC;
   const uint16_t mc_mask = uint16_t((1u << MC) - 1);
+  if (threadIdx.x == 0) pdl_trigger();
 
   if (warp == 0 && lane == 0) {
     tc::tma_prefetch_desc(&tmA);
@@ -164,17 +165,37 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
       uint32_t phase = 0;
       const uint32_t bytes = uint32_t(kGemmSmemA) + uint32_t(BN) * kGemmBK * 2;
       const int bh = BN / MC;   // W rows this CTA loads (and multicasts)
+      auto load_w = [&](int st, int kb, int nb) {
+        if (MC > 1)
+          tc::tma_load_2d_mc(sB + st * kSmemB + cr * bh * 128, &tmB, full + st, kb * kGemmBK, nb * BN + cr * bh,
+                             mc_mask);
+        else
+          tc::tma_load_2d(sB + st * kSmemB, &tmB, full + st, kb * kGemmBK, nb * BN);
+      };
+      // Weights never change: prefetch the first ring of W tiles before waiting for the
+      // upstream kernel (PDL), then stream the activations.
+      int pre = 0;
+      if (cid < tiles && MC == 1) {
+        const int nb0 = cid / num_mg;
+        pre = kblocks < kStages ? kblocks : kStages;
+        for (int kb = 0; kb < pre; ++kb) {
+          tc::mbar_expect_tx(full + kb, bytes);
+          load_w(kb, kb, nb0);
+        }
+      }
+      pdl_wait();
       for (int t = cid; t < tiles; t += ncl) {
         const int mb = (t % num_mg) * MC + cr, nb = t / num_mg;
         for (int kb = 0; kb < kblocks; ++kb) {
-          tc::mbar_wait(empty + stage, phase ^ 1);
-          tc::mbar_expect_tx(full + stage, bytes);
-          tc::tma_load_2d(sA + stage * kGemmSmemA, &tmA, full + stage, kb * kGemmBK, mb * kGemmBM);
-          if (MC > 1)
-            tc::tma_load_2d_mc(sB + stage * kSmemB + cr * bh * 128, &tmB, full + stage, kb * kGemmBK,
-                               nb * BN + cr * bh, mc_mask);
-          else
-            tc::tma_load_2d(sB + stage * kSmemB, &tmB, full + stage, kb * kGemmBK, nb * BN);
+          if (pre > 0) {   // first tile, W already in flight for this stage
+            tc::tma_load_2d(sA + stage * kGemmSmemA, &tmA, full + stage, kb * kGemmBK, mb * kGemmBM);
+            --pre;
+          } else {
+            tc::mbar_wait(empty + stage, phase ^ 1);
+            tc::mbar_expect_tx(full + stage, bytes);
+            tc::tma_load_2d(sA + stage * kGemmSmemA, &tmA, full + stage, kb * kGemmBK, mb * kGemmBM);
+            load_w(stage, kb, nb);
+          }
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
@@ -218,6 +239,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
       }
     }
   } else if (warp >= 4) {
+    pdl_wait();                         // epilogue reads x / gates produced upstream
     const int q = warp & 3;             // TMEM lane quarter accessible by this warp
     const int wg = (warp - 4) >> 2;     // epilogue warpgroup: 32-column chunks c % 2 == wg
     int acc = 0;
@@ -338,6 +360,13 @@ inline int tc_pick_bn(int M, int N, int sms, int MC) {
   return best;
 }
 
+// PDL for the projection GEMMs (set per call by the library; thread-local so the
+// kernel-level test hook launches without it).
+inline bool& gemm_pdl_flag() {
+  static thread_local bool f = false;
+  return f;
+}
+
 template <int EPI, typename TOut, int MC>
 inline cudaError_t gemm_launch(cudaStream_t s, int grid, const CUtensorMap& ma, const CUtensorMap& mb, int M, int N,
                                int K, int BN, const EpiArgs& ep) {
@@ -346,13 +375,15 @@ inline cudaError_t gemm_launch(cudaStream_t s, int grid, const CUtensorMap& ma, 
   cfg.blockDim = dim3(kGemmThreads);
   cfg.dynamicSmemBytes = kGemmSmem;
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = MC;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = gemm_pdl_flag() ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<EPI, TOut, MC>, ma, mb, M, N, K, BN, ep);
 }
 
@@ -370,7 +401,7 @@ inline cudaError_t gemm_dispatch(cudaStream_t s, int grid, const CUtensorMap& ma
 
 inline int tc_gemm_default_mc() {
   const char* e = getenv("SDV2_GEMM_MC");
-  return e ? atoi(e) : 2;
+  return e ? atoi(e) : 1;
 }
 
 inline bool tc_gemm(cudaStream_t s, TmaGemmPlan& p, const void* A, const void* W, int M, int N, int K, int epi,

@@ -40,6 +40,8 @@ __device__ __forceinline__ float sigma_of(const CtrlState* st, const StreamCfg& 
 // packet; rank 0 also needs the ring-closure latents assembled: lat[j] = ring_in[j-1].
 __global__ void assemble_kernel(const float* __restrict__ ring_in, float* __restrict__ lat, const TickDesc* td,
                                 int n, int CTHW) {
+  pdl_wait();
+  pdl_trigger();
   const int j = blockIdx.y + 1;
   if (j >= n || !td->e[j].active) return;
   const float4* src = reinterpret_cast<const float4*>(ring_in + size_t(j - 1) * CTHW);
@@ -51,6 +53,8 @@ __global__ void assemble_kernel(const float* __restrict__ ring_in, float* __rest
 // Time conditioning (C.2): sinusoid(1000 sigma) in fp64, then GEMVs.
 // ----------------------------------------------------------------------------
 __global__ void sinusoid_kernel(const float* __restrict__ sig, float* __restrict__ emb, int n, int dim) {
+  pdl_wait();
+  pdl_trigger();
   const int e = blockIdx.x;
   const int half = dim / 2;
   const double t = 1000.0 * double(sig[e]);
@@ -67,6 +71,8 @@ template <typename TIn, typename TOut>
 __global__ void __launch_bounds__(256) rms_rows_kernel(const TIn* __restrict__ y, TOut* __restrict__ out,
                                                        const float* __restrict__ g, int rows, int d, int ld_in,
                                                        float eps) {
+  pdl_wait();
+  pdl_trigger();
   const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (r >= rows) return;
   const TIn* yr = y + size_t(r) * ld_in;
@@ -113,6 +119,8 @@ template <typename TA>
 __global__ void __launch_bounds__(256) rebase_kernel(TA* __restrict__ K, const TickDesc* __restrict__ td, RopeTabs R,
                                                      int nblocks, int n, int S, int m, int W, int L, int d, int hd,
                                                      int T_reset) {
+  pdl_wait();
+  pdl_trigger();
   const int j = blockIdx.y;
   if (!td->e[j].active || !td->e[j].rebase) return;
   const size_t rows = size_t(nblocks) * W * L;
@@ -179,6 +187,8 @@ __device__ __forceinline__ void epi_store(const EpiArgs& ep, int r, int c, int N
 template <typename TIn, typename TW, typename TOut, int EPI>
 __global__ void __launch_bounds__(256) gemm_simt_kernel(const TIn* __restrict__ A, const TW* __restrict__ Wt, int M,
                                                         int N, int K, int lda, int ldw, EpiArgs ep) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float As[16][64 + 4];
   __shared__ float Ws[16][64 + 4];
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
@@ -237,6 +247,8 @@ struct AttnArgs {
 
 template <typename TA, int HD>
 __global__ void __launch_bounds__(128) attn_simt_kernel(AttnArgs a, const TickDesc* __restrict__ td) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int QT = 16, KT = HD == 128 ? 32 : 64;
   __shared__ float qs[QT][HD + 1];
   __shared__ float ks[KT][HD + 1];

@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <utility>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -143,6 +144,7 @@ struct sdv2_handle {
   TickDesc* td_host_cur = nullptr;
   // CUDA graphs of the call body, keyed by (active entries, call parity)
   bool graphs = true;
+  bool pdl = true;        // programmatic dependent launch of the per-call kernels
   cudaGraphExec_t graph_exec[2 * (kMaxSteps + 1)] = {};
   int64_t graph_launches[2 * (kMaxSteps + 1)] = {};
   // profiling (sdv2_profile_enable): event pairs around each launch, per class
@@ -393,7 +395,10 @@ sdv2_status gemm_act(sdv2_handle* h, const void* A, const void* W, int M, int N,
                                           epi, ep);
   if (tc_gemm_enabled()) {
     ++h->launches;
-    return tc_gemm(h->stream, h->gplan, A, W, M, N, K, epi, ep, &h->err) ? SDV2_OK : SDV2_E_CUDA;
+    gemm_pdl_flag() = h->pdl;
+    const bool ok = tc_gemm(h->stream, h->gplan, A, W, M, N, K, epi, ep, &h->err);
+    gemm_pdl_flag() = false;
+    return ok ? SDV2_OK : SDV2_E_CUDA;
   }
   return gemm_simt<bf16, bf16, bf16>(h, static_cast<const bf16*>(A), static_cast<const bf16*>(W), M, N, K, K, epi, ep);
 }
@@ -440,7 +445,7 @@ sdv2_status attention(sdv2_handle* h, const AttnArgs& aa, int Mrows_entries, dou
       }
       ++h->launches;   // + the combine kernel
       return tc_attention(h->stream, h->aplan, aa.q, h->Mmax, Kb, Vb, kv_rows, h->d, h->hd, tiles, ta, h->td_dev,
-                          &h->err) ? SDV2_OK : SDV2_E_CUDA;
+                          &h->err, h->pdl) ? SDV2_OK : SDV2_E_CUDA;
     }
     if (h->hd == 64) attn_simt_kernel<bf16, 64><<<grid, 128, 0, h->stream>>>(aa, h->td_dev);
     else attn_simt_kernel<bf16, 128><<<grid, 128, 0, h->stream>>>(aa, h->td_dev);
@@ -449,14 +454,34 @@ sdv2_status attention(sdv2_handle* h, const AttnArgs& aa, int Mrows_entries, dou
   return SDV2_OK;
 }
 
+// Every per-call kernel is launched with programmatic dependent launch (PDL): its
+// prologue (barrier init, TMEM alloc, descriptor / weight prefetch) overlaps the tail of
+// the previous kernel; each kernel executes griddepcontrol.wait before touching data
+// produced upstream.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                     Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 template <typename TA>
 sdv2_status launch_norm_args(sdv2_handle* h, int rows, const ModArgs& m) {
   const int nv = (h->d / 4 + kRowThreads - 1) / kRowThreads;
   if (nv <= 4)
-    norm_mod2_kernel<TA, 4><<<(rows + 1) / 2, 256, 0, h->stream>>>(h->st.x, static_cast<TA*>(h->a), rows, h->d, h->L,
+    launch_k(h->pdl, norm_mod2_kernel<TA, 4>, dim3((rows + 1) / 2), dim3(256), 0, h->stream, h->st.x, static_cast<TA*>(h->a), rows, h->d, h->L,
                                                                     m, h->md.eps, h->md.norm_center);
   else
-    norm_mod2_kernel<TA, 16><<<(rows + 1) / 2, 256, 0, h->stream>>>(h->st.x, static_cast<TA*>(h->a), rows, h->d, h->L,
+    launch_k(h->pdl, norm_mod2_kernel<TA, 16>, dim3((rows + 1) / 2), dim3(256), 0, h->stream, h->st.x, static_cast<TA*>(h->a), rows, h->d, h->L,
                                                                      m, h->md.eps, h->md.norm_center);
   CKL();
   return SDV2_OK;
@@ -504,11 +529,11 @@ sdv2_status run_block(sdv2_handle* h, int bl, int rows, int n_act) {
   {
     const int units_pt = (d / (16 / int(sizeof(TA))) + kRowThreads - 1) / kRowThreads;
     if (units_pt <= 2)
-      qkv_post2_kernel<TA, 2><<<(rows + 1) / 2, 256, 0, h->stream>>>(
+      launch_k(h->pdl, qkv_post2_kernel<TA, 2>, dim3((rows + 1) / 2), dim3(256), 0, h->stream, 
           static_cast<const TA*>(h->qkv), static_cast<TA*>(h->q), Kb, Vb, B.gq, B.gk, h->td_dev, h->rt, rows, d, h->hd,
           h->L, h->hn, h->wn, h->T, h->S, h->md.eps);
     else
-      qkv_post2_kernel<TA, 8><<<(rows + 1) / 2, 256, 0, h->stream>>>(
+      launch_k(h->pdl, qkv_post2_kernel<TA, 8>, dim3((rows + 1) / 2), dim3(256), 0, h->stream, 
           static_cast<const TA*>(h->qkv), static_cast<TA*>(h->q), Kb, Vb, B.gq, B.gk, h->td_dev, h->rt, rows, d, h->hd,
           h->L, h->hn, h->wn, h->T, h->S, h->md.eps);
     CKL();
@@ -530,9 +555,9 @@ sdv2_status run_block(sdv2_handle* h, int bl, int rows, int n_act) {
   {
     const int units_pt = (d / (16 / int(sizeof(TA))) + kRowThreads - 1) / kRowThreads;
     if (units_pt <= 2)
-      rms_rows2_kernel<TA, 2><<<(rows + 1) / 2, 256, 0, h->stream>>>(static_cast<TA*>(h->q), B.gcq, rows, d, h->md.eps);
+      launch_k(h->pdl, rms_rows2_kernel<TA, 2>, dim3((rows + 1) / 2), dim3(256), 0, h->stream, static_cast<TA*>(h->q), B.gcq, rows, d, h->md.eps);
     else
-      rms_rows2_kernel<TA, 8><<<(rows + 1) / 2, 256, 0, h->stream>>>(static_cast<TA*>(h->q), B.gcq, rows, d, h->md.eps);
+      launch_k(h->pdl, rms_rows2_kernel<TA, 8>, dim3((rows + 1) / 2), dim3(256), 0, h->stream, static_cast<TA*>(h->q), B.gcq, rows, d, h->md.eps);
     CKL();
   }
   const size_t px = size_t(h->Lt) * d;
@@ -571,7 +596,7 @@ sdv2_status embed_prompt(sdv2_handle* h, const float* prompt_host, int ver) {
     TA* Vd = static_cast<TA*>(h->Vx) + (size_t(ver & 1) * h->nb + b) * px;
     ep.out = h->ctx_tmp; ep.bias = B.bck;
     TRY((gemm_simt<float, TA, float>(h, h->ctx, static_cast<const TA*>(B.wck), Lt, d, d, d, EPI_STORE, ep)));
-    rms_rows_kernel<float, TA><<<(Lt + 7) / 8, 256, 0, h->stream>>>(h->ctx_tmp, Kd, B.gck, Lt, d, d, h->md.eps);
+    launch_k(h->pdl, rms_rows_kernel<float, TA>, dim3((Lt + 7) / 8), dim3(256), 0, h->stream, h->ctx_tmp, Kd, B.gck, Lt, d, d, h->md.eps);
     CKL();
     ep.out = Vd; ep.bias = B.bcv;
     TRY((gemm_simt<float, TA, TA>(h, h->ctx, static_cast<const TA*>(B.wcv), Lt, d, d, d, EPI_STORE, ep)));
@@ -607,20 +632,20 @@ sdv2_status tick_body(sdv2_handle* h, int na, int par) {
   const bool first = h->rank == 0, last = h->rank == h->K - 1;
   if (first) {
     // motion-aware noise controller then the step-0 blend on all SMs
-    motion_kernel<<<1, 1024, 0, h->stream>>>(h->lat_in, h->prev_frame, h->ctrl, h->st.sig, h->st.sign, h->td_dev,
+    launch_k(h->pdl, motion_kernel, dim3(1), dim3(1024), 0, h->stream, h->lat_in, h->prev_frame, h->ctrl, h->st.sig, h->st.sign, h->td_dev,
                                             h->scfg, h->CTHW, h->hh * h->ww, h->T);
     CKL();
-    blend_kernel<<<(h->CTHW + 255) / 256, 256, 0, h->stream>>>(h->lat_in, h->st.lat, h->st.sig, h->td_dev,
+    launch_k(h->pdl, blend_kernel, dim3((h->CTHW + 255) / 256), dim3(256), 0, h->stream, h->lat_in, h->st.lat, h->st.sig, h->td_dev,
                                                                h->scfg.seed, h->CTHW);
     CKL();
     if (na > 1) {
       // K = 1: the ring packet of call c-1 was written to ring[1][(c-1)&1] == ring[1][par^1]
       const float* rin = h->K == 1 ? h->ring[1][par ^ 1] : h->ring[0][par];
-      assemble_kernel<<<dim3(64, h->n - 1), 256, 0, h->stream>>>(rin, h->st.lat, h->td_dev, h->n, h->CTHW);
+      launch_k(h->pdl, assemble_kernel, dim3(dim3(64, h->n - 1)), dim3(256), 0, h->stream, rin, h->st.lat, h->td_dev, h->n, h->CTHW);
       CKL();
     }
     // patchify + patch embedding (C.1): x = u W_pe^T + b_pe, fp32 (K = 4C)
-    patchify_kernel<<<(rows * h->P + 255) / 256, 256, 0, h->stream>>>(h->st.lat, h->u, rows, h->L, h->C, h->T, h->hh,
+    launch_k(h->pdl, patchify_kernel, dim3((rows * h->P + 255) / 256), dim3(256), 0, h->stream, h->st.lat, h->u, rows, h->L, h->C, h->T, h->hh,
                                                                        h->ww);
     CKL();
     {
@@ -628,16 +653,16 @@ sdv2_status tick_body(sdv2_handle* h, int na, int par) {
       ep.out = h->st.x; ep.ldo = h->d; ep.bias = h->gw[G_PATCH_B]; ep.L = h->L;
       TRY((gemm_simt<float, float, float>(h, h->u, h->gw[G_PATCH_W], rows, h->d, h->P, h->P, EPI_STORE, ep)));
     }
-    sinusoid_kernel<<<na, 128, 0, h->stream>>>(h->st.sig, h->emb, na, h->md.freq_dim);
+    launch_k(h->pdl, sinusoid_kernel, dim3(na), dim3(128), 0, h->stream, h->st.sig, h->emb, na, h->md.freq_dim);
     CKL();
     const int d = h->d;
     // time MLP (C.2): e = W_t2 SiLU(W_t1 emb + b) + b; e0 = W_tp SiLU(e) + b
-    gemv2_kernel<float><<<(d + 31) / 32, 256, size_t(na) * h->md.freq_dim * 4, h->stream>>>(
+    launch_k(h->pdl, gemv2_kernel<float>, dim3((d + 31) / 32), dim3(256), size_t(na) * h->md.freq_dim * 4, h->stream, 
         h->gw[G_T1_W], h->gw[G_T1_B], h->emb, h->t1, na, d, h->md.freq_dim, 0);
-    gemv2_kernel<float><<<(d + 31) / 32, 256, size_t(na) * d * 4, h->stream>>>(h->gw[G_T2_W], h->gw[G_T2_B], h->t1,
+    launch_k(h->pdl, gemv2_kernel<float>, dim3((d + 31) / 32), dim3(256), size_t(na) * d * 4, h->stream, h->gw[G_T2_W], h->gw[G_T2_B], h->t1,
                                                                                h->st.e, na, d, d, 1);
     h->launches += 2;
-    gemv2_kernel<TA><<<(6 * d + 31) / 32, 256, size_t(na) * d * 4, h->stream>>>(
+    launch_k(h->pdl, gemv2_kernel<TA>, dim3((6 * d + 31) / 32), dim3(256), size_t(na) * d * 4, h->stream, 
         static_cast<const TA*>(h->tp_w), h->gw[G_TP_B], h->st.e, h->st.e0, na, 6 * d, d, 1);
     CKL();
   } else {
@@ -660,10 +685,12 @@ sdv2_status tick_body(sdv2_handle* h, int na, int par) {
                                           h->d, EPI_STORE, ep)));
     } else {
       ++h->launches;
-      if (!tc_gemm(h->stream, h->gplan, h->a, h->head_w_tw, rows, h->P, h->d, EPI_STORE_F32, ep, &h->err))
-        return SDV2_E_CUDA;
+      gemm_pdl_flag() = h->pdl;
+      const bool ok = tc_gemm(h->stream, h->gplan, h->a, h->head_w_tw, rows, h->P, h->d, EPI_STORE_F32, ep, &h->err);
+      gemm_pdl_flag() = false;
+      if (!ok) return SDV2_E_CUDA;
     }
-    flow_kernel<<<(na * h->CTHW + 255) / 256, 256, 0, h->stream>>>(
+    launch_k(h->pdl, flow_kernel, dim3((na * h->CTHW + 255) / 256), dim3(256), 0, h->stream, 
         h->yh, h->st.lat, h->st.sig, h->st.sign, h->out_stage, h->ring[1][par], h->td_dev, na, h->L, h->C, h->T,
         h->hh, h->ww, h->n, h->scfg.seed);
     CKL();
@@ -783,6 +810,7 @@ sdv2_status sdv2_create(const sdv2_model_desc* md, const sdv2_geometry* g, const
   }
   h->device = device;
   h->stream = static_cast<cudaStream_t>(stream);
+  if (const char* e = getenv("SDV2_PDL")) h->pdl = atoi(e) != 0;
   h->ws_bytes = workspace_bytes;
   if (cudaSetDevice(device) != cudaSuccess) {
     delete h;
