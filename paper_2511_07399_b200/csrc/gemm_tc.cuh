@@ -28,10 +28,12 @@ constexpr int kGemmThreads = 384;                        // 4 control warps + 8 
 
 // Stages of the TMA->MMA ring for a tile width: the ring must cover the L2/HBM latency
 // (about 1-2 us) at the MMA rate, so use all of shared memory.
-__host__ __device__ inline int gemm_stages(int BN) {
-  const int st = (kGemmSmem - 1024 - 512) / (kGemmSmemA + BN * kGemmBK * 2);
+__host__ __device__ inline int gemm_stages(int BN, bool res_tma) {
+  const int xs = res_tma ? BN * kGemmBM * 4 : 0;     // staged fp32 residual tile
+  const int st = (kGemmSmem - 1024 - 512 - xs) / (kGemmSmemA + BN * kGemmBK * 2);
   return st > kGemmMaxStages ? kGemmMaxStages : st;
 }
+constexpr int kResMaxBN = 192;   // residual epilogues: keep >= 3 stages next to the x tile
 
 template <int EPI, typename TOut>
 __device__ __forceinline__ void gemm_epilogue_chunk(const EpiArgs& ep, int r, int c0, int N, const uint32_t (&v)[32]) {
@@ -115,19 +117,27 @@ __device__ __forceinline__ void gemm_epilogue_chunk(const EpiArgs& ep, int r, in
 // 16 KB + BN*64 B per k-block from L2 instead of 16 KB + BN*128 B.
 template <int EPI, typename TOut, int MC>
 __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA,
-                                                         const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
+                                                         const __grid_constant__ CUtensorMap tmB,
+                                                         const __grid_constant__ CUtensorMap tmX, int M, int N, int K,
                                                          int BN, EpiArgs ep) {
+  // Residual epilogues stage the fp32 x tile in shared memory: TMA load issued as soon
+  // as the epilogue warps reach the tile (overlapping the mainloop), in-place update,
+  // TMA store.  128-byte swizzled 32-column boxes keep the row-per-thread smem accesses
+  // conflict-light.
+  constexpr bool kResTMA = (EPI == EPI_RES_GATE || EPI == EPI_RES);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int kStages = gemm_stages(BN);
+  const int kStages = gemm_stages(BN, kResTMA);
   const int kSmemB = BN * kGemmBK * 2;      // multiple of 1024 (BN multiple of 32... 8 rows x 128 B)
   uint8_t* sA = smem;
   uint8_t* sB = smem + kStages * kGemmSmemA;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + kStages * kSmemB);
+  uint8_t* sX = sB + kStages * kSmemB;      // [BN/32][128 rows][32 fp32], 16 KB per box
+  uint64_t* full = reinterpret_cast<uint64_t*>(sX + (kResTMA ? BN * kGemmBM * 4 : 0));
   uint64_t* empty = full + kStages;
   uint64_t* tfull = empty + kStages;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* x_full = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(x_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int num_m = (M + kGemmBM - 1) / kGemmBM, num_n = (N + BN - 1) / BN;
@@ -150,6 +160,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
       tc::mbar_init(tfull + s, 1);
       tc::mbar_init(tempty + s, 8);
     }
+    tc::mbar_init(x_full, 1);
+    if (kResTMA) tc::tma_prefetch_desc(&tmX);
     tc::fence_barrier_init();
   }
   if (warp == 2) tc::tmem_alloc(tmem_slot, 512);
@@ -242,28 +254,77 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
     pdl_wait();                         // epilogue reads x / gates produced upstream
     const int q = warp & 3;             // TMEM lane quarter accessible by this warp
     const int wg = (warp - 4) >> 2;     // epilogue warpgroup: 32-column chunks c % 2 == wg
+    const bool leader = (warp == 4 && lane == 0);
+    const int row = q * 32 + lane;      // row inside the tile
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = cid; t < tiles; t += ncl) {
+    int nt = 0;                         // tiles done by this CTA
+    for (int t = cid; t < tiles; t += ncl, ++nt) {
       const int mb = (t % num_mg) * MC + cr, nb = t / num_mg;
+      if (kResTMA && leader) {          // fetch the residual tile while the MMAs run
+        tc::mbar_expect_tx(x_full, uint32_t(BN) * kGemmBM * 4);
+        for (int c = 0; c < BN; c += 32)
+          tc::tma_load_2d(sX + (c / 32) * (kGemmBM * 128), &tmX, x_full, nb * BN + c, mb * kGemmBM);
+      }
       tc::mbar_wait(tfull + acc, acc_phase);
       tc::tc_fence_after();
-      const int r = mb * kGemmBM + q * 32 + lane;
+      const int r = mb * kGemmBM + row;
+      if (kResTMA) tc::mbar_wait(x_full, nt & 1);
       for (int c = wg * 32; c < BN; c += 64) {
         uint32_t v[32];
         tc::tmem_ld32(tmem + (uint32_t(q * 32) << 16) + uint32_t(acc * BN + c), v);
         tc::tmem_ld_wait();
         const int c0 = nb * BN + c;
-        if (r < M && c0 < N) gemm_epilogue_chunk<EPI, TOut>(ep, r, c0, N, v);
+        if (kResTMA) {
+          if (c0 + 32 <= N) {
+            uint8_t* xrow = sX + (c / 32) * (kGemmBM * 128) + (row >> 3) * 1024 + (row & 7) * 128;
+            const float4* bias4 = reinterpret_cast<const float4*>(ep.bias + c0);
+            const float4* gm = reinterpret_cast<const float4*>(ep.mod + ep.gate_row * N + c0);
+            const float4* ge =
+                reinterpret_cast<const float4*>(ep.e0 + size_t(r < M ? r / ep.L : 0) * 6 * N + ep.gate_row * N + c0);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              float4* px = reinterpret_cast<float4*>(xrow + ((u ^ (row & 7)) << 4));
+              float4 xv = *px;
+              const float4 bb = __ldg(bias4 + u);
+              float a0 = __uint_as_float(v[4 * u]) + bb.x, a1 = __uint_as_float(v[4 * u + 1]) + bb.y;
+              float a2 = __uint_as_float(v[4 * u + 2]) + bb.z, a3 = __uint_as_float(v[4 * u + 3]) + bb.w;
+              if (EPI == EPI_RES_GATE) {
+                const float4 ga = __ldg(gm + u), gb = __ldg(ge + u);
+                a0 *= ga.x + gb.x;
+                a1 *= ga.y + gb.y;
+                a2 *= ga.z + gb.z;
+                a3 *= ga.w + gb.w;
+              }
+              xv.x += a0;
+              xv.y += a1;
+              xv.z += a2;
+              xv.w += a3;
+              *px = xv;
+            }
+          }
+        } else if (r < M && c0 < N) {
+          gemm_epilogue_chunk<EPI, TOut>(ep, r, c0, N, v);
+        }
       }
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(tempty + acc);
+      if (kResTMA) {
+        tc::fence_proxy_async_smem();   // generic-proxy smem writes -> visible to the TMA store
+        asm volatile("bar.sync 2, 256;" ::: "memory");
+        if (leader) {
+          for (int c = 0; c < BN; c += 32)
+            tc::tma_store_2d(&tmX, sX + (c / 32) * (kGemmBM * 128), nb * BN + c, mb * kGemmBM);
+          tc::tma_store_commit_wait_read();   // smem reusable for the next tile's load
+        }
+      }
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
       }
     }
+    if (kResTMA && leader) tc::tma_store_wait_all();
   }
   tc::tc_fence_before();
   if (MC > 1) tc::cluster_sync();   // no CTA exits while its peer may still multicast into it
@@ -328,6 +389,27 @@ inline bool tc_make_map(TmaGemmPlan& p, CUtensorMap* m, const void* ptr, int row
   return true;
 }
 
+// fp32 [rows, ld] residual map, 32-column x 128-row boxes, 128-byte swizzle.
+inline const CUtensorMap* tc_map_res(TmaGemmPlan& p, const void* ptr, int rows, int cols, int ld, std::string* err) {
+  const std::string key = "res:" + std::to_string(reinterpret_cast<uintptr_t>(ptr)) + ":" + std::to_string(rows) +
+                          ":" + std::to_string(cols) + ":" + std::to_string(ld);
+  auto it = p.maps.find(key);
+  if (it != p.maps.end()) return &it->second;
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
+  const cuuint64_t strides[1] = {cuuint64_t(ld) * 4};
+  const cuuint32_t box[2] = {32, uint32_t(kGemmBM)};
+  const cuuint32_t es[2] = {1, 1};
+  CUresult r = p.encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    *err = "cuTensorMapEncodeTiled (residual) failed (" + std::to_string(int(r)) + ")";
+    return nullptr;
+  }
+  return &(p.maps.emplace(key, m).first->second);
+}
+
 inline const CUtensorMap* tc_map(TmaGemmPlan& p, const void* ptr, int rows, int K, int box_rows, std::string* err) {
   const std::string key = std::to_string(reinterpret_cast<uintptr_t>(ptr)) + ":" + std::to_string(rows) + ":" +
                           std::to_string(K) + ":" + std::to_string(box_rows);
@@ -340,13 +422,13 @@ inline const CUtensorMap* tc_map(TmaGemmPlan& p, const void* ptr, int rows, int 
 
 // Tile width N chosen to balance (M/128/MC) x (N/BN) cluster tiles over the SMs:
 // maximise useful-column fraction x useful-row fraction x wave efficiency.
-inline int tc_pick_bn(int M, int N, int sms, int MC) {
+inline int tc_pick_bn(int M, int N, int sms, int MC, int max_bn = 256) {
   const int num_m = (M + kGemmBM - 1) / kGemmBM;
   const int num_mg = (num_m + MC - 1) / MC;
   const int slots = sms / MC;
   int best = 256;
   double best_eff = -1.0;
-  for (int bn = 256; bn >= 64; bn -= 32) {
+  for (int bn = max_bn; bn >= 64; bn -= 32) {
     const int num_n = (N + bn - 1) / bn;
     const int tiles = num_mg * num_n;
     const int waves = (tiles + slots - 1) / slots;
@@ -368,8 +450,8 @@ inline bool& gemm_pdl_flag() {
 }
 
 template <int EPI, typename TOut, int MC>
-inline cudaError_t gemm_launch(cudaStream_t s, int grid, const CUtensorMap& ma, const CUtensorMap& mb, int M, int N,
-                               int K, int BN, const EpiArgs& ep) {
+inline cudaError_t gemm_launch(cudaStream_t s, int grid, const CUtensorMap& ma, const CUtensorMap& mb,
+                               const CUtensorMap& mx, int M, int N, int K, int BN, const EpiArgs& ep) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kGemmThreads);
@@ -384,18 +466,18 @@ inline cudaError_t gemm_launch(cudaStream_t s, int grid, const CUtensorMap& ma, 
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = gemm_pdl_flag() ? 2 : 1;
-  return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<EPI, TOut, MC>, ma, mb, M, N, K, BN, ep);
+  return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<EPI, TOut, MC>, ma, mb, mx, M, N, K, BN, ep);
 }
 
 template <int MC>
-inline cudaError_t gemm_dispatch(cudaStream_t s, int grid, const CUtensorMap& ma, const CUtensorMap& mb, int M, int N,
-                                 int K, int BN, int epi, const EpiArgs& ep) {
+inline cudaError_t gemm_dispatch(cudaStream_t s, int grid, const CUtensorMap& ma, const CUtensorMap& mb,
+                                 const CUtensorMap& mx, int M, int N, int K, int BN, int epi, const EpiArgs& ep) {
   switch (epi) {
-    case EPI_STORE: return gemm_launch<EPI_STORE, bf16, MC>(s, grid, ma, mb, M, N, K, BN, ep);
-    case EPI_GELU: return gemm_launch<EPI_GELU, bf16, MC>(s, grid, ma, mb, M, N, K, BN, ep);
-    case EPI_RES_GATE: return gemm_launch<EPI_RES_GATE, bf16, MC>(s, grid, ma, mb, M, N, K, BN, ep);
-    case EPI_STORE_F32: return gemm_launch<EPI_STORE, float, MC>(s, grid, ma, mb, M, N, K, BN, ep);
-    default: return gemm_launch<EPI_RES, bf16, MC>(s, grid, ma, mb, M, N, K, BN, ep);
+    case EPI_STORE: return gemm_launch<EPI_STORE, bf16, MC>(s, grid, ma, mb, mx, M, N, K, BN, ep);
+    case EPI_GELU: return gemm_launch<EPI_GELU, bf16, MC>(s, grid, ma, mb, mx, M, N, K, BN, ep);
+    case EPI_RES_GATE: return gemm_launch<EPI_RES_GATE, bf16, MC>(s, grid, ma, mb, mx, M, N, K, BN, ep);
+    case EPI_STORE_F32: return gemm_launch<EPI_STORE, float, MC>(s, grid, ma, mb, mx, M, N, K, BN, ep);
+    default: return gemm_launch<EPI_RES, bf16, MC>(s, grid, ma, mb, mx, M, N, K, BN, ep);
   }
 }
 
@@ -412,15 +494,22 @@ inline bool tc_gemm(cudaStream_t s, TmaGemmPlan& p, const void* A, const void* W
   }
   const int num_m = (M + kGemmBM - 1) / kGemmBM;
   const int MC = (num_m >= 2 && tc_gemm_default_mc() == 2) ? 2 : 1;
-  const int BN = tc_pick_bn(M, N, p.num_sms, MC);
+  const bool res = (epi == EPI_RES_GATE || epi == EPI_RES);
+  if (res && N % 32 != 0) {
+    *err = "tc_gemm: residual epilogue needs N % 32 == 0";
+    return false;
+  }
+  const int BN = tc_pick_bn(M, N, p.num_sms, MC, res ? kResMaxBN : 256);
   const CUtensorMap* ma = tc_map(p, A, a_rows_alloc > 0 ? a_rows_alloc : M, K, kGemmBM, err);
   const CUtensorMap* mb = tc_map(p, W, N, K, BN / MC, err);
   if (!ma || !mb) return false;
+  const CUtensorMap* mx = res ? tc_map_res(p, ep.out, M, N, ep.ldo, err) : ma;
+  if (!mx) return false;
   const int tiles = ((num_m + MC - 1) / MC) * ((N + BN - 1) / BN);
   const int slots = p.num_sms / MC;
   const int grid = MC * (tiles < slots ? tiles : slots);
-  cudaError_t e = MC == 2 ? gemm_dispatch<2>(s, grid, *ma, *mb, M, N, K, BN, epi, ep)
-                          : gemm_dispatch<1>(s, grid, *ma, *mb, M, N, K, BN, epi, ep);
+  cudaError_t e = MC == 2 ? gemm_dispatch<2>(s, grid, *ma, *mb, *mx, M, N, K, BN, epi, ep)
+                          : gemm_dispatch<1>(s, grid, *ma, *mb, *mx, M, N, K, BN, epi, ep);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     *err = std::string("gemm_tc launch: ") + cudaGetErrorString(e);
