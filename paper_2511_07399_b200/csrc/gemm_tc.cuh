@@ -14,7 +14,10 @@
 // of the tile shape, so results are batch invariant.
 #pragma once
 #include <string>
+#include <algorithm>
 #include <unordered_map>
+#include <utility>
+#include <vector>
 
 #include "kernels.cuh"
 #include "tc_common.cuh"
@@ -344,6 +347,7 @@ struct TmaGemmPlan {
   PFN_encodeTiled encode = nullptr;
   int num_sms = 148;
   std::unordered_map<std::string, CUtensorMap> maps;
+  std::unordered_map<std::string, std::pair<int, int>> tuned;   // "M:N:K:epi" -> (MC, BN)
 };
 
 inline bool tc_gemm_enabled() { return true; }
@@ -486,21 +490,16 @@ inline int tc_gemm_default_mc() {
   return e ? atoi(e) : 1;
 }
 
-inline bool tc_gemm(cudaStream_t s, TmaGemmPlan& p, const void* A, const void* W, int M, int N, int K, int epi,
-                    const EpiArgs& ep, std::string* err, int a_rows_alloc = 0) {
-  if (K % kGemmBK != 0 || N % 16 != 0) {
-    *err = "tc_gemm: K % 64 or N % 16";
-    return false;
-  }
+inline std::string gemm_key(int M, int N, int K, int epi) {
+  return std::to_string(M) + ":" + std::to_string(N) + ":" + std::to_string(K) + ":" + std::to_string(epi);
+}
+
+// One launch with an explicit (cluster size, tile width) configuration.
+inline bool tc_gemm_cfg(cudaStream_t s, TmaGemmPlan& p, const void* A, const void* W, int M, int N, int K, int epi,
+                        const EpiArgs& ep, int MC, int BN, std::string* err) {
   const int num_m = (M + kGemmBM - 1) / kGemmBM;
-  const int MC = (num_m >= 2 && tc_gemm_default_mc() == 2) ? 2 : 1;
   const bool res = (epi == EPI_RES_GATE || epi == EPI_RES);
-  if (res && N % 32 != 0) {
-    *err = "tc_gemm: residual epilogue needs N % 32 == 0";
-    return false;
-  }
-  const int BN = tc_pick_bn(M, N, p.num_sms, MC, res ? kResMaxBN : 256);
-  const CUtensorMap* ma = tc_map(p, A, a_rows_alloc > 0 ? a_rows_alloc : M, K, kGemmBM, err);
+  const CUtensorMap* ma = tc_map(p, A, M, K, kGemmBM, err);
   const CUtensorMap* mb = tc_map(p, W, N, K, BN / MC, err);
   if (!ma || !mb) return false;
   const CUtensorMap* mx = res ? tc_map_res(p, ep.out, M, N, ep.ldo, err) : ma;
@@ -516,6 +515,88 @@ inline bool tc_gemm(cudaStream_t s, TmaGemmPlan& p, const void* A, const void* W
     return false;
   }
   return true;
+}
+
+inline bool tc_gemm_check(int N, int K, int epi, std::string* err) {
+  if (K % kGemmBK != 0 || N % 16 != 0) {
+    *err = "tc_gemm: K % 64 or N % 16";
+    return false;
+  }
+  if ((epi == EPI_RES_GATE || epi == EPI_RES) && N % 32 != 0) {
+    *err = "tc_gemm: residual epilogue needs N % 32 == 0";
+    return false;
+  }
+  return true;
+}
+
+// Default configuration from the tile-balance model (used when a shape was not tuned).
+inline void tc_gemm_default_cfg(const TmaGemmPlan& p, int M, int N, int epi, int* MC, int* BN) {
+  const int num_m = (M + kGemmBM - 1) / kGemmBM;
+  *MC = (num_m >= 2 && tc_gemm_default_mc() == 2) ? 2 : 1;
+  const bool res = (epi == EPI_RES_GATE || epi == EPI_RES);
+  *BN = tc_pick_bn(M, N, p.num_sms, *MC, res ? kResMaxBN : 256);
+}
+
+inline bool tc_gemm(cudaStream_t s, TmaGemmPlan& p, const void* A, const void* W, int M, int N, int K, int epi,
+                    const EpiArgs& ep, std::string* err, int a_rows_alloc = 0) {
+  (void)a_rows_alloc;
+  if (!tc_gemm_check(N, K, epi, err)) return false;
+  int MC, BN;
+  auto it = p.tuned.find(gemm_key(M, N, K, epi));
+  if (it != p.tuned.end()) {
+    MC = it->second.first;
+    BN = it->second.second;
+  } else {
+    tc_gemm_default_cfg(p, M, N, epi, &MC, &BN);
+  }
+  return tc_gemm_cfg(s, p, A, W, M, N, K, epi, ep, MC, BN, err);
+}
+
+// Create-time autotuning of one GEMM shape on the real buffers: the best of
+// {MC = 1, 2} x the three best tile widths of the balance model, by CUDA-event time.
+inline bool tc_gemm_tune(cudaStream_t s, TmaGemmPlan& p, const void* A, const void* W, int M, int N, int K, int epi,
+                         const EpiArgs& ep, std::string* err) {
+  if (!tc_gemm_check(N, K, epi, err)) return false;
+  const std::string key = gemm_key(M, N, K, epi);
+  if (p.tuned.count(key)) return true;
+  const int num_m = (M + kGemmBM - 1) / kGemmBM;
+  const bool res = (epi == EPI_RES_GATE || epi == EPI_RES);
+  std::vector<std::pair<int, int>> cands;
+  for (int MC = 1; MC <= (num_m >= 2 ? 2 : 1); ++MC) {
+    std::vector<std::pair<double, int>> ranked;
+    const int num_mg = (num_m + MC - 1) / MC, slots = p.num_sms / MC;
+    for (int bn = res ? kResMaxBN : 256; bn >= 64; bn -= 32) {
+      const int num_n = (N + bn - 1) / bn, tiles = num_mg * num_n, waves = (tiles + slots - 1) / slots;
+      const double eff = double(N) / double(num_n * bn) * double(num_m) / double(num_mg * MC) * double(tiles) /
+                         double(waves * slots);
+      ranked.push_back({-eff, -bn});
+    }
+    std::sort(ranked.begin(), ranked.end());
+    for (size_t i = 0; i < ranked.size() && i < 3; ++i) cands.push_back({MC, -ranked[i].second});
+  }
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  float best = 1e30f;
+  std::pair<int, int> best_cfg = cands.front();
+  for (auto& c : cands) {
+    for (int i = 0; i < 2; ++i)
+      if (!tc_gemm_cfg(s, p, A, W, M, N, K, epi, ep, c.first, c.second, err)) return false;
+    cudaEventRecord(a, s);
+    for (int i = 0; i < 5; ++i) tc_gemm_cfg(s, p, A, W, M, N, K, epi, ep, c.first, c.second, err);
+    cudaEventRecord(b, s);
+    cudaEventSynchronize(b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    if (ms < best) {
+      best = ms;
+      best_cfg = c;
+    }
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  p.tuned[key] = best_cfg;
+  return cudaGetLastError() == cudaSuccess;
 }
 
 }  // namespace sdv2

@@ -878,6 +878,31 @@ sdv2_status sdv2_create(const sdv2_model_desc* md, const sdv2_geometry* g, const
     if (!tc_gemm_plan(h->gplan, &h->err)) return fail(SDV2_E_CUDA);
     attn_plan_init(h->aplan, h->gplan.encode, std::min(h->gplan.num_sms, kMaxSMs));
   }
+  if (h->prec == SDV2_BF16 && !(getenv("SDV2_TUNE") && atoi(getenv("SDV2_TUNE")) == 0)) {
+    // Autotune the projection GEMMs of every tick shape (M = active entries x L) on the
+    // real buffers (their contents are scratch until reset_stream).
+    const BlockW& B = h->bw[0];
+    const int d = h->d;
+    for (int na = 1; na <= h->n; ++na) {
+      const int M = na * h->L;
+      EpiArgs ep{};
+      ep.L = h->L; ep.mod = B.mod; ep.e0 = h->st.e0; ep.gate_row = 2;
+      struct Sh { const void* A; const void* W; int N, K, epi; void* out; int ldo; const float* bias; } shapes[] = {
+          {h->a, B.wqkv, 3 * d, d, EPI_STORE, h->qkv, 3 * d, B.bqkv},
+          {h->o, B.wo, d, d, EPI_RES_GATE, h->st.x, d, B.bo},
+          {h->a, B.wcq, d, d, EPI_STORE, h->q, d, B.bcq},
+          {h->o, B.wco, d, d, EPI_RES, h->st.x, d, B.bco},
+          {h->a, B.w1, h->F, d, EPI_GELU, h->hbuf, h->F, B.b1},
+          {h->hbuf, B.w2, d, h->F, EPI_RES_GATE, h->st.x, d, B.b2},
+          {h->a, h->head_w_tw, h->P, d, EPI_STORE_F32, h->yh, h->P, h->gw[G_HEAD_B]},
+      };
+      for (auto& sh : shapes) {
+        ep.out = sh.out; ep.ldo = sh.ldo; ep.bias = sh.bias;
+        if (!tc_gemm_tune(h->stream, h->gplan, sh.A, sh.W, M, sh.N, sh.K, sh.epi, ep, &h->err)) return fail(SDV2_E_CUDA);
+      }
+    }
+    if (cudaStreamSynchronize(h->stream) != cudaSuccess) return fail(SDV2_E_CUDA);
+  }
   cudaFuncSetAttribute(gemv2_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(gemv2_kernel<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   *out = h;
