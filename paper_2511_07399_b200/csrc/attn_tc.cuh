@@ -32,7 +32,7 @@ struct AttnSmem {
   static constexpr int Q = kAttnBQ * HD * 2;          // 32 KB (hd 128)
   static constexpr int KV = kAttnBKV * HD * 2;        // one K or V tile
   static constexpr int P = kAttnBQ * kAttnBKV * 2;    // 32 KB
-  static constexpr int total = Q + 4 * KV + P + 1024 + 256 + 4 * 256 * 4;
+  static constexpr int total = Q + 4 * KV + P + 1024 + 256 + 512 * 4;
 };
 
 struct AttnTcArgs {
@@ -110,12 +110,12 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
   uint64_t* v_empty = bar + 7;  // [2]
   uint64_t* s_full = bar + 9;   // [2]
   uint64_t* s_empty = bar + 11; // [2]
-  uint64_t* p_full = bar + 13;
-  uint64_t* p_empty = bar + 14;
+  uint64_t* p_full = bar + 13;   // [2] per key half (4 softmax warps each)
+  uint64_t* p_empty = bar + 19;  // [2] per key half (PV of that half done)
   uint64_t* q_empty = bar + 15;
   uint64_t* o_empty = bar + 16;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 18);
-  float* xch = reinterpret_cast<float*>(bar + 20);   // [2 tiles][2 halves][128] row-max exchange + [2][128] sums
+  float* xch = reinterpret_cast<float*>(bar + 22);   // [2 halves][128] (max, sum) exchange at segment end
 
   pdl_wait();      // q, K/V lanes and o are produced / consumed by the neighbouring kernels
   pdl_trigger();
@@ -150,8 +150,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
       tc::mbar_init(s_full + s, 1);
       tc::mbar_init(s_empty + s, 8);
     }
-    tc::mbar_init(p_full, 8);
-    tc::mbar_init(p_empty, 1);
+    for (int hh = 0; hh < 2; ++hh) {
+      tc::mbar_init(p_full + hh, 4);
+      tc::mbar_init(p_empty + hh, 1);
+    }
     tc::fence_barrier_init();
   }
   if (warp == 0) tc::tmem_alloc(tmem_slot, 512);
@@ -160,7 +162,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t tS[2] = {tmem, tmem + 128u};
-  const uint32_t tO = tmem + 256u;
+  // Each key half (64 of the 128 keys of a tile) has its own O accumulator and running
+  // max, so the two softmax warpgroups never synchronise per tile; they are merged once
+  // per unit.  TMEM: S0 | S1 | O_half0 | O_half1 (128 columns each).
+  const uint32_t tO2[2] = {tmem + 256u, tmem + 384u};
 
   // Segment iteration: [gs, ge) of global tiles inside one unit.
   struct Seg {
@@ -243,19 +248,22 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
         if (nt > 1) issue_S(gi + 1);
         for (int t = 0; t < nt; ++t) {
           const int gt = gi + t;
-          tc::mbar_wait(p_full, gt & 1);
           tc::mbar_wait(v_full + (gt & 1), (gt >> 1) & 1);
           if (t == 0 && sg > 0) tc::mbar_wait(o_empty, (sg - 1) & 1);
-          tc::tc_fence_after();
           const uint32_t va = tc::smem_u32(sV + (gt & 1) * SM::KV);
 #pragma unroll
-          for (int k = 0; k < kAttnBKV / 16; ++k) {
-            const uint32_t poff = (k >> 2) * (kAttnBQ * 128) + (k & 3) * 32;
-            tc::mma_bf16(tO, tc::sw128_kmajor_desc(pa + poff),
-                         tc::sw128_mnmajor_desc(va + k * 2048, kAttnBKV * 128), idO, (t | k) != 0);
+          for (int hh = 0; hh < 2; ++hh) {   // O_h += P[:, 64h : 64h+64] V[64h : 64h+64, :]
+            tc::mbar_wait(p_full + hh, gt & 1);
+            tc::tc_fence_after();
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const uint32_t poff = hh * (kAttnBQ * 128) + k * 32;
+              tc::mma_bf16(tO2[hh], tc::sw128_kmajor_desc(pa + poff),
+                           tc::sw128_mnmajor_desc(va + (hh * 4 + k) * 2048, kAttnBKV * 128), idO, (t | k) != 0);
+            }
+            tc::mma_commit(p_empty + hh);
           }
           tc::mma_commit(v_empty + (gt & 1));
-          tc::mma_commit(p_empty);
           if (t + 2 < nt) issue_S(gt + 2);
         }
         tc::mma_commit(q_empty);
@@ -310,23 +318,19 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
             mx = fmaxf(mx, sv[i]);
           }
         }
-        // exchange the row max between the two column halves
-        float* xm = xch + (t & 1) * 256;
-        xm[half * 128 + row] = mx;
-        asm volatile("bar.sync 1, 256;" ::: "memory");
-        mx = fmaxf(mx, xm[(half ^ 1) * 128 + row]) * a.scale_log2;
-        // PV of the previous tile finished: P smem free and O stable in TMEM
-        if (gt > 0) tc::mbar_wait(p_empty, (gt - 1) & 1);
+        mx *= a.scale_log2;
+        // PV of this half's previous tile finished: its P chunk is free and O_half stable
+        if (gt > 0) tc::mbar_wait(p_empty + half, (gt - 1) & 1);
         tc::tc_fence_after();
         if (mx > m_used + 8.f) {
           const float m_new = mx;
-          if (t > 0) {
+          if (t > 0) {     // rescale this half's O row (all HD columns) in TMEM
             const float alpha = ex2(m_used - m_new);
             l *= alpha;
 #pragma unroll
-            for (int cc = 0; cc < HO / 16; ++cc) {
+            for (int cc = 0; cc < HD / 16; ++cc) {
               uint32_t r[16];
-              const uint32_t ta = tO + lane_off + half * HO + cc * 16;
+              const uint32_t ta = tO2[half] + lane_off + cc * 16;
               asm volatile(
                   "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
                   "[%16];"
@@ -343,7 +347,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
           }
           m_used = m_new;
         }
-        // P = exp2(s * scale - m_used) -> bf16, this half = P chunk `half` (64 keys, 128 B/row)
+        // P = exp2(s * scale - m_used) -> bf16, this half = P chunk `half` (64 keys, 128 B/row);
+        // a half with no valid key yet (m_used = -inf) writes P = 0
+        const float msub = m_used == -INFINITY ? 0.f : m_used;
         float rs = 0.f;
         uint8_t* prow_base = sP + half * (kAttnBQ * 128) + (row >> 3) * 1024 + (row & 7) * 128;
 #pragma unroll
@@ -351,8 +357,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
           uint32_t pk[4];
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            const float p0 = ex2(fmaf(sv[gq * 8 + 2 * u], a.scale_log2, -m_used));
-            const float p1 = ex2(fmaf(sv[gq * 8 + 2 * u + 1], a.scale_log2, -m_used));
+            const float p0 = ex2(fmaf(sv[gq * 8 + 2 * u], a.scale_log2, -msub));
+            const float p1 = ex2(fmaf(sv[gq * 8 + 2 * u + 1], a.scale_log2, -msub));
             rs += p0 + p1;
             __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
             pk[u] = *reinterpret_cast<uint32_t*>(&b2);
@@ -364,33 +370,41 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         tc::tc_fence_before();
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive(p_full);
+        if (lane == 0) tc::mbar_arrive(p_full + half);
       }
-      // end of segment: combine the two halves' sums, wait for the last PV, read O
-      float* xl = xch + 512;
-      xl[half * 128 + row] = l;
+      // end of segment: wait for this half's last PV; exchange (m, l) with the other half
+      tc::mbar_wait(p_empty + half, (gi + nt - 1) & 1);
+      xch[half * 256 + row] = m_used;
+      xch[half * 256 + 128 + row] = l;
       asm volatile("bar.sync 1, 256;" ::: "memory");
-      const float lt = l + xl[(half ^ 1) * 128 + row];
-      tc::mbar_wait(p_empty, (gi + nt - 1) & 1);
+      tc::mbar_wait(p_empty + (half ^ 1), (gi + nt - 1) & 1);   // other half's O complete too
       tc::tc_fence_after();
+      const float m0 = xch[row], l0 = xch[128 + row], m1 = xch[256 + row], l1 = xch[384 + row];
+      const float M = fmaxf(m0, m1);
+      const float w0 = m0 == -INFINITY ? 0.f : ex2(m0 - M), w1 = m1 == -INFINITY ? 0.f : ex2(m1 - M);
+      const float lt = l0 * w0 + l1 * w1;
       const bool full = (s.jb == 0 && s.je == s.J);
       const int slot = (g == t0) ? 0 : 1;
       const int qr = s.q0 + row;
-      const float inv = 1.f / lt;
+      const float inv = full ? 1.f / lt : 1.f;
+      const float c0w = w0 * inv, c1w = w1 * inv;
       bf16* orow = reinterpret_cast<bf16*>(a.o) + size_t(s.e * a.L + qr) * a.ldo + s.h * HD + half * HO;
       float* prow = a.part_o + ((size_t(c) * 2 + slot) * kAttnBQ + row) * HD + half * HO;
 #pragma unroll
       for (int cc = 0; cc < HO / 32; ++cc) {
-        uint32_t r[32];
-        tc::tmem_ld32(tO + lane_off + half * HO + cc * 32, r);
+        uint32_t r0[32], r1[32];
+        tc::tmem_ld32(tO2[0] + lane_off + half * HO + cc * 32, r0);
+        tc::tmem_ld32(tO2[1] + lane_off + half * HO + cc * 32, r1);
         tc::tmem_ld_wait();
+        float o[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) o[i] = __uint_as_float(r0[i]) * c0w + __uint_as_float(r1[i]) * c1w;
         if (full) {
           if (qr < a.L) {
             uint32_t pk[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
-              __nv_bfloat162 b2 =
-                  __floats2bfloat162_rn(__uint_as_float(r[2 * i]) * inv, __uint_as_float(r[2 * i + 1]) * inv);
+              __nv_bfloat162 b2 = __floats2bfloat162_rn(o[2 * i], o[2 * i + 1]);
               pk[i] = *reinterpret_cast<uint32_t*>(&b2);
             }
 #pragma unroll
@@ -401,18 +415,16 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
         } else {
 #pragma unroll
           for (int i = 0; i < 8; ++i)
-            reinterpret_cast<float4*>(prow + cc * 32)[i] =
-                make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]), __uint_as_float(r[4 * i + 2]),
-                            __uint_as_float(r[4 * i + 3]));
+            reinterpret_cast<float4*>(prow + cc * 32)[i] = make_float4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
         }
       }
       if (!full && half == 0) {
         float* ml = a.part_ml + ((size_t(c) * 2 + slot) * kAttnBQ + row) * 2;
-        ml[0] = m_used;
+        ml[0] = M;
         ml[1] = lt;
       }
       tc::tc_fence_before();
-      __syncwarp();
+      asm volatile("bar.sync 1, 256;" ::: "memory");   // xch reusable, both halves done with O
       if (lane == 0) tc::mbar_arrive(o_empty);
       gi += nt;
       g = s.ge;
