@@ -54,15 +54,22 @@ def test_tiny_stream_parity(tiny_ref, prec):
 
 def _truncated(cfg_name, nblocks, num_chunks, prompt_switch=()):
     """A BASELINE.json config at full width (d, heads, F, latent) truncated to the first
-    `nblocks` DiT blocks (oracle and library both run blocks [0, nblocks) then the head)."""
+    `nblocks` DiT blocks (oracle and library both run blocks [0, nblocks) then the head).
+    wan14_480p_1step = configs[3]'s 14B block shapes with a 1-step stream (oracle time)."""
     import dataclasses
-    cfg = sg.CONFIGS[cfg_name]
+    if cfg_name == "wan14_480p_1step":
+        base = sg.CONFIGS["wan14_480p_4step"]
+        cfg = dataclasses.replace(base, geom=dataclasses.replace(base.geom, steps=1),
+                                  stream=dataclasses.replace(base.stream, timesteps=sg.SCHEDULES[1]))
+    else:
+        cfg = sg.CONFIGS[cfg_name]
     md = dataclasses.replace(cfg.model, num_blocks=nblocks)
     return dataclasses.replace(cfg, model=md, num_chunks=num_chunks, prompt_switch=prompt_switch)
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name,nblocks,chunks", [("wan13_480p_1step", 2, 6), ("wan13_512_4step", 1, 6)])
+@pytest.mark.parametrize("name,nblocks,chunks", [("wan13_480p_1step", 2, 6), ("wan13_512_4step", 1, 6),
+                                                 ("wan14_480p_1step", 1, 3)])
 def test_full_width_parity_bf16(name, nblocks, chunks):
     """1.3B-shaped blocks at 480p (L = 1560, ragged 128-row tiles) and 512x512 with a
     4-step stream batch: per-block rel-L2 <= 2e-2 vs the fp32 oracle, bit-exact metadata.
