@@ -89,6 +89,21 @@ def chunk_frames_px(cfg):
     return 4 * cfg.geom.chunk_frames
 
 
+def gen_weights_device(md, seed=0):
+    """Same seeded values as gen_weights_parallel, moved tensor by tensor to the GPU so
+    the host never holds the whole fp32 model (14B: 57 GB)."""
+    import torch
+    from concurrent.futures import ThreadPoolExecutor
+    names = sg.all_tensor_names(md)
+
+    def one(n):
+        return torch.from_numpy(sg.gen_tensor(md, n, seed)).cuda()
+
+    with ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 4)) as ex:
+        arrs = list(ex.map(one, names))
+    return dict(zip(names, arrs))
+
+
 def gen_weights_parallel(md, seed=0):
     from concurrent.futures import ThreadPoolExecutor
     names = sg.all_tensor_names(md)
@@ -192,9 +207,14 @@ def run_ours(args, cfg):
     torch.cuda.set_device(local)
     md, g, sd = cfg.model, cfg.geom, cfg.stream
     t0 = time.time()
-    W = gen_weights_parallel(md)
+    big = md.dim >= 4096
+    W = gen_weights_device(md) if big else gen_weights_parallel(md)
     t_gen = time.time() - t0
     stage = Stage(md, g, W, precision=SDV2_BF16, device=local)
+    if big:   # free the fp32 device copies; the oracle baseline regenerates 2 blocks on host
+        del W
+        torch.cuda.empty_cache()
+        W = sg.gen_weights(md, seed=0, blocks=[0, 1])
     stream = stage.stream
     torch.cuda.set_stream(stream)      # everything below is ordered on the stage's stream
     prompt = sg.gen_prompt(md, 0)

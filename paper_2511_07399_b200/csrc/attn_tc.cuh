@@ -20,6 +20,8 @@
 #include <string>
 #include <unordered_map>
 
+#include <cuda_fp16.h>
+
 #include "kernels.cuh"
 #include "tc_common.cuh"
 
@@ -87,6 +89,16 @@ __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+// Two exp2 per MUFU op: the softmax probabilities are rounded to bf16 (8-bit mantissa)
+// for the PV MMA anyway; fp16 arguments (x <= 8 after the lazy-rescale threshold) lose
+// precision only for terms below 2^-16 of the row maximum.
+__device__ __forceinline__ float2 ex2x2(float x0, float x1) {
+  uint32_t in, out;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(in) : "f"(x1), "f"(x0));
+  asm("ex2.approx.f16x2 %0, %1;" : "=r"(out) : "r"(in));
+  __half2 h = *reinterpret_cast<__half2*>(&out);
+  return __half22float2(h);
 }
 
 template <int HD>
@@ -357,8 +369,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
           uint32_t pk[4];
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            const float p0 = ex2(fmaf(sv[gq * 8 + 2 * u], a.scale_log2, -msub));
-            const float p1 = ex2(fmaf(sv[gq * 8 + 2 * u + 1], a.scale_log2, -msub));
+            const float2 pp = ex2x2(fmaf(sv[gq * 8 + 2 * u], a.scale_log2, -msub),
+                                    fmaf(sv[gq * 8 + 2 * u + 1], a.scale_log2, -msub));
+            const float p0 = pp.x, p1 = pp.y;
             rs += p0 + p1;
             __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
             pk[u] = *reinterpret_cast<uint32_t*>(&b2);
