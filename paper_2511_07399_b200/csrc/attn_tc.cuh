@@ -237,8 +237,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
       const uint32_t qa = tc::smem_u32(sQ), pa = tc::smem_u32(sP);
       auto issue_S = [&](int gg) {     // gg = local tile counter
         const int st = gg & 1;
+        // S_gg reuses the TMEM buffer of tile gg-2, whose P was consumed by PV_{gg-2}:
+        // issued earlier by this thread, and tcgen05 MMAs execute in issue order.
         tc::mbar_wait(k_full + st, (gg >> 1) & 1);
-        if (gg >= 2) tc::mbar_wait(s_empty + st, ((gg >> 1) - 1) & 1);
         tc::tc_fence_after();
         const uint32_t ka = tc::smem_u32(sK + st * SM::KV);
 #pragma unroll
@@ -268,10 +269,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
             tc::mbar_wait(p_full + hh, gt & 1);
             tc::tc_fence_after();
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const uint32_t poff = hh * (kAttnBQ * 128) + k * 32;
-              tc::mma_bf16(tO2[hh], tc::sw128_kmajor_desc(pa + poff),
-                           tc::sw128_mnmajor_desc(va + (hh * 4 + k) * 2048, kAttnBKV * 128), idO, (t | k) != 0);
+            for (int k = 0; k < 4; ++k) {   // A = P_half from TMEM (bf16 pairs, 8 columns per K=16)
+              tc::mma_bf16_ts(tO2[hh], tS[gt & 1] + hh * 64 + k * 8,
+                              tc::sw128_mnmajor_desc(va + (hh * 4 + k) * 2048, kAttnBKV * 128), idO, (t | k) != 0);
             }
             tc::mma_commit(p_empty + hh);
           }
@@ -315,9 +315,6 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
 #pragma unroll
           for (int i = 0; i < 32; ++i) sv[cc * 32 + i] = __uint_as_float(r[i]);
         }
-        tc::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(s_empty + st);
         const int kvalid = Lk - (s.jb + t) * kAttnBKV - half * HC;
         float mx = -INFINITY;
         if (kvalid >= HC) {
@@ -359,28 +356,21 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
           }
           m_used = m_new;
         }
-        // P = exp2(s * scale - m_used) -> bf16, this half = P chunk `half` (64 keys, 128 B/row);
-        // a half with no valid key yet (m_used = -inf) writes P = 0
+        // P = exp2(s * scale - m_used) -> bf16 pairs written over this half's own S columns
+        // in TMEM (A operand of the PV MMA); a half with no valid key yet writes P = 0
         const float msub = m_used == -INFINITY ? 0.f : m_used;
         float rs = 0.f;
-        uint8_t* prow_base = sP + half * (kAttnBQ * 128) + (row >> 3) * 1024 + (row & 7) * 128;
+        uint32_t pk[HC / 2];
 #pragma unroll
-        for (int gq = 0; gq < HC / 8; ++gq) {
-          uint32_t pk[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const float2 pp = ex2x2(fmaf(sv[gq * 8 + 2 * u], a.scale_log2, -msub),
-                                    fmaf(sv[gq * 8 + 2 * u + 1], a.scale_log2, -msub));
-            const float p0 = pp.x, p1 = pp.y;
-            rs += p0 + p1;
-            __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
-            pk[u] = *reinterpret_cast<uint32_t*>(&b2);
-          }
-          uint8_t* dst = prow_base + ((gq ^ (row & 7)) << 4);
-          *reinterpret_cast<uint4*>(dst) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        for (int i = 0; i < HC / 2; ++i) {
+          const float2 pp = ex2x2(fmaf(sv[2 * i], a.scale_log2, -msub), fmaf(sv[2 * i + 1], a.scale_log2, -msub));
+          rs += pp.x + pp.y;
+          __nv_bfloat162 b2 = __floats2bfloat162_rn(pp.x, pp.y);
+          pk[i] = *reinterpret_cast<uint32_t*>(&b2);
         }
+        tc::tmem_st32(tS[st] + lane_off + half * HC, pk);
+        tc::tmem_st_wait();
         l += rs;
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(p_full + half);
