@@ -34,7 +34,8 @@ struct AttnSmem {
   static constexpr int Q = kAttnBQ * HD * 2;          // 32 KB (hd 128)
   static constexpr int KV = kAttnBKV * HD * 2;        // one K or V tile
   static constexpr int P = kAttnBQ * kAttnBKV * 2;    // 32 KB
-  static constexpr int total = Q + 4 * KV + P + 1024 + 256 + 512 * 4;
+  static constexpr int KS = 3, VS = 2;               // K / V ring stages
+  static constexpr int total = Q + (KS + VS) * KV + 1024 + 256 + 512 * 4;
 };
 
 struct AttnTcArgs {
@@ -83,7 +84,7 @@ struct AttnGeo {
   __device__ int cta_of(long long g, int G) const { return int(((g + 1) * G + T - 1) / T) - 1; }
 };
 
-constexpr int kAttnThreads = 320;   // warp 0 TMA, 1 MMA, 2..9 softmax (two column halves)
+constexpr int kAttnThreads = 352;   // warp 0 TMA Q+K, 1 MMA, 2..9 softmax (two key halves), 10 TMA V
 
 __device__ __forceinline__ float ex2(float x) {
   float y;
@@ -111,23 +112,22 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
-  uint8_t* sK = sQ + SM::Q;                 // 2 stages
-  uint8_t* sV = sK + 2 * SM::KV;            // 2 stages
-  uint8_t* sP = sV + 2 * SM::KV;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sP + SM::P);
+  constexpr int KS = SM::KS, VS = SM::VS;
+  uint8_t* sK = sQ + SM::Q;                 // KS stages
+  uint8_t* sV = sK + KS * SM::KV;           // VS stages
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sV + VS * SM::KV);
   uint64_t* q_full = bar;
-  uint64_t* k_full = bar + 1;   // [2]
-  uint64_t* k_empty = bar + 3;  // [2]
-  uint64_t* v_full = bar + 5;   // [2]
-  uint64_t* v_empty = bar + 7;  // [2]
-  uint64_t* s_full = bar + 9;   // [2]
-  uint64_t* s_empty = bar + 11; // [2]
-  uint64_t* p_full = bar + 13;   // [2] per key half (4 softmax warps each)
-  uint64_t* p_empty = bar + 19;  // [2] per key half (PV of that half done)
-  uint64_t* q_empty = bar + 15;
-  uint64_t* o_empty = bar + 16;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 18);
-  float* xch = reinterpret_cast<float*>(bar + 22);   // [2 halves][128] (max, sum) exchange at segment end
+  uint64_t* q_empty = bar + 1;
+  uint64_t* o_empty = bar + 2;
+  uint64_t* p_full = bar + 3;    // [2] per key half (4 softmax warps each)
+  uint64_t* p_empty = bar + 5;   // [2] per key half (PV of that half done)
+  uint64_t* s_full = bar + 7;    // [2]
+  uint64_t* k_full = bar + 9;    // [KS]
+  uint64_t* k_empty = bar + 12;  // [KS]
+  uint64_t* v_full = bar + 15;   // [VS]
+  uint64_t* v_empty = bar + 17;  // [VS]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 19);
+  float* xch = reinterpret_cast<float*>(bar + 20);   // [2 halves][128] (max, sum) exchange at segment end
 
   pdl_wait();      // q, K/V lanes and o are produced / consumed by the neighbouring kernels
   pdl_trigger();
@@ -154,14 +154,15 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
     tc::mbar_init(q_full, 1);
     tc::mbar_init(q_empty, 1);
     tc::mbar_init(o_empty, 8);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < KS; ++s) {
       tc::mbar_init(k_full + s, 1);
       tc::mbar_init(k_empty + s, 1);
+    }
+    for (int s = 0; s < VS; ++s) {
       tc::mbar_init(v_full + s, 1);
       tc::mbar_init(v_empty + s, 1);
-      tc::mbar_init(s_full + s, 1);
-      tc::mbar_init(s_empty + s, 8);
     }
+    for (int s = 0; s < 2; ++s) tc::mbar_init(s_full + s, 1);
     for (int hh = 0; hh < 2; ++hh) {
       tc::mbar_init(p_full + hh, 4);
       tc::mbar_init(p_empty + hh, 1);
@@ -212,21 +213,37 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
         for (int ch = 0; ch < NCH; ++ch)
           tc::tma_load_2d(sQ + ch * (kAttnBQ * 128), &tmQ, q_full, col + ch * 64, s.e * a.L + s.q0);
         for (int j = s.jb; j < s.je; ++j, ++gi) {
-          const int st = gi & 1;
-          const uint32_t ph = ((gi >> 1) & 1) ^ 1;
-          tc::mbar_wait(k_empty + st, ph);
+          const int st = gi % KS;
+          tc::mbar_wait(k_empty + st, ((gi / KS) & 1) ^ 1);
           tc::mbar_expect_tx(k_full + st, SM::KV);
           for (int ch = 0; ch < NCH; ++ch)
             tc::tma_load_2d(sK + st * SM::KV + ch * (kAttnBKV * 128), &tmK, k_full + st, col + ch * 64,
                             kv_row + j * kAttnBKV);
-          tc::mbar_wait(v_empty + st, ph);
+        }
+        g = s.ge;
+        ++sg;
+      }
+    }
+  } else if (warp == 10) {
+    // ------------------------------------------------------------ TMA producer (V)
+    // V tiles are consumed one MMA phase later than K: an own producer keeps the K
+    // prefetch from waiting on V slots.
+    if (lane == 0) {
+      long long g = t0;
+      int gi = 0;
+      while (g < t1) {
+        const Seg s = seg_at(g);
+        const int col = s.h * HD;
+        const int kv_row = a.kv_row0 + (a.cross ? (td->e[s.e].pver & 1) : s.e) * a.kv_lane_rows;
+        for (int j = s.jb; j < s.je; ++j, ++gi) {
+          const int st = gi % VS;
+          tc::mbar_wait(v_empty + st, ((gi / VS) & 1) ^ 1);
           tc::mbar_expect_tx(v_full + st, SM::KV);
           for (int ch = 0; ch < NCH; ++ch)
             tc::tma_load_2d(sV + st * SM::KV + ch * (kAttnBKV * 128), &tmV, v_full + st, col + ch * 64,
                             kv_row + j * kAttnBKV);
         }
         g = s.ge;
-        ++sg;
       }
     }
   } else if (warp == 1) {
@@ -234,21 +251,22 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
     if (lane == 0) {
       const uint32_t idS = tc::idesc_bf16(kAttnBQ, kAttnBKV);
       const uint32_t idO = tc::idesc_bf16(kAttnBQ, HD, true);
-      const uint32_t qa = tc::smem_u32(sQ), pa = tc::smem_u32(sP);
+      const uint32_t qa = tc::smem_u32(sQ);
       auto issue_S = [&](int gg) {     // gg = local tile counter
-        const int st = gg & 1;
+        const int st = gg & 1;         // S / P TMEM buffer
+        const int ks = gg % KS;        // K smem stage
         // S_gg reuses the TMEM buffer of tile gg-2, whose P was consumed by PV_{gg-2}:
         // issued earlier by this thread, and tcgen05 MMAs execute in issue order.
-        tc::mbar_wait(k_full + st, (gg >> 1) & 1);
+        tc::mbar_wait(k_full + ks, (gg / KS) & 1);
         tc::tc_fence_after();
-        const uint32_t ka = tc::smem_u32(sK + st * SM::KV);
+        const uint32_t ka = tc::smem_u32(sK + ks * SM::KV);
 #pragma unroll
         for (int k = 0; k < HD / 16; ++k) {
           const uint32_t off = (k >> 2) * (kAttnBQ * 128) + (k & 3) * 32;
           const uint32_t koff = (k >> 2) * (kAttnBKV * 128) + (k & 3) * 32;
           tc::mma_bf16(tS[st], tc::sw128_kmajor_desc(qa + off), tc::sw128_kmajor_desc(ka + koff), idS, k > 0);
         }
-        tc::mma_commit(k_empty + st);
+        tc::mma_commit(k_empty + ks);
         tc::mma_commit(s_full + st);
       };
       long long g = t0;
@@ -261,9 +279,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
         if (nt > 1) issue_S(gi + 1);
         for (int t = 0; t < nt; ++t) {
           const int gt = gi + t;
-          tc::mbar_wait(v_full + (gt & 1), (gt >> 1) & 1);
+          tc::mbar_wait(v_full + (gt % VS), (gt / VS) & 1);
           if (t == 0 && sg > 0) tc::mbar_wait(o_empty, (sg - 1) & 1);
-          const uint32_t va = tc::smem_u32(sV + (gt & 1) * SM::KV);
+          const uint32_t va = tc::smem_u32(sV + (gt % VS) * SM::KV);
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {   // O_h += P[:, 64h : 64h+64] V[64h : 64h+64, :]
             tc::mbar_wait(p_full + hh, gt & 1);
@@ -275,7 +293,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
             }
             tc::mma_commit(p_empty + hh);
           }
-          tc::mma_commit(v_empty + (gt & 1));
+          tc::mma_commit(v_empty + (gt % VS));
           if (t + 2 < nt) issue_S(gt + 2);
         }
         tc::mma_commit(q_empty);
@@ -284,7 +302,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
         ++sg;
       }
     }
-  } else {
+  } else if (warp <= 9) {
     // ------------------------------------------------ softmax / correction / epilogue
     // 8 warps: TMEM lane quarter = warp & 3 (row), column half = (warp - 2) / 4.
     constexpr int HC = kAttnBKV / 2;            // S columns per thread
