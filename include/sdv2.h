@@ -208,7 +208,7 @@ sdv2_status sdv2_debug_gemm(const void* A, const void* W, const float* bias, voi
 
 /* Kernel-level test hook: tensor-core attention softmax(q K^T / sqrt(hd)) V for one
  * query block q [Lq, H*hd] over keys K/V [Lk, H*hd] (bf16, device) -> o [Lq, H*hd]
- * bf16.  `scratch` is >= 1 KB of device memory.  Synchronises `stream`. */
+ * bf16.  `scratch` is >= 1 KB of device memory; enqueued on `stream`. */
 sdv2_status sdv2_debug_attention(const void* q, const void* K, const void* V, void* o, int32_t Lq, int32_t Lk,
                                  int32_t H, int32_t hd, void* scratch, void* stream);
 

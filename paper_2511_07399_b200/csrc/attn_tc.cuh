@@ -346,12 +346,13 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
           }
         }
         mx *= a.scale_log2;
-        // PV of this half's previous tile finished: its P chunk is free and O_half stable
-        if (gt > 0) tc::mbar_wait(p_empty + half, (gt - 1) & 1);
-        tc::tc_fence_after();
+        // P_t lands in S buffer t&1 (not the one PV_{t-1} reads), so the softmax runs ahead
+        // of the PV MMAs; only an O rescale needs PV_{t-1} of this half to be complete.
         if (mx > m_used + 8.f) {
           const float m_new = mx;
           if (t > 0) {     // rescale this half's O row (all HD columns) in TMEM
+            tc::mbar_wait(p_empty + half, (gt - 1) & 1);
+            tc::tc_fence_after();
             const float alpha = ex2(m_used - m_new);
             l *= alpha;
 #pragma unroll
