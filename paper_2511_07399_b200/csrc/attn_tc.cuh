@@ -35,7 +35,7 @@ struct AttnSmem {
   static constexpr int KV = kAttnBKV * HD * 2;        // one K or V tile
   static constexpr int P = kAttnBQ * kAttnBKV * 2;    // 32 KB
   static constexpr int KS = 3, VS = 2;               // K / V ring stages
-  static constexpr int total = Q + (KS + VS) * KV + 1024 + 256 + 512 * 4;
+  static constexpr int total = Q + (KS + VS) * KV + 1024 + 256 + 512 * 4 + 64;
 };
 
 struct AttnTcArgs {
@@ -119,15 +119,18 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
   uint64_t* q_full = bar;
   uint64_t* q_empty = bar + 1;
   uint64_t* o_empty = bar + 2;
-  uint64_t* p_full = bar + 3;    // [2] per key half (4 softmax warps each)
-  uint64_t* p_empty = bar + 5;   // [2] per key half (PV of that half done)
-  uint64_t* s_full = bar + 7;    // [2]
-  uint64_t* k_full = bar + 9;    // [KS]
-  uint64_t* k_empty = bar + 12;  // [KS]
-  uint64_t* v_full = bar + 15;   // [VS]
-  uint64_t* v_empty = bar + 17;  // [VS]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 19);
-  float* xch = reinterpret_cast<float*>(bar + 20);   // [2 halves][128] (max, sum) exchange at segment end
+  // p_full / p_empty are indexed [S buffer][key half]: with the softmax running ahead of
+  // the PV MMAs, per-buffer barriers never get more than one phase ahead of a waiter
+  // (parity waits stay unambiguous).
+  uint64_t* p_full = bar + 3;    // [2][2] P of (buffer, half) written (4 softmax warps)
+  uint64_t* p_empty = bar + 7;   // [2][2] PV of (buffer, half) done
+  uint64_t* s_full = bar + 11;   // [2]
+  uint64_t* k_full = bar + 13;   // [KS]
+  uint64_t* k_empty = bar + 16;  // [KS]
+  uint64_t* v_full = bar + 19;   // [VS]
+  uint64_t* v_empty = bar + 21;  // [VS]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 23);
+  float* xch = reinterpret_cast<float*>(bar + 24);   // [2 halves][128] (max, sum) exchange at segment end
 
   pdl_wait();      // q, K/V lanes and o are produced / consumed by the neighbouring kernels
   pdl_trigger();
@@ -163,9 +166,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
       tc::mbar_init(v_empty + s, 1);
     }
     for (int s = 0; s < 2; ++s) tc::mbar_init(s_full + s, 1);
-    for (int hh = 0; hh < 2; ++hh) {
-      tc::mbar_init(p_full + hh, 4);
-      tc::mbar_init(p_empty + hh, 1);
+    for (int i = 0; i < 4; ++i) {
+      tc::mbar_init(p_full + i, 4);
+      tc::mbar_init(p_empty + i, 1);
     }
     tc::fence_barrier_init();
   }
@@ -284,14 +287,14 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
           const uint32_t va = tc::smem_u32(sV + (gt % VS) * SM::KV);
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {   // O_h += P[:, 64h : 64h+64] V[64h : 64h+64, :]
-            tc::mbar_wait(p_full + hh, gt & 1);
+            tc::mbar_wait(p_full + (gt & 1) * 2 + hh, (gt >> 1) & 1);
             tc::tc_fence_after();
 #pragma unroll
             for (int k = 0; k < 4; ++k) {   // A = P_half from TMEM (bf16 pairs, 8 columns per K=16)
               tc::mma_bf16_ts(tO2[hh], tS[gt & 1] + hh * 64 + k * 8,
                               tc::sw128_mnmajor_desc(va + (hh * 4 + k) * 2048, kAttnBKV * 128), idO, (t | k) != 0);
             }
-            tc::mma_commit(p_empty + hh);
+            tc::mma_commit(p_empty + (gt & 1) * 2 + hh);
           }
           tc::mma_commit(v_empty + (gt % VS));
           if (t + 2 < nt) issue_S(gt + 2);
@@ -351,7 +354,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
         if (mx > m_used + 8.f) {
           const float m_new = mx;
           if (t > 0) {     // rescale this half's O row (all HD columns) in TMEM
-            tc::mbar_wait(p_empty + half, (gt - 1) & 1);
+            tc::mbar_wait(p_empty + ((gt - 1) & 1) * 2 + half, ((gt - 1) >> 1) & 1);
             tc::tc_fence_after();
             const float alpha = ex2(m_used - m_new);
             l *= alpha;
@@ -392,14 +395,15 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
         l += rs;
         tc::tc_fence_before();
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive(p_full + half);
+        if (lane == 0) tc::mbar_arrive(p_full + (gt & 1) * 2 + half);
       }
       // end of segment: wait for this half's last PV; exchange (m, l) with the other half
-      tc::mbar_wait(p_empty + half, (gi + nt - 1) & 1);
+      const int gl = gi + nt - 1;   // last tile of the segment
+      tc::mbar_wait(p_empty + (gl & 1) * 2 + half, (gl >> 1) & 1);
       xch[half * 256 + row] = m_used;
       xch[half * 256 + 128 + row] = l;
       asm volatile("bar.sync 1, 256;" ::: "memory");
-      tc::mbar_wait(p_empty + (half ^ 1), (gi + nt - 1) & 1);   // other half's O complete too
+      tc::mbar_wait(p_empty + (gl & 1) * 2 + (half ^ 1), (gl >> 1) & 1);   // other half's O complete too
       tc::tc_fence_after();
       const float m0 = xch[row], l0 = xch[128 + row], m1 = xch[256 + row], l1 = xch[384 + row];
       const float M = fmaxf(m0, m1);
