@@ -91,23 +91,6 @@ __device__ __forceinline__ float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-// exp2 on the FMA / ALU pipes (no MUFU): round-to-nearest split x = n + f, f in [-1/2, 1/2],
-// degree-3 fit of 2^f (max rel. error 1.8e-4, below bf16's 2^-9), 2^n by exponent add.
-__device__ __forceinline__ float exp2_poly(float x) {
-  x = fmaxf(x, -127.f);
-  const float j = x + 12582912.f;                 // 1.5 * 2^23: integer part in the mantissa
-  const float f = x - (j - 12582912.f);
-  const float p = fmaf(fmaf(fmaf(0.05460262f, f, 0.24192413f), f, 0.69331648f), f, 1.f);
-  return __int_as_float(__float_as_int(p) + ((__float_as_int(j) - 0x4B400000) << 23));
-}
-// bf16 by truncation (ALU byte-permute instead of an XU conversion); the caller sums the
-// truncated values so the softmax normalisation matches the MMA operand exactly.
-__device__ __forceinline__ float trunc_bf16(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFF0000u); }
-__device__ __forceinline__ uint32_t pack_trunc_bf16x2(float lo, float hi) {
-  uint32_t r;
-  asm("prmt.b32 %0, %1, %2, 0x7632;" : "=r"(r) : "r"(__float_as_uint(lo)), "r"(__float_as_uint(hi)));
-  return r;
-}
 // Two exp2 per MUFU op: the softmax probabilities are rounded to bf16 (8-bit mantissa)
 // for the PV MMA anyway; fp16 arguments (x <= 8 after the lazy-rescale threshold) lose
 // precision only for terms below 2^-16 of the row maximum.
@@ -399,15 +382,13 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
         // in TMEM (A operand of the PV MMA); a half with no valid key yet writes P = 0
         const float msub = m_used == -INFINITY ? 0.f : m_used;
         float rs = 0.f;
-        // XU-pipe budget: half of the exps on MUFU, half as an FMA-pipe polynomial;
-        // bf16 packing by truncation on the ALU pipe.
         uint32_t pk[HC / 2];
 #pragma unroll
         for (int i = 0; i < HC / 2; ++i) {
-          const float p0 = trunc_bf16(ex2(fmaf(sv[2 * i], a.scale_log2, -msub)));
-          const float p1 = trunc_bf16(exp2_poly(fmaf(sv[2 * i + 1], a.scale_log2, -msub)));
-          rs += p0 + p1;
-          pk[i] = pack_trunc_bf16x2(p0, p1);
+          const float2 pp = ex2x2(fmaf(sv[2 * i], a.scale_log2, -msub), fmaf(sv[2 * i + 1], a.scale_log2, -msub));
+          rs += pp.x + pp.y;
+          __nv_bfloat162 b2 = __floats2bfloat162_rn(pp.x, pp.y);
+          pk[i] = *reinterpret_cast<uint32_t*>(&b2);
         }
         tc::tmem_st32(tS[st] + lane_off + half * HC, pk);
         tc::tmem_st_wait();
