@@ -1150,13 +1150,18 @@ extern "C" sdv2_status sdv2_debug_attention(const void* q, const void* K, const 
     attn_plan_init(ap, gp.encode, std::min(gp.num_sms, kMaxSMs));
     ready = true;
   }
-  ap.maps.clear();
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  TickDesc tdh;
-  std::memset(&tdh, 0, sizeof(tdh));
-  tdh.n_active = 1;
-  tdh.e[0].active = 1;
-  if (cudaMemcpyAsync(scratch, &tdh, sizeof(tdh), cudaMemcpyHostToDevice, s) != cudaSuccess) return SDV2_E_CUDA;
+  // one active entry; written once per scratch buffer (a pageable copy per call would
+  // serialise the stream and pollute kernel timings)
+  static void* last_scratch = nullptr;
+  if (scratch != last_scratch) {
+    TickDesc tdh;
+    std::memset(&tdh, 0, sizeof(tdh));
+    tdh.n_active = 1;
+    tdh.e[0].active = 1;
+    if (cudaMemcpy(scratch, &tdh, sizeof(tdh), cudaMemcpyHostToDevice) != cudaSuccess) return SDV2_E_CUDA;
+    last_scratch = scratch;
+  }
   static float* part = nullptr;
   if (!part && cudaMalloc(&part, attn_scratch_floats(kMaxSMs, 128) * 4) != cudaSuccess) return SDV2_E_CUDA;
   AttnTcArgs ta{};
