@@ -34,8 +34,10 @@ struct AttnSmem {
   static constexpr int Q = kAttnBQ * HD * 2;          // 32 KB (hd 128)
   static constexpr int KV = kAttnBKV * HD * 2;        // one K or V tile
   static constexpr int P = kAttnBQ * kAttnBKV * 2;    // 32 KB
-  static constexpr int KS = 3, VS = 2;               // K / V ring stages
-  static constexpr int total = Q + (KS + VS) * KV + 1024 + 256 + 512 * 4 + 64;
+  // K / V ring stages.  V is consumed a softmax later than K and its loads see ~2800
+  // cycles of latency under load (tools/attn_trace.py): the deeper ring goes to V.
+  static constexpr int KS = 2, VS = 3;
+  static constexpr int total = Q + (KS + VS) * KV + 1024 + 256 + 768 * 4 + 64;
 };
 
 struct AttnTcArgs {
@@ -52,14 +54,27 @@ struct AttnTcArgs {
   float* part_o;       // [G][2][128][HD] fp32 partial (unnormalised) O
   float* part_ml;      // [G][2][128][2] running max (log2 domain), sum
   int per_unit;        // 1: one CTA per unit (grid = units, no merge); 0: stream-K
+  int dbg;             // test hook only (pipeline timing): bit 0 skips the softmax math,
+                       // bit 1 the MMAs, bit 2 the K/V loads, bit 3 the PV MMAs, bit 4 the
+                       // S MMAs; 0 in the product path
+  long long* trace;    // test hook only: per-tile clock64 stamps of CTA 0 (nullptr = off)
 };
+
+// Pipeline trace (test hook): stamp event `ev` of local tile `t` (CTA 0, first 256 tiles).
+#define ATTN_TRACE(ev, t)                                                  \
+  do {                                                                     \
+    if (a.trace != nullptr && blockIdx.x == 0 && lane == 0 && (t) < 256)   \
+      a.trace[(t) * 16 + (ev)] = clock64();                                \
+  } while (0)
 
 // Stream-K geometry shared by the attention and the combine kernels.
 struct AttnGeo {
   long long off[kMaxSteps + 1];   // tile offset of entry e's first unit
   int J[kMaxSteps];               // key tiles per unit of entry e
   long long T;                    // total tiles
-  __device__ void init(const AttnTcArgs& a, const TickDesc* td) {
+  int QP;                         // query-tile groups per head (CL query tiles per group)
+  __device__ void init(const AttnTcArgs& a, const TickDesc* td, int CL) {
+    QP = (a.QT + CL - 1) / CL;
     off[0] = 0;
     for (int e = 0; e < kMaxSteps; ++e) {
       int j = 0;
@@ -68,7 +83,7 @@ struct AttnGeo {
         j = (Lk + kAttnBKV - 1) / kAttnBKV;
       }
       J[e] = j;
-      off[e + 1] = off[e] + (long long)a.H * a.QT * j;
+      off[e + 1] = off[e] + (long long)a.H * QP * j;
     }
     T = off[kMaxSteps];
   }
@@ -91,18 +106,81 @@ __device__ __forceinline__ float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-// Two exp2 per MUFU op: the softmax probabilities are rounded to bf16 (8-bit mantissa)
-// for the PV MMA anyway; fp16 arguments (x <= 8 after the lazy-rescale threshold) lose
-// precision only for terms below 2^-16 of the row maximum.
-__device__ __forceinline__ float2 ex2x2(float x0, float x1) {
-  uint32_t in, out;
-  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(in) : "f"(x1), "f"(x0));
-  asm("ex2.approx.f16x2 %0, %1;" : "=r"(out) : "r"(in));
-  __half2 h = *reinterpret_cast<__half2*>(&out);
-  return __half22float2(h);
+// Packed fp32x2 arithmetic (sm_100 FFMA2 / FADD2): two softmax elements per instruction.
+__device__ __forceinline__ uint64_t f2pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float2 f2unpack(uint64_t r) {
+  float2 v;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+  return v;
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.ftz.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.ftz.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t fsub2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("sub.rn.ftz.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// 2^x for a pair on the FMA / ALU pipes instead of the MUFU (which would otherwise pace
+// the softmax at one ex2 per element): x = n + f with n = rint(x) (magic-number add),
+// 2^f on [-1/2, 1/2] by a degree-3 minimax polynomial (max rel. error 7.5e-5, far below
+// the bf16 rounding of P), and n added into the exponent field.  x is clamped at -126 so
+// the exponent never wraps; callers use it only on tiles with no masked (-inf) key.
+__device__ __forceinline__ float2 ex2_poly2(uint64_t x2) {
+  float2 x = f2unpack(x2);
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
+  const uint64_t magic = f2pack(12582912.f, 12582912.f);   // 1.5 * 2^23
+  const uint64_t xc = f2pack(x.x, x.y);
+  const uint64_t t = fadd2(xc, magic);
+  const uint64_t f = fsub2(xc, fsub2(t, magic));
+  uint64_t p = ffma2(f2pack(0.0551716685f, 0.0551716685f), f, f2pack(0.242611155f, 0.242611155f));
+  p = ffma2(p, f, f2pack(0.693260968f, 0.693260968f));
+  p = ffma2(p, f, f2pack(0.999928057f, 0.999928057f));
+  const float2 pv = f2unpack(p), tv = f2unpack(t);
+  return make_float2(__uint_as_float(__float_as_uint(pv.x) + (__float_as_uint(tv.x) << 23)),
+                     __uint_as_float(__float_as_uint(pv.y) + (__float_as_uint(tv.y) << 23)));
 }
 
-template <int HD>
+// P = 2^(s * scale - m) for one thread's HC scores -> bf16 pairs in pk, returns the row
+// sum.  POLY: pairs with i % 8 in {2, 5, 7} (3/8) use ex2_poly2 instead of the MUFU.
+template <int HC, bool POLY>
+__device__ __forceinline__ float p_row(const float* sv, uint32_t* pk, uint64_t sc2, uint64_t nm2) {
+  uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};   // packed row-sum chains (0.0f bits)
+#pragma unroll
+  for (int i = 0; i < HC / 2; ++i) {
+    const uint64_t x2 = ffma2(f2pack(sv[2 * i], sv[2 * i + 1]), sc2, nm2);
+    float2 pp;
+    if (POLY && ((i & 7) == 2 || (i & 7) == 5 || (i & 7) == 7)) {
+      pp = ex2_poly2(x2);
+    } else {
+      const float2 x = f2unpack(x2);
+      pp = make_float2(ex2(x.x), ex2(x.y));
+    }
+    acc[i & 3] = fadd2(acc[i & 3], f2pack(pp.x, pp.y));
+    __nv_bfloat162 b2 = __floats2bfloat162_rn(pp.x, pp.y);
+    pk[i] = *reinterpret_cast<uint32_t*>(&b2);
+  }
+  const float2 s01 = f2unpack(fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3])));
+  return s01.x + s01.y;
+}
+
+// CL = CTAs per cluster along the query tiles of one head (1 or 2).  With CL = 2 the
+// pair walks the same key tiles; each CTA loads half of every K / V tile and multicasts
+// it to both, halving the L2 -> SM traffic (every query tile of a head otherwise
+// re-reads the whole lane).
+template <int HD, int CL>
 __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ,
                                                          const __grid_constant__ CUtensorMap tmK,
                                                          const __grid_constant__ CUtensorMap tmV, AttnTcArgs a,
@@ -118,28 +196,32 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
   uint64_t* bar = reinterpret_cast<uint64_t*>(sV + VS * SM::KV);
   uint64_t* q_full = bar;
   uint64_t* q_empty = bar + 1;
-  uint64_t* o_empty = bar + 2;
-  // p_full / p_empty are indexed [S buffer][key half]: with the softmax running ahead of
-  // the PV MMAs, per-buffer barriers never get more than one phase ahead of a waiter
-  // (parity waits stay unambiguous).
-  uint64_t* p_full = bar + 3;    // [2][2] P of (buffer, half) written (4 softmax warps)
-  uint64_t* p_empty = bar + 7;   // [2][2] PV of (buffer, half) done
-  uint64_t* s_full = bar + 11;   // [2]
-  uint64_t* k_full = bar + 13;   // [KS]
-  uint64_t* k_empty = bar + 16;  // [KS]
-  uint64_t* v_full = bar + 19;   // [VS]
-  uint64_t* v_empty = bar + 21;  // [VS]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 23);
-  float* xch = reinterpret_cast<float*>(bar + 24);   // [2 halves][128] (max, sum) exchange at segment end
+  uint64_t* o_empty = bar + 2;   // O read out by the 8 softmax warps at a segment end
+  // S / P TMEM buffers rotate over 3 slots (tile gt uses slot gt % 3, phase (gt / 3) & 1):
+  // S_{t+2} is issued before PV_t, so the tensor pipe never waits on the softmax of the
+  // tile it has just finished.  No waiter can fall two phases behind (S_{t+3} needs PV_t,
+  // which needs P_t).
+  uint64_t* s_full = bar + 3;    // [3] S ready (MMA commit)
+  uint64_t* p_full = bar + 6;    // [3] P written (8 softmax warps)
+  uint64_t* pv_done = bar + 9;   // [3] PV complete (MMA commit)
+  uint64_t* k_full = bar + 12;       // [KS]
+  uint64_t* k_empty = k_full + KS;   // [KS]
+  uint64_t* v_full = k_empty + KS;   // [VS]
+  uint64_t* v_empty = v_full + VS;   // [VS]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(v_empty + VS);
+  float* xm = reinterpret_cast<float*>(bar + 32);   // [2 tile parity][2 halves][128] row-max exchange
+  float* xl = xm + 512;                             // [2 halves][128] row-sum exchange at segment end
 
   pdl_wait();      // q, K/V lanes and o are produced / consumed by the neighbouring kernels
   pdl_trigger();
   AttnGeo geo;
-  geo.init(a, td);
-  const int G = gridDim.x, c = blockIdx.x;
+  geo.init(a, td, CL);
+  const int G = gridDim.x / CL, c = blockIdx.x / CL;   // cluster (query-tile group) index
+  const int cr = CL > 1 ? int(tc::cluster_ctarank()) : 0;
+  const uint16_t mc_mask = uint16_t((1u << CL) - 1);
   long long t0, t1;
   if (a.per_unit) {
-    const int e = c / (a.H * a.QT), w = c % (a.H * a.QT);
+    const int e = c / (a.H * geo.QP), w = c % (a.H * geo.QP);
     if (e >= kMaxSteps || geo.J[e] == 0) return;
     t0 = geo.off[e] + (long long)w * geo.J[e];
     t1 = t0 + geo.J[e];
@@ -159,29 +241,30 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
     tc::mbar_init(o_empty, 8);
     for (int s = 0; s < KS; ++s) {
       tc::mbar_init(k_full + s, 1);
-      tc::mbar_init(k_empty + s, 1);
+      tc::mbar_init(k_empty + s, CL);   // both CTAs' MMAs release a multicast stage
     }
     for (int s = 0; s < VS; ++s) {
       tc::mbar_init(v_full + s, 1);
-      tc::mbar_init(v_empty + s, 1);
+      tc::mbar_init(v_empty + s, CL);
     }
-    for (int s = 0; s < 2; ++s) tc::mbar_init(s_full + s, 1);
-    for (int i = 0; i < 4; ++i) {
-      tc::mbar_init(p_full + i, 4);
-      tc::mbar_init(p_empty + i, 1);
+    for (int i = 0; i < 3; ++i) {
+      tc::mbar_init(s_full + i, 1);
+      tc::mbar_init(p_full + i, 8);
+      tc::mbar_init(pv_done + i, 1);
     }
     tc::fence_barrier_init();
   }
   if (warp == 0) tc::tmem_alloc(tmem_slot, 512);
   tc::tc_fence_before();
-  __syncthreads();
+  if (CL > 1) tc::cluster_sync();   // peer barriers initialised before any multicast
+  else __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tS[2] = {tmem, tmem + 128u};
-  // Each key half (64 of the 128 keys of a tile) has its own O accumulator and running
-  // max, so the two softmax warpgroups never synchronise per tile; they are merged once
-  // per unit.  TMEM: S0 | S1 | O_half0 | O_half1 (128 columns each).
-  const uint32_t tO2[2] = {tmem + 256u, tmem + 384u};
+  // TMEM: O (HD columns) | S0 | S1 | S2 (128 fp32 columns each, from column 128).  One O
+  // accumulator per row: the two softmax warps of a row (key halves) agree on the row
+  // max every tile through a shared-memory exchange.
+  const uint32_t tO = tmem;
+  auto tS = [&](int b) { return tmem + 128u + uint32_t(b) * 128u; };
 
   // Segment iteration: [gs, ge) of global tiles inside one unit.
   struct Seg {
@@ -192,8 +275,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
     Seg s;
     int w, j;
     geo.locate(g, s.e, w, j);
-    s.h = w / a.QT;
-    s.q0 = (w % a.QT) * kAttnBQ;
+    s.h = w / geo.QP;
+    s.q0 = ((w % geo.QP) * CL + cr) * kAttnBQ;
     s.J = geo.J[s.e];
     s.jb = j;
     const long long unit_end = g - j + s.J;
@@ -204,7 +287,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
+    {   // whole warp walks the loop; one elected lane issues
       long long g = t0;
       int gi = 0, sg = 0;   // local tile counter, segment counter
       while (g < t1) {
@@ -212,16 +295,33 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
         const int col = s.h * HD;
         const int kv_row = a.kv_row0 + (a.cross ? (td->e[s.e].pver & 1) : s.e) * a.kv_lane_rows;
         if (sg > 0) tc::mbar_wait(q_empty, (sg - 1) & 1);
-        tc::mbar_expect_tx(q_full, SM::Q);
-        for (int ch = 0; ch < NCH; ++ch)
-          tc::tma_load_2d(sQ + ch * (kAttnBQ * 128), &tmQ, q_full, col + ch * 64, s.e * a.L + s.q0);
+        if (tc::elect_one()) {
+          tc::mbar_expect_tx(q_full, SM::Q);
+          for (int ch = 0; ch < NCH; ++ch)
+            tc::tma_load_2d(sQ + ch * (kAttnBQ * 128), &tmQ, q_full, col + ch * 64, s.e * a.L + s.q0);
+        }
+        __syncwarp();
         for (int j = s.jb; j < s.je; ++j, ++gi) {
           const int st = gi % KS;
           tc::mbar_wait(k_empty + st, ((gi / KS) & 1) ^ 1);
-          tc::mbar_expect_tx(k_full + st, SM::KV);
-          for (int ch = 0; ch < NCH; ++ch)
-            tc::tma_load_2d(sK + st * SM::KV + ch * (kAttnBKV * 128), &tmK, k_full + st, col + ch * 64,
-                            kv_row + j * kAttnBKV);
+          ATTN_TRACE(8, gi);
+          if (tc::elect_one()) {
+            if (a.dbg & 4) {
+              tc::mbar_arrive(k_full + st);
+            } else {
+              tc::mbar_expect_tx(k_full + st, SM::KV);
+              for (int ch = 0; ch < NCH; ++ch) {
+                if (CL > 1)
+                  tc::tma_load_2d_mc(sK + st * SM::KV + ch * (kAttnBKV * 128) + cr * (kAttnBKV / CL) * 128, &tmK,
+                                     k_full + st, col + ch * 64, kv_row + j * kAttnBKV + cr * (kAttnBKV / CL),
+                                     mc_mask);
+                else
+                  tc::tma_load_2d(sK + st * SM::KV + ch * (kAttnBKV * 128), &tmK, k_full + st, col + ch * 64,
+                                  kv_row + j * kAttnBKV);
+              }
+            }
+          }
+          __syncwarp();
         }
         g = s.ge;
         ++sg;
@@ -231,7 +331,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
     // ------------------------------------------------------------ TMA producer (V)
     // V tiles are consumed one MMA phase later than K: an own producer keeps the K
     // prefetch from waiting on V slots.
-    if (lane == 0) {
+    {
       long long g = t0;
       int gi = 0;
       while (g < t1) {
@@ -241,36 +341,54 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
         for (int j = s.jb; j < s.je; ++j, ++gi) {
           const int st = gi % VS;
           tc::mbar_wait(v_empty + st, ((gi / VS) & 1) ^ 1);
-          tc::mbar_expect_tx(v_full + st, SM::KV);
-          for (int ch = 0; ch < NCH; ++ch)
-            tc::tma_load_2d(sV + st * SM::KV + ch * (kAttnBKV * 128), &tmV, v_full + st, col + ch * 64,
-                            kv_row + j * kAttnBKV);
+          ATTN_TRACE(9, gi);
+          if (tc::elect_one()) {
+            if (a.dbg & 4) {
+              tc::mbar_arrive(v_full + st);
+            } else {
+              tc::mbar_expect_tx(v_full + st, SM::KV);
+              for (int ch = 0; ch < NCH; ++ch) {
+                if (CL > 1)
+                  tc::tma_load_2d_mc(sV + st * SM::KV + ch * (kAttnBKV * 128) + cr * (kAttnBKV / CL) * 128, &tmV,
+                                     v_full + st, col + ch * 64, kv_row + j * kAttnBKV + cr * (kAttnBKV / CL),
+                                     mc_mask);
+                else
+                  tc::tma_load_2d(sV + st * SM::KV + ch * (kAttnBKV * 128), &tmV, v_full + st, col + ch * 64,
+                                  kv_row + j * kAttnBKV);
+              }
+            }
+          }
+          __syncwarp();
         }
         g = s.ge;
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    {   // whole warp walks the loop; one elected lane issues (see tc::elect_one)
       const uint32_t idS = tc::idesc_bf16(kAttnBQ, kAttnBKV);
       const uint32_t idO = tc::idesc_bf16(kAttnBQ, HD, true);
       const uint32_t qa = tc::smem_u32(sQ);
       auto issue_S = [&](int gg) {     // gg = local tile counter
-        const int st = gg & 1;         // S / P TMEM buffer
+        const int b = gg % 3;          // S / P TMEM slot: last read by PV_{gg-3}, issued earlier
         const int ks = gg % KS;        // K smem stage
-        // S_gg reuses the TMEM buffer of tile gg-2, whose P was consumed by PV_{gg-2}:
-        // issued earlier by this thread, and tcgen05 MMAs execute in issue order.
         tc::mbar_wait(k_full + ks, (gg / KS) & 1);
+        ATTN_TRACE(3, gg);
         tc::tc_fence_after();
         const uint32_t ka = tc::smem_u32(sK + ks * SM::KV);
+        if (tc::elect_one()) {
 #pragma unroll
-        for (int k = 0; k < HD / 16; ++k) {
-          const uint32_t off = (k >> 2) * (kAttnBQ * 128) + (k & 3) * 32;
-          const uint32_t koff = (k >> 2) * (kAttnBKV * 128) + (k & 3) * 32;
-          tc::mma_bf16(tS[st], tc::sw128_kmajor_desc(qa + off), tc::sw128_kmajor_desc(ka + koff), idS, k > 0);
+          for (int k = 0; k < HD / 16; ++k) {
+            const uint32_t off = (k >> 2) * (kAttnBQ * 128) + (k & 3) * 32;
+            const uint32_t koff = (k >> 2) * (kAttnBKV * 128) + (k & 3) * 32;
+            if (!(a.dbg & 18))
+              tc::mma_bf16(tS(b), tc::sw128_kmajor_desc(qa + off), tc::sw128_kmajor_desc(ka + koff), idS, k > 0);
+          }
+          if (CL > 1) tc::mma_commit_mc(k_empty + ks, mc_mask);
+          else tc::mma_commit(k_empty + ks);
+          tc::mma_commit(s_full + b);
         }
-        tc::mma_commit(k_empty + ks);
-        tc::mma_commit(s_full + st);
+        __syncwarp();
       };
       long long g = t0;
       int gi = 0, sg = 0;
@@ -278,28 +396,40 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
         const Seg s = seg_at(g);
         const int nt = s.je - s.jb;
         tc::mbar_wait(q_full, sg & 1);
+        auto release_q = [&]() {   // last S of the segment issued: Q smem reusable once it lands
+          if (tc::elect_one()) tc::mma_commit(q_empty);
+          __syncwarp();
+        };
         issue_S(gi);
         if (nt > 1) issue_S(gi + 1);
+        if (nt <= 2) release_q();
         for (int t = 0; t < nt; ++t) {
           const int gt = gi + t;
-          tc::mbar_wait(v_full + (gt % VS), (gt / VS) & 1);
-          if (t == 0 && sg > 0) tc::mbar_wait(o_empty, (sg - 1) & 1);
-          const uint32_t va = tc::smem_u32(sV + (gt % VS) * SM::KV);
-#pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {   // O_h += P[:, 64h : 64h+64] V[64h : 64h+64, :]
-            tc::mbar_wait(p_full + (gt & 1) * 2 + hh, (gt >> 1) & 1);
-            tc::tc_fence_after();
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {   // A = P_half from TMEM (bf16 pairs, 8 columns per K=16)
-              tc::mma_bf16_ts(tO2[hh], tS[gt & 1] + hh * 64 + k * 8,
-                              tc::sw128_mnmajor_desc(va + (hh * 4 + k) * 2048, kAttnBKV * 128), idO, (t | k) != 0);
-            }
-            tc::mma_commit(p_empty + (gt & 1) * 2 + hh);
+          if (t + 2 < nt) {
+            issue_S(gt + 2);
+            if (t + 3 == nt) release_q();
           }
-          tc::mma_commit(v_empty + (gt % VS));
-          if (t + 2 < nt) issue_S(gt + 2);
+          tc::mbar_wait(v_full + (gt % VS), (gt / VS) & 1);
+          ATTN_TRACE(0, gt);
+          if (t == 0 && sg > 0) tc::mbar_wait(o_empty, (sg - 1) & 1);
+          tc::mbar_wait(p_full + gt % 3, (gt / 3) & 1);
+          ATTN_TRACE(1, gt);
+          tc::tc_fence_after();
+          const uint32_t va = tc::smem_u32(sV + (gt % VS) * SM::KV);
+          if (tc::elect_one()) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {   // O += P V; A = P from TMEM (bf16 pairs, 8 columns per K=16):
+                                            // keys 64h..64h+63 sit in slot columns [64h, 64h+32)
+              if (!(a.dbg & 10))
+                tc::mma_bf16_ts(tO, tS(gt % 3) + (k >> 2) * 64 + (k & 3) * 8,
+                                tc::sw128_mnmajor_desc(va + k * 2048, kAttnBKV * 128), idO, (t | k) != 0);
+            }
+            if (CL > 1) tc::mma_commit_mc(v_empty + (gt % VS), mc_mask);
+            else tc::mma_commit(v_empty + (gt % VS));
+            tc::mma_commit(pv_done + gt % 3);
+          }
+          __syncwarp();
         }
-        tc::mma_commit(q_empty);
         gi += nt;
         g = s.ge;
         ++sg;
@@ -307,61 +437,83 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
     }
   } else if (warp <= 9) {
     // ------------------------------------------------ softmax / correction / epilogue
-    // 8 warps: TMEM lane quarter = warp & 3 (row), column half = (warp - 2) / 4.
+    // 8 warps: TMEM lane quarter = warp & 3 (row), key half = (warp - 2) / 4.  The two
+    // warps of a row quarter (same SMSP) exchange their half-row maxima every tile.
     constexpr int HC = kAttnBKV / 2;            // S columns per thread
-    constexpr int HO = HD / 2;                  // O columns per thread
+    constexpr int HO = HD / 2;                  // O columns per thread (rescale, epilogue)
     const int quarter = warp & 3;
     const int half = (warp - 2) >> 2;
     const int row = quarter * 32 + lane;
     const uint32_t lane_off = uint32_t(quarter * 32) << 16;
+    auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(2 + quarter) : "memory"); };
     long long g = t0;
     int gi = 0, sg = 0;
     while (g < t1) {
       const Seg s = seg_at(g);
       const int nt = s.je - s.jb;
       const int Lk = a.cross ? a.Lk_cross : td->e[s.e].nvalid * a.L;
-      float m_used = -INFINITY;   // max the current P / O are relative to (log2 domain)
+      float m_used = -INFINITY;   // row max the current P / O are relative to (log2 domain)
       float l = 0.f;              // this half's share of the row sum
       for (int t = 0; t < nt; ++t) {
         const int gt = gi + t;
-        const int st = gt & 1;
-        tc::mbar_wait(s_full + st, (gt >> 1) & 1);
+        const int b = gt % 3;
+        tc::mbar_wait(s_full + b, (gt / 3) & 1);
+        if (quarter == 0) ATTN_TRACE(4 + 2 * half, gt);
         tc::tc_fence_after();
-        float sv[HC];
+        if (a.dbg & 1) {   // timing experiment: no softmax work, P = 0
+          uint32_t z[32];
 #pragma unroll
-        for (int cc = 0; cc < HC / 32; ++cc) {
-          uint32_t r[32];
-          tc::tmem_ld32(tS[st] + lane_off + half * HC + cc * 32, r);
+          for (int i = 0; i < 32; ++i) z[i] = 0u;
+          tc::tmem_st32(tS(b) + lane_off + half * HC, z);
+          tc::tmem_st_wait();
+          l = 1.f;
+          m_used = 0.f;
+          tc::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(p_full + b);
+          if (quarter == 0) ATTN_TRACE(5 + 2 * half, gt);
+          continue;
+        }
+        float sv[HC];
+        {
+          uint32_t r[HC];
+#pragma unroll
+          for (int cc = 0; cc < HC / 32; ++cc)
+            tc::tmem_ld32(tS(b) + lane_off + half * HC + cc * 32, *reinterpret_cast<uint32_t(*)[32]>(r + cc * 32));
           tc::tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) sv[cc * 32 + i] = __uint_as_float(r[i]);
+          for (int i = 0; i < HC; ++i) sv[i] = __uint_as_float(r[i]);
         }
+        if (quarter == 0) ATTN_TRACE(10 + 2 * half, gt);
         const int kvalid = Lk - (s.jb + t) * kAttnBKV - half * HC;
-        float mx = -INFINITY;
-        if (kvalid >= HC) {
+        const bool full_tile = kvalid >= HC;
+        if (!full_tile) {
 #pragma unroll
-          for (int i = 0; i < HC; ++i) mx = fmaxf(mx, sv[i]);
-        } else {
-#pragma unroll
-          for (int i = 0; i < HC; ++i) {
-            sv[i] = (i < kvalid) ? sv[i] : -INFINITY;
-            mx = fmaxf(mx, sv[i]);
-          }
+          for (int i = 0; i < HC; ++i) sv[i] = (i < kvalid) ? sv[i] : -INFINITY;
         }
-        mx *= a.scale_log2;
-        // P_t lands in S buffer t&1 (not the one PV_{t-1} reads), so the softmax runs ahead
-        // of the PV MMAs; only an O rescale needs PV_{t-1} of this half to be complete.
+        float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};   // 4 independent chains
+#pragma unroll
+        for (int i = 0; i < HC; i += 8) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) mq[k] = fmaxf(mq[k], fmaxf(sv[i + 2 * k], sv[i + 2 * k + 1]));
+        }
+        float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3])) * a.scale_log2;
+        // row max over both key halves (both warps then take the same rescale decision)
+        xm[((gt & 1) * 2 + half) * 128 + row] = mx;
+        pair_sync();
+        mx = fmaxf(mx, xm[((gt & 1) * 2 + (half ^ 1)) * 128 + row]);
+        if (quarter == 0) ATTN_TRACE(11 + 2 * half, gt);
+        // lazy rescale: P / O stay relative to m_used until the max grows by > 2^8
         if (mx > m_used + 8.f) {
-          const float m_new = mx;
-          if (t > 0) {     // rescale this half's O row (all HD columns) in TMEM
-            tc::mbar_wait(p_empty + ((gt - 1) & 1) * 2 + half, ((gt - 1) >> 1) & 1);
+          if (t > 0) {     // O row (this half's HD/2 columns) *= 2^(m_used - m_new) once PV_{t-1} landed
+            tc::mbar_wait(pv_done + (gt - 1) % 3, ((gt - 1) / 3) & 1);
             tc::tc_fence_after();
-            const float alpha = ex2(m_used - m_new);
+            const float alpha = ex2(m_used - mx);
             l *= alpha;
 #pragma unroll
-            for (int cc = 0; cc < HD / 16; ++cc) {
+            for (int cc = 0; cc < HO / 16; ++cc) {
               uint32_t r[16];
-              const uint32_t ta = tO2[half] + lane_off + cc * 16;
+              const uint32_t ta = tO + lane_off + half * HO + cc * 16;
               asm volatile(
                   "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
                   "[%16];"
@@ -376,55 +528,45 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
             }
             tc::tmem_st_wait();
           }
-          m_used = m_new;
+          m_used = mx;
         }
-        // P = exp2(s * scale - m_used) -> bf16 pairs written over this half's own S columns
-        // in TMEM (A operand of the PV MMA); a half with no valid key yet writes P = 0
+        // P = exp2(s * scale - m_used) -> bf16 pairs over this half's own S columns (A
+        // operand of the PV MMA); a row with no valid key yet writes P = 0
         const float msub = m_used == -INFINITY ? 0.f : m_used;
-        float rs = 0.f;
+        const uint64_t sc2 = f2pack(a.scale_log2, a.scale_log2), nm2 = f2pack(-msub, -msub);
         uint32_t pk[HC / 2];
-#pragma unroll
-        for (int i = 0; i < HC / 2; ++i) {
-          const float2 pp = ex2x2(fmaf(sv[2 * i], a.scale_log2, -msub), fmaf(sv[2 * i + 1], a.scale_log2, -msub));
-          rs += pp.x + pp.y;
-          __nv_bfloat162 b2 = __floats2bfloat162_rn(pp.x, pp.y);
-          pk[i] = *reinterpret_cast<uint32_t*>(&b2);
-        }
-        tc::tmem_st32(tS[st] + lane_off + half * HC, pk);
+        // full tiles move a share of the exponentials to the FMA pipe (the MUFU alone would
+        // need 8 cycles per warp instruction x 64 per half-row: the MMA time of a tile)
+        const float rs = full_tile ? p_row<HC, true>(sv, pk, sc2, nm2) : p_row<HC, false>(sv, pk, sc2, nm2);
+        tc::tmem_st32(tS(b) + lane_off + half * HC, pk);
         tc::tmem_st_wait();
         l += rs;
         tc::tc_fence_before();
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive(p_full + (gt & 1) * 2 + half);
+        if (lane == 0) tc::mbar_arrive(p_full + b);
+        if (quarter == 0) ATTN_TRACE(5 + 2 * half, gt);
       }
-      // end of segment: wait for this half's last PV; exchange (m, l) with the other half
+      // end of segment: last PV landed -> O / (l_half0 + l_half1), this half's columns
       const int gl = gi + nt - 1;   // last tile of the segment
-      tc::mbar_wait(p_empty + (gl & 1) * 2 + half, (gl >> 1) & 1);
-      xch[half * 256 + row] = m_used;
-      xch[half * 256 + 128 + row] = l;
-      asm volatile("bar.sync 1, 256;" ::: "memory");
-      tc::mbar_wait(p_empty + (gl & 1) * 2 + (half ^ 1), (gl >> 1) & 1);   // other half's O complete too
+      xl[half * 128 + row] = l;
+      tc::mbar_wait(pv_done + gl % 3, (gl / 3) & 1);
       tc::tc_fence_after();
-      const float m0 = xch[row], l0 = xch[128 + row], m1 = xch[256 + row], l1 = xch[384 + row];
-      const float M = fmaxf(m0, m1);
-      const float w0 = m0 == -INFINITY ? 0.f : ex2(m0 - M), w1 = m1 == -INFINITY ? 0.f : ex2(m1 - M);
-      const float lt = l0 * w0 + l1 * w1;
+      pair_sync();
+      const float lt = l + xl[(half ^ 1) * 128 + row];
       const bool full = (s.jb == 0 && s.je == s.J);
       const int slot = (g == t0) ? 0 : 1;
       const int qr = s.q0 + row;
       const float inv = full ? 1.f / lt : 1.f;
-      const float c0w = w0 * inv, c1w = w1 * inv;
       bf16* orow = reinterpret_cast<bf16*>(a.o) + size_t(s.e * a.L + qr) * a.ldo + s.h * HD + half * HO;
-      float* prow = a.part_o + ((size_t(c) * 2 + slot) * kAttnBQ + row) * HD + half * HO;
+      float* prow = a.part_o + ((size_t(c * CL + cr) * 2 + slot) * kAttnBQ + row) * HD + half * HO;
 #pragma unroll
       for (int cc = 0; cc < HO / 32; ++cc) {
-        uint32_t r0[32], r1[32];
-        tc::tmem_ld32(tO2[0] + lane_off + half * HO + cc * 32, r0);
-        tc::tmem_ld32(tO2[1] + lane_off + half * HO + cc * 32, r1);
+        uint32_t r0[32];
+        tc::tmem_ld32(tO + lane_off + half * HO + cc * 32, r0);
         tc::tmem_ld_wait();
         float o[32];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) o[i] = __uint_as_float(r0[i]) * c0w + __uint_as_float(r1[i]) * c1w;
+        for (int i = 0; i < 32; ++i) o[i] = __uint_as_float(r0[i]) * inv;
         if (full) {
           if (qr < a.L) {
             uint32_t pk[16];
@@ -445,12 +587,12 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
         }
       }
       if (!full && half == 0) {
-        float* ml = a.part_ml + ((size_t(c) * 2 + slot) * kAttnBQ + row) * 2;
-        ml[0] = M;
+        float* ml = a.part_ml + ((size_t(c * CL + cr) * 2 + slot) * kAttnBQ + row) * 2;
+        ml[0] = m_used;
         ml[1] = lt;
       }
       tc::tc_fence_before();
-      asm volatile("bar.sync 1, 256;" ::: "memory");   // xch reusable, both halves done with O
+      pair_sync();   // xl reusable
       if (lane == 0) tc::mbar_arrive(o_empty);
       gi += nt;
       g = s.ge;
@@ -458,7 +600,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
     }
   }
   tc::tc_fence_before();
-  __syncthreads();
+  if (CL > 1) tc::cluster_sync();   // no CTA exits while its peer may still multicast into it
+  else __syncthreads();
   if (warp == 0) {
     tc::tc_fence_after();
     tc::tmem_dealloc(tmem, 512);
@@ -468,20 +611,21 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
 // Merge the partial units (split between consecutive CTAs) in CTA order:
 // O = sum_k 2^(m_k - M) O_k / sum_k 2^(m_k - M) l_k.  One CTA per unit; a warp per row,
 // lanes across the head dim (coalesced 512 B row reads).
-template <int HD>
+template <int HD, int CL>
 __global__ void __launch_bounds__(256) attn_combine_kernel(AttnTcArgs a, const TickDesc* __restrict__ td, int G) {
   pdl_wait();
   pdl_trigger();
   constexpr int PL = HD / 32;   // columns per lane
   AttnGeo geo;
-  geo.init(a, td);
-  const int u = blockIdx.x;
-  const int e = u / (a.H * a.QT), w = u % (a.H * a.QT);
+  geo.init(a, td, CL);
+  const int pu = blockIdx.x / CL, cr = blockIdx.x % CL;   // query-tile group unit, member
+  const int e = pu / (a.H * geo.QP), w = pu % (a.H * geo.QP);
   if (e >= a.n_entries || geo.J[e] == 0) return;
   const long long off = geo.off[e] + (long long)w * geo.J[e];
   const int cf = geo.cta_of(off, G), cl = geo.cta_of(off + geo.J[e] - 1, G);
-  if (a.per_unit || cf == cl) return;   // one CTA covered the whole unit and wrote the final output
-  const int h = w / a.QT, q0 = (w % a.QT) * kAttnBQ;
+  if (a.per_unit || cf == cl) return;   // one cluster covered the whole unit and wrote the final output
+  const int h = w / geo.QP, q0 = ((w % geo.QP) * CL + cr) * kAttnBQ;
+  if (q0 >= a.L) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int slot_f = geo.start(cf, G) < off ? 1 : 0;
   for (int row = warp; row < kAttnBQ; row += 8) {
@@ -490,14 +634,14 @@ __global__ void __launch_bounds__(256) attn_combine_kernel(AttnTcArgs a, const T
     float M = -INFINITY;
     for (int cc = cf; cc <= cl; ++cc) {
       const int slot = cc == cf ? slot_f : 0;
-      M = fmaxf(M, a.part_ml[((size_t(cc) * 2 + slot) * kAttnBQ + row) * 2]);
+      M = fmaxf(M, a.part_ml[((size_t(cc * CL + cr) * 2 + slot) * kAttnBQ + row) * 2]);
     }
     float den = 0.f, acc[PL];
 #pragma unroll
     for (int i = 0; i < PL; ++i) acc[i] = 0.f;
     for (int cc = cf; cc <= cl; ++cc) {
       const int slot = cc == cf ? slot_f : 0;
-      const size_t base = (size_t(cc) * 2 + slot) * kAttnBQ + row;
+      const size_t base = (size_t(cc * CL + cr) * 2 + slot) * kAttnBQ + row;
       const float wgt = exp2f(a.part_ml[base * 2] - M);
       den += wgt * a.part_ml[base * 2 + 1];
       const float* po = a.part_o + base * HD + lane * PL;
@@ -534,11 +678,18 @@ inline int attn_pick_per_unit(long long units, long long tiles, int num_sms) {
   return per_unit <= streamk ? 1 : 0;
 }
 
+inline int attn_cluster() {
+  const char* e = getenv("SDV2_ATTN_CL");
+  return e ? (atoi(e) == 2 ? 2 : 1) : 1;   // measured neutral at the 1.3B shapes: off by default
+}
+
 inline bool attn_plan_init(AttnPlan& p, PFN_encodeTiled enc, int num_sms) {
   p.encode = enc;
   p.num_sms = num_sms;
-  cudaFuncSetAttribute(attn_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, AttnSmem<128>::total);
-  cudaFuncSetAttribute(attn_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, AttnSmem<64>::total);
+  cudaFuncSetAttribute(attn_tc_kernel<128, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, AttnSmem<128>::total);
+  cudaFuncSetAttribute(attn_tc_kernel<64, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, AttnSmem<64>::total);
+  cudaFuncSetAttribute(attn_tc_kernel<128, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, AttnSmem<128>::total);
+  cudaFuncSetAttribute(attn_tc_kernel<64, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, AttnSmem<64>::total);
   p.ready = true;
   return true;
 }
@@ -576,30 +727,51 @@ inline bool tc_attention(cudaStream_t s, AttnPlan& p, const void* q, long long q
                          const void* Vbase, long long kv_rows, int d, int hd, long long total_tiles_hint,
                          const AttnTcArgs& a, const TickDesc* td, std::string* err, bool pdl = false) {
   const CUtensorMap* mq = attn_map(p, q, q_rows, d, kAttnBQ, err);
-  const CUtensorMap* mk = attn_map(p, Kbase, kv_rows, d, kAttnBKV, err);
-  const CUtensorMap* mv = attn_map(p, Vbase, kv_rows, d, kAttnBKV, err);
+  const int CL = attn_cluster();
+  const CUtensorMap* mk = attn_map(p, Kbase, kv_rows, d, kAttnBKV / CL, err);
+  const CUtensorMap* mv = attn_map(p, Vbase, kv_rows, d, kAttnBKV / CL, err);
   if (!mq || !mk || !mv) return false;
-  const int units = a.n_entries * a.H * a.QT;
-  const int G = a.per_unit ? units : int(total_tiles_hint < p.num_sms ? total_tiles_hint : p.num_sms);
+  const int QP = (a.QT + CL - 1) / CL;
+  const long long units = (long long)a.n_entries * a.H * QP;                   // query-tile groups
+  const long long tiles = total_tiles_hint * QP / (a.QT > 0 ? a.QT : 1);       // group x key tiles
+  const int slots = p.num_sms / CL;
+  const int G = a.per_unit ? int(units) : int(tiles < slots ? tiles : slots);  // clusters
   cudaLaunchConfig_t cfg{};
   cfg.blockDim = dim3(kAttnThreads);
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = pdl ? 1 : 0;
+  cfg.numAttrs = pdl ? 2 : 1;
   cudaError_t e;
-  cfg.gridDim = dim3(G);
+  cfg.gridDim = dim3(G * CL);
   cfg.dynamicSmemBytes = hd == 128 ? AttnSmem<128>::total : AttnSmem<64>::total;
-  e = hd == 128 ? cudaLaunchKernelEx(&cfg, attn_tc_kernel<128>, *mq, *mk, *mv, a, td)
-                : cudaLaunchKernelEx(&cfg, attn_tc_kernel<64>, *mq, *mk, *mv, a, td);
+  if (CL == 2)
+    e = hd == 128 ? cudaLaunchKernelEx(&cfg, attn_tc_kernel<128, 2>, *mq, *mk, *mv, a, td)
+                  : cudaLaunchKernelEx(&cfg, attn_tc_kernel<64, 2>, *mq, *mk, *mv, a, td);
+  else
+    e = hd == 128 ? cudaLaunchKernelEx(&cfg, attn_tc_kernel<128, 1>, *mq, *mk, *mv, a, td)
+                  : cudaLaunchKernelEx(&cfg, attn_tc_kernel<64, 1>, *mq, *mk, *mv, a, td);
   if (e == cudaSuccess && !a.per_unit) {
-    cfg.gridDim = dim3(units);
+    cfg.gridDim = dim3(unsigned(units * CL));
     cfg.blockDim = dim3(256);
     cfg.dynamicSmemBytes = 0;
-    e = hd == 128 ? cudaLaunchKernelEx(&cfg, attn_combine_kernel<128>, a, td, G)
-                  : cudaLaunchKernelEx(&cfg, attn_combine_kernel<64>, a, td, G);
+    cfg.numAttrs = 0;
+    if (pdl) {
+      cfg.attrs = at + 1;
+      cfg.numAttrs = 1;
+    }
+    if (CL == 2)
+      e = hd == 128 ? cudaLaunchKernelEx(&cfg, attn_combine_kernel<128, 2>, a, td, G)
+                    : cudaLaunchKernelEx(&cfg, attn_combine_kernel<64, 2>, a, td, G);
+    else
+      e = hd == 128 ? cudaLaunchKernelEx(&cfg, attn_combine_kernel<128, 1>, a, td, G)
+                    : cudaLaunchKernelEx(&cfg, attn_combine_kernel<64, 1>, a, td, G);
   }
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {

@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {
+    {   // whole warp walks the loop; one elected lane issues (see tc::elect_one)
       int stage = 0;
       uint32_t phase = 0;
       const uint32_t bytes = uint32_t(kGemmSmemA) + uint32_t(BN) * kGemmBK * 2;
@@ -193,24 +193,31 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
       if (cid < tiles && MC == 1) {
         const int nb0 = cid / num_mg;
         pre = kblocks < kStages ? kblocks : kStages;
-        for (int kb = 0; kb < pre; ++kb) {
-          tc::mbar_expect_tx(full + kb, bytes);
-          load_w(kb, kb, nb0);
+        if (tc::elect_one()) {
+          for (int kb = 0; kb < pre; ++kb) {
+            tc::mbar_expect_tx(full + kb, bytes);
+            load_w(kb, kb, nb0);
+          }
         }
+        __syncwarp();
       }
       pdl_wait();
       for (int t = cid; t < tiles; t += ncl) {
         const int mb = (t % num_mg) * MC + cr, nb = t / num_mg;
         for (int kb = 0; kb < kblocks; ++kb) {
           if (pre > 0) {   // first tile, W already in flight for this stage
-            tc::tma_load_2d(sA + stage * kGemmSmemA, &tmA, full + stage, kb * kGemmBK, mb * kGemmBM);
+            if (tc::elect_one())
+              tc::tma_load_2d(sA + stage * kGemmSmemA, &tmA, full + stage, kb * kGemmBK, mb * kGemmBM);
             --pre;
           } else {
             tc::mbar_wait(empty + stage, phase ^ 1);
-            tc::mbar_expect_tx(full + stage, bytes);
-            tc::tma_load_2d(sA + stage * kGemmSmemA, &tmA, full + stage, kb * kGemmBK, mb * kGemmBM);
-            load_w(stage, kb, nb);
+            if (tc::elect_one()) {
+              tc::mbar_expect_tx(full + stage, bytes);
+              tc::tma_load_2d(sA + stage * kGemmSmemA, &tmA, full + stage, kb * kGemmBK, mb * kGemmBM);
+              load_w(stage, kb, nb);
+            }
           }
+          __syncwarp();
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
@@ -219,7 +226,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {   // whole warp walks the loop; one elected lane issues (see tc::elect_one)
       const uint32_t idesc = tc::idesc_bf16(kGemmBM, BN);
       int stage = 0;
       uint32_t phase = 0;
@@ -234,19 +241,23 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
           tc::tc_fence_after();
           const uint32_t a0 = tc::smem_u32(sA + stage * kGemmSmemA);
           const uint32_t b0 = tc::smem_u32(sB + stage * kSmemB);
+          if (tc::elect_one()) {
 #pragma unroll
-          for (int k = 0; k < kGemmBK / 16; ++k) {
-            tc::mma_bf16(d_tmem, tc::sw128_kmajor_desc(a0 + k * 32), tc::sw128_kmajor_desc(b0 + k * 32), idesc,
-                         (kb | k) != 0);
+            for (int k = 0; k < kGemmBK / 16; ++k) {
+              tc::mma_bf16(d_tmem, tc::sw128_kmajor_desc(a0 + k * 32), tc::sw128_kmajor_desc(b0 + k * 32), idesc,
+                           (kb | k) != 0);
+            }
+            if (MC > 1) tc::mma_commit_mc(empty + stage, mc_mask);
+            else tc::mma_commit(empty + stage);
           }
-          if (MC > 1) tc::mma_commit_mc(empty + stage, mc_mask);
-          else tc::mma_commit(empty + stage);
+          __syncwarp();
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
           }
         }
-        tc::mma_commit(tfull + acc);
+        if (tc::elect_one()) tc::mma_commit(tfull + acc);
+        __syncwarp();
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;

@@ -429,7 +429,11 @@ sdv2_status attention(sdv2_handle* h, const AttnArgs& aa, int Mrows_entries, dou
         const int Lk = aa.cross ? aa.Lk_cross : h->td_host_cur->e[e].nvalid * h->L;
         tiles += (long long)ta.H * ta.QT * ((Lk + kAttnBKV - 1) / kAttnBKV);
       }
-      ta.per_unit = attn_pick_per_unit((long long)Mrows_entries * ta.H * ta.QT, tiles, h->aplan.num_sms);
+      {
+        const int CL = attn_cluster(), QP = (ta.QT + CL - 1) / CL;   // decide on query-tile groups
+        ta.per_unit = attn_pick_per_unit((long long)Mrows_entries * ta.H * QP, tiles * QP / ta.QT,
+                                         h->aplan.num_sms / CL);
+      }
       const void *Kb, *Vb;
       long long kv_rows;
       if (aa.cross) {
@@ -1180,9 +1184,29 @@ extern "C" sdv2_status sdv2_debug_attention(const void* q, const void* K, const 
   ta.kv_lane_rows = 0;
   const long long tiles = (long long)H * ta.QT * ((Lk + kAttnBKV - 1) / kAttnBKV);
   ta.per_unit = getenv("SDV2_ATTN_PER_UNIT") ? atoi(getenv("SDV2_ATTN_PER_UNIT")) : 0;
+  ta.dbg = getenv("SDV2_ATTN_DBG") ? atoi(getenv("SDV2_ATTN_DBG")) : 0;
+  // SDV2_ATTN_TRACE=<file>: per-tile clock64 stamps of CTA 0 (pipeline analysis)
+  const char* trace_path = getenv("SDV2_ATTN_TRACE");
+  static long long* trace = nullptr;
+  if (trace_path) {
+    if (!trace && cudaMalloc(&trace, 256 * 16 * sizeof(long long)) != cudaSuccess) return SDV2_E_CUDA;
+    cudaMemsetAsync(trace, 0, 256 * 16 * sizeof(long long), s);
+    ta.trace = trace;
+  }
   if (!tc_attention(s, ap, q, Lq, K, V, Lk, H * hd, hd, tiles, ta, static_cast<const TickDesc*>(scratch), &err)) {
     fprintf(stderr, "sdv2_debug_attention: %s\n", err.c_str());
     return SDV2_E_CUDA;
+  }
+  if (trace_path) {
+    std::vector<long long> h(256 * 16);
+    cudaStreamSynchronize(s);
+    cudaMemcpy(h.data(), trace, h.size() * sizeof(long long), cudaMemcpyDeviceToHost);
+    if (FILE* f = fopen(trace_path, "w")) {
+      for (int t = 0; t < 256; ++t) {
+        for (int e = 0; e < 16; ++e) fprintf(f, "%lld%c", h[t * 16 + e], e == 15 ? '\n' : ',');
+      }
+      fclose(f);
+    }
   }
   return SDV2_OK;
 }
