@@ -31,47 +31,77 @@ constexpr int kGemmThreads = 384;                        // 4 control warps + 8 
 
 // Stages of the TMA->MMA ring for a tile width: the ring must cover the L2/HBM latency
 // (about 1-2 us) at the MMA rate, so use all of shared memory.
-__host__ __device__ inline int gemm_stages(int BN, bool res_tma) {
+constexpr int kGemmEpiVec = 3 * kGemmMaxBN * 4 + 8 * 2048;   // bias + 2 gate vectors per tile, 8 x 2 KB store staging
+// BNl = W rows held per CTA (BN, or BN / 2 for a CTA pair).
+__host__ __device__ inline int gemm_stages(int BN, bool res_tma, int BNl) {
   const int xs = res_tma ? BN * kGemmBM * 4 : 0;     // staged fp32 residual tile
-  const int st = (kGemmSmem - 1024 - 512 - xs) / (kGemmSmemA + BN * kGemmBK * 2);
+  const int st = (kGemmSmem - 1024 - 512 - kGemmEpiVec - xs) / (kGemmSmemA + BNl * kGemmBK * 2);
   return st > kGemmMaxStages ? kGemmMaxStages : st;
 }
 constexpr int kResMaxBN = 192;   // residual epilogues: keep >= 3 stages next to the x tile
 
+// Pipeline trace (test hook): event `ev` of k-block / tile index `i` of CTA 0 and 1
+// (CTA 1 at +4096): [i * 8 + ev], i < 512.
+#define GEMM_TRACE(ev, i)                                                               \
+  do {                                                                                  \
+    if (ep.trace != nullptr && blockIdx.x < 2 && (i) < 512)                             \
+      ep.trace[blockIdx.x * 4096 + (i) * 8 + (ev)] = clock64();                         \
+  } while (0)
+
+// sbias: the chunk's 32 bias values (shared memory, staged per tile).  bf16 outputs go
+// through a per-warp 2 KB staging buffer (XOR-swizzled 16 B granules, conflict-free)
+// and leave as 8 rows x 64 B per store instruction instead of 32 scattered rows.
+// Every lane of the warp must call it (rows >= M are computed but not stored).
 template <int EPI, typename TOut>
-__device__ __forceinline__ void gemm_epilogue_chunk(const EpiArgs& ep, int r, int c0, int N, const uint32_t (&v)[32]) {
+__device__ __forceinline__ void gemm_epilogue_chunk(const EpiArgs& ep, int r, int M, int c0, int N,
+                                                    const uint32_t (&v)[32], const float* sbias, uint4* stage,
+                                                    int lane, int r_warp0) {
   if (c0 + 32 <= N) {
     float acc[32];
+    const uint32_t sb = tc::smem_u32(sbias);
 #pragma unroll
     for (int i = 0; i < 32; i += 4) {
-      const float4 b = *reinterpret_cast<const float4*>(ep.bias + c0 + i);
+      const float4 b = tc::ld_shared_f4(sb + i * 4);
       acc[i] = __uint_as_float(v[i]) + b.x;
       acc[i + 1] = __uint_as_float(v[i + 1]) + b.y;
       acc[i + 2] = __uint_as_float(v[i + 2]) + b.z;
       acc[i + 3] = __uint_as_float(v[i + 3]) + b.w;
     }
     if (EPI == EPI_STORE || EPI == EPI_GELU) {
-      TOut* o = reinterpret_cast<TOut*>(ep.out) + size_t(r) * ep.ldo + c0;
       if constexpr (sizeof(TOut) == 2) {
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           float a0 = acc[2 * i], a1 = acc[2 * i + 1];
           if (EPI == EPI_GELU) {
-            a0 = gelu_tanh(a0);
-            a1 = gelu_tanh(a1);
+            a0 = gelu_tanh_fast(a0);
+            a1 = gelu_tanh_fast(a1);
           }
           __nv_bfloat162 h2 = __floats2bfloat162_rn(a0, a1);
           pk[i] = *reinterpret_cast<uint32_t*>(&h2);
         }
+        const uint32_t st0 = tc::smem_u32(stage);
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-          reinterpret_cast<uint4*>(o)[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+        for (int j = 0; j < 4; ++j)
+          tc::st_shared_v4(st0 + (lane * 4 + (j ^ ((lane >> 1) & 3))) * 16,
+                           make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]));
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int rr = i * 8 + (lane >> 2), seg = lane & 3;
+          const uint4 w = tc::ld_shared_v4(st0 + (rr * 4 + (seg ^ ((rr >> 1) & 3))) * 16);
+          if (r_warp0 + rr < M)
+            *reinterpret_cast<uint4*>(reinterpret_cast<TOut*>(ep.out) + size_t(r_warp0 + rr) * ep.ldo + c0 + seg * 8) = w;
+        }
+        __syncwarp();
       } else {
+        if (r < M) {
+          TOut* o = reinterpret_cast<TOut*>(ep.out) + size_t(r) * ep.ldo + c0;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) o[i] = from_f<TOut>(EPI == EPI_GELU ? gelu_tanh(acc[i]) : acc[i]);
+          for (int i = 0; i < 32; ++i) o[i] = from_f<TOut>(EPI == EPI_GELU ? gelu_tanh(acc[i]) : acc[i]);
+        }
       }
-    } else {
+    } else if (r < M) {
       // Residual epilogues: issue every load (x row segment, gate vectors through the
       // read-only path) before the first store, so the 8 x 16 B round trips overlap
       // instead of serialising on possible aliasing between x and the gate pointers.
@@ -108,16 +138,18 @@ __device__ __forceinline__ void gemm_epilogue_chunk(const EpiArgs& ep, int r, in
 #pragma unroll
       for (int i = 0; i < 8; ++i) reinterpret_cast<float4*>(x)[i] = xv[i];
     }
-  } else {
+  } else if (r < M) {
     for (int i = 0; i < 32; ++i)
       if (c0 + i < N) epi_store<TOut, EPI>(ep, r, c0 + i, N, __uint_as_float(v[i]));
   }
 }
 
-// MC = CTAs per cluster along M (1 or 2).  With MC = 2 the two CTAs work on
-// consecutive m-blocks of the same n-block: each loads its own A tile and one half of
-// the shared W tile, multicast into both CTAs' shared memory, so every SM pulls
-// 16 KB + BN*64 B per k-block from L2 instead of 16 KB + BN*128 B.
+// MC = CTAs per cluster along M (1 or 2).  MC = 2 is a CTA pair (tcgen05 cta_group::2):
+// the two CTAs hold consecutive m-blocks (A rows) and one half each of the BN W rows;
+// the even CTA issues M = 256 MMAs that read both halves in place and accumulate 128
+// rows into each CTA's TMEM.  Every SM then pulls 16 KB + BN * 64 B per k-block instead
+// of 16 KB + BN * 128 B: the 128 x 256 single-CTA tile needs ~94 B/cycle/SM at the MMA
+// rate, above the ~63-85 B/cycle/SM the L2 delivers (tools/ubench_tma), the pair ~62.
 template <int EPI, typename TOut, int MC>
 __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA,
                                                          const __grid_constant__ CUtensorMap tmB,
@@ -130,8 +162,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
   constexpr bool kResTMA = (EPI == EPI_RES_GATE || EPI == EPI_RES);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int kStages = gemm_stages(BN, kResTMA);
-  const int kSmemB = BN * kGemmBK * 2;      // multiple of 1024 (BN multiple of 32... 8 rows x 128 B)
+  const int BNl = BN / MC;                  // W rows held by this CTA
+  const int kStages = gemm_stages(BN, kResTMA, BNl);
+  const int kSmemB = BNl * kGemmBK * 2;     // multiple of 1024 (BNl multiple of 16... 8 rows x 128 B)
   uint8_t* sA = smem;
   uint8_t* sB = smem + kStages * kGemmSmemA;
   uint8_t* sX = sB + kStages * kSmemB;      // [BN/32][128 rows][32 fp32], 16 KB per box
@@ -141,6 +174,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
   uint64_t* tempty = tfull + 2;
   uint64_t* x_full = tempty + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(x_full + 1);
+  float* sBias = reinterpret_cast<float*>(x_full + 2);   // [BN] bias, then [2][BN] gate sums
+  float* sGate = sBias + kGemmMaxBN;
+  uint4* sStage = reinterpret_cast<uint4*>(sGate + 2 * kGemmMaxBN);   // [8 epilogue warps][128] x 16 B
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int num_m = (M + kGemmBM - 1) / kGemmBM, num_n = (N + BN - 1) / BN;
@@ -156,18 +192,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
     tc::tma_prefetch_desc(&tmA);
     tc::tma_prefetch_desc(&tmB);
     for (int s = 0; s < kStages; ++s) {
-      tc::mbar_init(full + s, 1);
-      tc::mbar_init(empty + s, MC);      // both CTAs' MMAs must release a stage (MC = 2)
+      tc::mbar_init(full + s, 1);        // pair: the even CTA's barrier counts both CTAs' bytes
+      tc::mbar_init(empty + s, 1);       // pair: released by the even CTA's multicast commit
     }
     for (int s = 0; s < 2; ++s) {
       tc::mbar_init(tfull + s, 1);
-      tc::mbar_init(tempty + s, 8);
+      tc::mbar_init(tempty + s, 8 * MC); // pair: both CTAs' epilogue warps free the accumulator
     }
     tc::mbar_init(x_full, 1);
     if (kResTMA) tc::tma_prefetch_desc(&tmX);
     tc::fence_barrier_init();
   }
-  if (warp == 2) tc::tmem_alloc(tmem_slot, 512);
+  if (warp == 2) {
+    if (MC > 1) tc::tmem_alloc_cg2(tmem_slot, 512);
+    else tc::tmem_alloc(tmem_slot, 512);
+  }
   tc::tc_fence_before();
   if (MC > 1) tc::cluster_sync();   // peer barriers initialised before any multicast
   else __syncthreads();
@@ -178,12 +217,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
     {   // whole warp walks the loop; one elected lane issues (see tc::elect_one)
       int stage = 0;
       uint32_t phase = 0;
-      const uint32_t bytes = uint32_t(kGemmSmemA) + uint32_t(BN) * kGemmBK * 2;
-      const int bh = BN / MC;   // W rows this CTA loads (and multicasts)
+      // bytes landing on the stage's full barrier (pair: both CTAs' A and W halves)
+      const uint32_t bytes = MC * (uint32_t(kGemmSmemA) + uint32_t(BNl) * kGemmBK * 2);
+      auto load_a = [&](int st, int kb, int mb) {
+        if (MC > 1)
+          tc::tma_load_2d_cg2(sA + st * kGemmSmemA, &tmA, tc::mapa_shared(full + st, 0), kb * kGemmBK, mb * kGemmBM);
+        else
+          tc::tma_load_2d(sA + st * kGemmSmemA, &tmA, full + st, kb * kGemmBK, mb * kGemmBM);
+      };
       auto load_w = [&](int st, int kb, int nb) {
         if (MC > 1)
-          tc::tma_load_2d_mc(sB + st * kSmemB + cr * bh * 128, &tmB, full + st, kb * kGemmBK, nb * BN + cr * bh,
-                             mc_mask);
+          tc::tma_load_2d_cg2(sB + st * kSmemB, &tmB, tc::mapa_shared(full + st, 0), kb * kGemmBK,
+                              nb * BN + cr * BNl);
         else
           tc::tma_load_2d(sB + st * kSmemB, &tmB, full + st, kb * kGemmBK, nb * BN);
       };
@@ -202,18 +247,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
         __syncwarp();
       }
       pdl_wait();
+      int kg = 0;   // k-blocks loaded by this CTA (trace index)
       for (int t = cid; t < tiles; t += ncl) {
         const int mb = (t % num_mg) * MC + cr, nb = t / num_mg;
-        for (int kb = 0; kb < kblocks; ++kb) {
+        for (int kb = 0; kb < kblocks; ++kb, ++kg) {
           if (pre > 0) {   // first tile, W already in flight for this stage
-            if (tc::elect_one())
-              tc::tma_load_2d(sA + stage * kGemmSmemA, &tmA, full + stage, kb * kGemmBK, mb * kGemmBM);
+            if (tc::elect_one()) load_a(stage, kb, mb);
             --pre;
           } else {
             tc::mbar_wait(empty + stage, phase ^ 1);
+            if (lane == 0) GEMM_TRACE(0, kg);
             if (tc::elect_one()) {
-              tc::mbar_expect_tx(full + stage, bytes);
-              tc::tma_load_2d(sA + stage * kGemmSmemA, &tmA, full + stage, kb * kGemmBK, mb * kGemmBM);
+              if (cr == 0) tc::mbar_expect_tx(full + stage, bytes);
+              load_a(stage, kb, mb);
               load_w(stage, kb, nb);
             }
           }
@@ -226,28 +272,35 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
       }
     }
   } else if (warp == 1) {
-    {   // whole warp walks the loop; one elected lane issues (see tc::elect_one)
-      const uint32_t idesc = tc::idesc_bf16(kGemmBM, BN);
+    if (cr == 0) {   // whole warp walks the loop; one elected lane issues (see tc::elect_one)
+      const uint32_t idesc = tc::idesc_bf16(kGemmBM * MC, BN);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = cid; t < tiles; t += ncl) {
+      int kg = 0, nt = 0;
+      for (int t = cid; t < tiles; t += ncl, ++nt) {
         tc::mbar_wait(tempty + acc, acc_phase ^ 1);
+        if (lane == 0) GEMM_TRACE(2, nt);
         tc::tc_fence_after();
         const uint32_t d_tmem = tmem + uint32_t(acc * BN);
-        for (int kb = 0; kb < kblocks; ++kb) {
+        for (int kb = 0; kb < kblocks; ++kb, ++kg) {
           tc::mbar_wait(full + stage, phase);
+          if (lane == 0) GEMM_TRACE(1, kg);
           tc::tc_fence_after();
           const uint32_t a0 = tc::smem_u32(sA + stage * kGemmSmemA);
           const uint32_t b0 = tc::smem_u32(sB + stage * kSmemB);
           if (tc::elect_one()) {
 #pragma unroll
             for (int k = 0; k < kGemmBK / 16; ++k) {
-              tc::mma_bf16(d_tmem, tc::sw128_kmajor_desc(a0 + k * 32), tc::sw128_kmajor_desc(b0 + k * 32), idesc,
-                           (kb | k) != 0);
+              if (MC > 1)
+                tc::mma_bf16_cg2(d_tmem, tc::sw128_kmajor_desc(a0 + k * 32), tc::sw128_kmajor_desc(b0 + k * 32), idesc,
+                                 (kb | k) != 0);
+              else
+                tc::mma_bf16(d_tmem, tc::sw128_kmajor_desc(a0 + k * 32), tc::sw128_kmajor_desc(b0 + k * 32), idesc,
+                             (kb | k) != 0);
             }
-            if (MC > 1) tc::mma_commit_mc(empty + stage, mc_mask);
+            if (MC > 1) tc::mma_commit_cg2_mc(empty + stage, mc_mask);
             else tc::mma_commit(empty + stage);
           }
           __syncwarp();
@@ -256,7 +309,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
             phase ^= 1;
           }
         }
-        if (tc::elect_one()) tc::mma_commit(tfull + acc);
+        if (tc::elect_one()) {
+          if (MC > 1) tc::mma_commit_cg2_mc(tfull + acc, mc_mask);
+          else tc::mma_commit(tfull + acc);
+        }
+        if (lane == 0) GEMM_TRACE(3, nt);
         __syncwarp();
         if (++acc == 2) {
           acc = 0;
@@ -280,50 +337,96 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
         for (int c = 0; c < BN; c += 32)
           tc::tma_load_2d(sX + (c / 32) * (kGemmBM * 128), &tmX, x_full, nb * BN + c, mb * kGemmBM);
       }
+      // stage the tile's bias (and gate = mod + e0 rows of the tile's entries) in shared
+      // memory while the MMAs run: the per-chunk loop then only waits on TMEM
+      const int row0 = mb * kGemmBM;
+      const int e_lo = (row0 < M ? row0 : M - 1) / ep.L;
+      const int e_hi = ((row0 + kGemmBM - 1) < M ? row0 + kGemmBM - 1 : M - 1) / ep.L;
+      const bool gate_smem = EPI == EPI_RES_GATE && e_hi <= e_lo + 1;
+      asm volatile("bar.sync 3, 256;" ::: "memory");   // previous tile's readers done
+      for (int i = threadIdx.x - 128; i < BN; i += 256) {
+        const int col = nb * BN + i;
+        const bool ok = col < N;
+        sBias[i] = ok ? ep.bias[col] : 0.f;
+        if (EPI == EPI_RES_GATE && gate_smem) {
+          const float gm = ok ? ep.mod[ep.gate_row * N + col] : 0.f;
+          sGate[i] = ok ? gm + ep.e0[size_t(e_lo) * 6 * N + ep.gate_row * N + col] : 0.f;
+          if (e_hi > e_lo) sGate[kGemmMaxBN + i] = ok ? gm + ep.e0[size_t(e_hi) * 6 * N + ep.gate_row * N + col] : 0.f;
+        }
+      }
+      asm volatile("bar.sync 3, 256;" ::: "memory");
       tc::mbar_wait(tfull + acc, acc_phase);
+      if (warp == 4 && lane == 0) GEMM_TRACE(4, nt);
       tc::tc_fence_after();
       const int r = mb * kGemmBM + row;
+      const float* gsm = sGate + ((r < M ? r : M - 1) / ep.L > e_lo ? kGemmMaxBN : 0);
       if (kResTMA) tc::mbar_wait(x_full, nt & 1);
-      for (int c = wg * 32; c < BN; c += 64) {
-        uint32_t v[32];
-        tc::tmem_ld32(tmem + (uint32_t(q * 32) << 16) + uint32_t(acc * BN + c), v);
-        tc::tmem_ld_wait();
+      const uint32_t tbase = tmem + (uint32_t(q * 32) << 16) + uint32_t(acc * BN);
+      auto chunk = [&](const uint32_t(&v)[32], int c) {
         const int c0 = nb * BN + c;
         if (kResTMA) {
           if (c0 + 32 <= N) {
-            uint8_t* xrow = sX + (c / 32) * (kGemmBM * 128) + (row >> 3) * 1024 + (row & 7) * 128;
-            const float4* bias4 = reinterpret_cast<const float4*>(ep.bias + c0);
+            const uint32_t xrow = tc::smem_u32(sX + (c / 32) * (kGemmBM * 128) + (row >> 3) * 1024 + (row & 7) * 128);
+            const uint32_t bias4 = tc::smem_u32(sBias + c), gs = tc::smem_u32(gsm + c);
             const float4* gm = reinterpret_cast<const float4*>(ep.mod + ep.gate_row * N + c0);
             const float4* ge =
                 reinterpret_cast<const float4*>(ep.e0 + size_t(r < M ? r / ep.L : 0) * 6 * N + ep.gate_row * N + c0);
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
-              float4* px = reinterpret_cast<float4*>(xrow + ((u ^ (row & 7)) << 4));
-              float4 xv = *px;
-              const float4 bb = __ldg(bias4 + u);
+              const uint32_t px = xrow + ((u ^ (row & 7)) << 4);
+              float4 xv = tc::ld_shared_f4(px);
+              const float4 bb = tc::ld_shared_f4(bias4 + u * 16);
               float a0 = __uint_as_float(v[4 * u]) + bb.x, a1 = __uint_as_float(v[4 * u + 1]) + bb.y;
               float a2 = __uint_as_float(v[4 * u + 2]) + bb.z, a3 = __uint_as_float(v[4 * u + 3]) + bb.w;
               if (EPI == EPI_RES_GATE) {
-                const float4 ga = __ldg(gm + u), gb = __ldg(ge + u);
-                a0 *= ga.x + gb.x;
-                a1 *= ga.y + gb.y;
-                a2 *= ga.z + gb.z;
-                a3 *= ga.w + gb.w;
+                float4 g;
+                if (gate_smem) {
+                  g = tc::ld_shared_f4(gs + u * 16);
+                } else {
+                  const float4 ga = __ldg(gm + u), gb = __ldg(ge + u);
+                  g = make_float4(ga.x + gb.x, ga.y + gb.y, ga.z + gb.z, ga.w + gb.w);
+                }
+                a0 *= g.x;
+                a1 *= g.y;
+                a2 *= g.z;
+                a3 *= g.w;
               }
               xv.x += a0;
               xv.y += a1;
               xv.z += a2;
               xv.w += a3;
-              *px = xv;
+              tc::st_shared_v4(px, make_uint4(__float_as_uint(xv.x), __float_as_uint(xv.y), __float_as_uint(xv.z),
+                                              __float_as_uint(xv.w)));
             }
           }
-        } else if (r < M && c0 < N) {
-          gemm_epilogue_chunk<EPI, TOut>(ep, r, c0, N, v);
+        } else if (c0 < N) {
+          gemm_epilogue_chunk<EPI, TOut>(ep, r, M, c0, N, v, sBias + c, sStage + (warp - 4) * 128, lane,
+                                         mb * kGemmBM + q * 32);
         }
+      };
+      // two TMEM chunks in flight: the next 32 columns load while this chunk is processed
+      uint32_t va[32], vb[32];
+      int c = wg * 32;
+      if (c < BN) tc::tmem_ld32(tbase + c, va);
+      while (c < BN) {
+        tc::tmem_ld_wait_dep(va);
+        if (warp == 4 && lane == 0 && c == 0) GEMM_TRACE(6, nt);
+        if (c + 64 < BN) tc::tmem_ld32(tbase + c + 64, vb);
+        chunk(va, c);
+        if (warp == 4 && lane == 0 && c == 0) GEMM_TRACE(7, nt);
+        c += 64;
+        if (c >= BN) break;
+        tc::tmem_ld_wait_dep(vb);
+        if (c + 64 < BN) tc::tmem_ld32(tbase + c + 64, va);
+        chunk(vb, c);
+        c += 64;
       }
       tc::tc_fence_before();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(tempty + acc);
+      if (lane == 0) {
+        if (MC > 1) tc::mbar_arrive_cluster(tc::mapa_shared(tempty + acc, 0));
+        else tc::mbar_arrive(tempty + acc);
+      }
       if (kResTMA) {
         tc::fence_proxy_async_smem();   // generic-proxy smem writes -> visible to the TMA store
         asm volatile("bar.sync 2, 256;" ::: "memory");
@@ -333,6 +436,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
           tc::tma_store_commit_wait_read();   // smem reusable for the next tile's load
         }
       }
+      if (warp == 4 && lane == 0) GEMM_TRACE(5, nt);
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
@@ -345,7 +449,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
   else __syncthreads();
   if (warp == 2) {
     tc::tc_fence_after();
-    tc::tmem_dealloc(tmem, 512);
+    if (MC > 1) tc::tmem_dealloc_cg2(tmem, 512);
+    else tc::tmem_dealloc(tmem, 512);
   }
 }
 

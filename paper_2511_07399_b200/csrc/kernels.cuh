@@ -160,10 +160,17 @@ struct EpiArgs {
   const float* e0;      // [n, 6, d] (RES_GATE)
   int gate_row;         // 2 (g1) or 5 (g2)
   int L;                // rows per entry
+  long long* trace;     // test hook only (tc GEMM): clock64 stamps of CTA 0 / 1, nullptr = off
 };
 
 __device__ __forceinline__ float gelu_tanh(float z) {
   return 0.5f * z * (1.f + tanhf(0.7978845608028654f * (z + 0.044715f * z * z * z)));
+}
+// bf16-output variant: tanh.approx (MUFU, rel. error ~2^-11, below the bf16 rounding)
+__device__ __forceinline__ float gelu_tanh_fast(float z) {
+  float t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.7978845608028654f * (z + 0.044715f * z * z * z)));
+  return 0.5f * z * (1.f + t);
 }
 
 template <typename TOut, int EPI>

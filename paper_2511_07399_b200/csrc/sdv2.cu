@@ -1136,9 +1136,29 @@ extern "C" sdv2_status sdv2_debug_gemm(const void* A, const void* W, const float
   ep.e0 = e0;
   ep.gate_row = gate_row;
   ep.L = L > 0 ? L : 1;
+  // SDV2_GEMM_TRACE=<file>: clock64 stamps of CTAs 0 and 1 (pipeline analysis)
+  const char* trace_path = getenv("SDV2_GEMM_TRACE");
+  static long long* trace = nullptr;
+  const size_t tn = 2 * 4096;
+  if (trace_path) {
+    if (!trace && cudaMalloc(&trace, tn * sizeof(long long)) != cudaSuccess) return SDV2_E_CUDA;
+    cudaMemsetAsync(trace, 0, tn * sizeof(long long), static_cast<cudaStream_t>(stream));
+    ep.trace = trace;
+  }
   if (!tc_gemm(static_cast<cudaStream_t>(stream), plan, A, W, M, N, K, epi, ep, &err)) {
     fprintf(stderr, "sdv2_debug_gemm: %s\n", err.c_str());
     return SDV2_E_CUDA;
+  }
+  if (trace_path) {
+    std::vector<long long> h(tn);
+    cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
+    cudaMemcpy(h.data(), trace, tn * sizeof(long long), cudaMemcpyDeviceToHost);
+    if (FILE* f = fopen(trace_path, "w")) {
+      for (size_t i = 0; i < tn / 8; ++i) {
+        for (int e = 0; e < 8; ++e) fprintf(f, "%lld%c", h[i * 8 + e], e == 7 ? '\n' : ',');
+      }
+      fclose(f);
+    }
   }
   return SDV2_OK;
 }

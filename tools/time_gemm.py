@@ -14,13 +14,19 @@ epis = [int(x) for x in os.environ.get("EPIS", "0,2").split(",")]
 
 
 def t_us(fn, n=50):
-    for _ in range(5):
+    """Device time per call: n calls captured in a CUDA graph, replayed (no host launch cost)."""
+    for _ in range(3):
         fn()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(n):
+            fn()
+    g.replay()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
-    for _ in range(n):
-        fn()
+    g.replay()
     b.record()
     torch.cuda.synchronize()
     return a.elapsed_time(b) / n * 1e3
@@ -38,7 +44,8 @@ for (M, N, K) in shapes:
     for epi in epis:
         out = outb if epi < 2 else outf
         us = t_us(lambda: L_.sdv2_debug_gemm(A.data_ptr(), W.data_ptr(), b.data_ptr(), out.data_ptr(), M, N, K, epi,
-                                              mod.data_ptr(), e0.data_ptr(), 2, 1560, s))
+                                              mod.data_ptr(), e0.data_ptr(), 2, 1560,
+                                              torch.cuda.current_stream().cuda_stream))
         line += f" | epi{epi} {us:7.1f} us {2*M*N*K/us/1e6:6.0f} TF"
     us = t_us(lambda: torch.matmul(A, W.T, out=outb))
     line += f" | cuBLAS {us:7.1f} us {2*M*N*K/us/1e6:6.0f} TF"
