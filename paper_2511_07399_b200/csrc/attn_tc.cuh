@@ -29,14 +29,15 @@ namespace sdv2 {
 
 constexpr int kAttnBQ = 128, kAttnBKV = 128;
 
-template <int HD>
+template <int HD, int CL = 1>
 struct AttnSmem {
   static constexpr int Q = kAttnBQ * HD * 2;          // 32 KB (hd 128)
-  static constexpr int KV = kAttnBKV * HD * 2;        // one K or V tile
+  static constexpr int KV = kAttnBKV * HD * 2 / CL;   // one K or V tile (CTA pair: this CTA's half)
   static constexpr int P = kAttnBQ * kAttnBKV * 2;    // 32 KB
   // K / V ring stages.  V is consumed a softmax later than K and its loads see ~2800
   // cycles of latency under load (tools/attn_trace.py): the deeper ring goes to V.
-  static constexpr int KS = 2, VS = 3;
+  // A CTA pair holds half of every K / V tile per CTA: twice the stages in the same space.
+  static constexpr int KS = CL == 2 ? 4 : 2, VS = CL == 2 ? 4 : 3;
   static constexpr int total = Q + (KS + VS) * KV + 1024 + 256 + 768 * 4 + 64;
 };
 
@@ -176,16 +177,20 @@ __device__ __forceinline__ float p_row(const float* sv, uint32_t* pk, uint64_t s
   return s01.x + s01.y;
 }
 
-// CL = CTAs per cluster along the query tiles of one head (1 or 2).  With CL = 2 the
-// pair walks the same key tiles; each CTA loads half of every K / V tile and multicasts
-// it to both, halving the L2 -> SM traffic (every query tile of a head otherwise
-// re-reads the whole lane).
+// CL = CTAs per cluster along the query tiles of one head (1 or 2).  CL = 2 is a CTA
+// pair (tcgen05 cta_group::2, head dim 128): the two CTAs take adjacent query tiles of
+// one head and walk the same key tiles; each loads half of every K tile (64 keys) and
+// half of every V tile (64 head-dim columns), and the even CTA issues M = 256 MMAs that
+// read both halves in place.  Per SM the K/V stream halves (32 KB per 128 x 128 tile
+// instead of 64 KB), so the loads stay ahead of the tensor pipe (tools/attn_trace.py
+// showed single-CTA K/V loads queueing ~2.8-4.6k cycles).
 template <int HD, int CL>
 __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ,
                                                          const __grid_constant__ CUtensorMap tmK,
                                                          const __grid_constant__ CUtensorMap tmV, AttnTcArgs a,
                                                          const TickDesc* __restrict__ td) {
-  using SM = AttnSmem<HD>;
+  static_assert(CL == 1 || HD == 128, "CTA-pair attention needs head dim 128");
+  using SM = AttnSmem<HD, CL>;
   constexpr int NCH = HD / 64;              // 64-column chunks of the head dim
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -238,25 +243,28 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
     tc::tma_prefetch_desc(&tmV);
     tc::mbar_init(q_full, 1);
     tc::mbar_init(q_empty, 1);
-    tc::mbar_init(o_empty, 8);
+    tc::mbar_init(o_empty, 8 * CL);      // pair: both CTAs' softmax warps (on the even CTA)
     for (int s = 0; s < KS; ++s) {
       tc::mbar_init(k_full + s, 1);
-      tc::mbar_init(k_empty + s, CL);   // both CTAs' MMAs release a multicast stage
+      tc::mbar_init(k_empty + s, 1);
     }
     for (int s = 0; s < VS; ++s) {
       tc::mbar_init(v_full + s, 1);
-      tc::mbar_init(v_empty + s, CL);
+      tc::mbar_init(v_empty + s, 1);
     }
     for (int i = 0; i < 3; ++i) {
       tc::mbar_init(s_full + i, 1);
-      tc::mbar_init(p_full + i, 8);
+      tc::mbar_init(p_full + i, 8 * CL);
       tc::mbar_init(pv_done + i, 1);
     }
     tc::fence_barrier_init();
   }
-  if (warp == 0) tc::tmem_alloc(tmem_slot, 512);
+  if (warp == 0) {
+    if (CL > 1) tc::tmem_alloc_cg2(tmem_slot, 512);
+    else tc::tmem_alloc(tmem_slot, 512);
+  }
   tc::tc_fence_before();
-  if (CL > 1) tc::cluster_sync();   // peer barriers initialised before any multicast
+  if (CL > 1) tc::cluster_sync();   // peer barriers initialised before any remote arrive
   else __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
@@ -296,9 +304,16 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
         const int kv_row = a.kv_row0 + (a.cross ? (td->e[s.e].pver & 1) : s.e) * a.kv_lane_rows;
         if (sg > 0) tc::mbar_wait(q_empty, (sg - 1) & 1);
         if (tc::elect_one()) {
-          tc::mbar_expect_tx(q_full, SM::Q);
-          for (int ch = 0; ch < NCH; ++ch)
-            tc::tma_load_2d(sQ + ch * (kAttnBQ * 128), &tmQ, q_full, col + ch * 64, s.e * a.L + s.q0);
+          if (CL > 1) {   // both CTAs' Q land on the even CTA's barrier
+            if (cr == 0) tc::mbar_expect_tx(q_full, 2 * SM::Q);
+            for (int ch = 0; ch < NCH; ++ch)
+              tc::tma_load_2d_cg2(sQ + ch * (kAttnBQ * 128), &tmQ, tc::mapa_shared(q_full, 0), col + ch * 64,
+                                  s.e * a.L + s.q0);
+          } else {
+            tc::mbar_expect_tx(q_full, SM::Q);
+            for (int ch = 0; ch < NCH; ++ch)
+              tc::tma_load_2d(sQ + ch * (kAttnBQ * 128), &tmQ, q_full, col + ch * 64, s.e * a.L + s.q0);
+          }
         }
         __syncwarp();
         for (int j = s.jb; j < s.je; ++j, ++gi) {
@@ -308,17 +323,16 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
           if (tc::elect_one()) {
             if (a.dbg & 4) {
               tc::mbar_arrive(k_full + st);
+            } else if (CL > 1) {   // this CTA's 64 keys x 128 dims, counted on the even CTA
+              if (cr == 0) tc::mbar_expect_tx(k_full + st, 2 * SM::KV);
+              for (int ch = 0; ch < NCH; ++ch)
+                tc::tma_load_2d_cg2(sK + st * SM::KV + ch * (kAttnBKV / 2 * 128), &tmK, tc::mapa_shared(k_full + st, 0),
+                                    col + ch * 64, kv_row + j * kAttnBKV + cr * (kAttnBKV / 2));
             } else {
               tc::mbar_expect_tx(k_full + st, SM::KV);
-              for (int ch = 0; ch < NCH; ++ch) {
-                if (CL > 1)
-                  tc::tma_load_2d_mc(sK + st * SM::KV + ch * (kAttnBKV * 128) + cr * (kAttnBKV / CL) * 128, &tmK,
-                                     k_full + st, col + ch * 64, kv_row + j * kAttnBKV + cr * (kAttnBKV / CL),
-                                     mc_mask);
-                else
-                  tc::tma_load_2d(sK + st * SM::KV + ch * (kAttnBKV * 128), &tmK, k_full + st, col + ch * 64,
-                                  kv_row + j * kAttnBKV);
-              }
+              for (int ch = 0; ch < NCH; ++ch)
+                tc::tma_load_2d(sK + st * SM::KV + ch * (kAttnBKV * 128), &tmK, k_full + st, col + ch * 64,
+                                kv_row + j * kAttnBKV);
             }
           }
           __syncwarp();
@@ -345,17 +359,15 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
           if (tc::elect_one()) {
             if (a.dbg & 4) {
               tc::mbar_arrive(v_full + st);
+            } else if (CL > 1) {   // 128 keys x this CTA's 64 head-dim columns
+              if (cr == 0) tc::mbar_expect_tx(v_full + st, 2 * SM::KV);
+              tc::tma_load_2d_cg2(sV + st * SM::KV, &tmV, tc::mapa_shared(v_full + st, 0), col + cr * 64,
+                                  kv_row + j * kAttnBKV);
             } else {
               tc::mbar_expect_tx(v_full + st, SM::KV);
-              for (int ch = 0; ch < NCH; ++ch) {
-                if (CL > 1)
-                  tc::tma_load_2d_mc(sV + st * SM::KV + ch * (kAttnBKV * 128) + cr * (kAttnBKV / CL) * 128, &tmV,
-                                     v_full + st, col + ch * 64, kv_row + j * kAttnBKV + cr * (kAttnBKV / CL),
-                                     mc_mask);
-                else
-                  tc::tma_load_2d(sV + st * SM::KV + ch * (kAttnBKV * 128), &tmV, v_full + st, col + ch * 64,
-                                  kv_row + j * kAttnBKV);
-              }
+              for (int ch = 0; ch < NCH; ++ch)
+                tc::tma_load_2d(sV + st * SM::KV + ch * (kAttnBKV * 128), &tmV, v_full + st, col + ch * 64,
+                                kv_row + j * kAttnBKV);
             }
           }
           __syncwarp();
@@ -365,10 +377,14 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    {   // whole warp walks the loop; one elected lane issues (see tc::elect_one)
-      const uint32_t idS = tc::idesc_bf16(kAttnBQ, kAttnBKV);
-      const uint32_t idO = tc::idesc_bf16(kAttnBQ, HD, true);
+    if (cr == 0) {   // whole warp walks the loop; one elected lane issues (see tc::elect_one)
+      const uint32_t idS = tc::idesc_bf16(kAttnBQ * CL, kAttnBKV);
+      const uint32_t idO = tc::idesc_bf16(kAttnBQ * CL, HD, true);
       const uint32_t qa = tc::smem_u32(sQ);
+      auto commit = [&](uint64_t* bar) {   // pair: arrive on the barrier in both CTAs
+        if (CL > 1) tc::mma_commit_cg2_mc(bar, mc_mask);
+        else tc::mma_commit(bar);
+      };
       auto issue_S = [&](int gg) {     // gg = local tile counter
         const int b = gg % 3;          // S / P TMEM slot: last read by PV_{gg-3}, issued earlier
         const int ks = gg % KS;        // K smem stage
@@ -380,13 +396,16 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
 #pragma unroll
           for (int k = 0; k < HD / 16; ++k) {
             const uint32_t off = (k >> 2) * (kAttnBQ * 128) + (k & 3) * 32;
-            const uint32_t koff = (k >> 2) * (kAttnBKV * 128) + (k & 3) * 32;
-            if (!(a.dbg & 18))
-              tc::mma_bf16(tS(b), tc::sw128_kmajor_desc(qa + off), tc::sw128_kmajor_desc(ka + koff), idS, k > 0);
+            const uint32_t koff = (k >> 2) * (kAttnBKV / CL * 128) + (k & 3) * 32;
+            if (!(a.dbg & 18)) {
+              if (CL > 1)
+                tc::mma_bf16_cg2(tS(b), tc::sw128_kmajor_desc(qa + off), tc::sw128_kmajor_desc(ka + koff), idS, k > 0);
+              else
+                tc::mma_bf16(tS(b), tc::sw128_kmajor_desc(qa + off), tc::sw128_kmajor_desc(ka + koff), idS, k > 0);
+            }
           }
-          if (CL > 1) tc::mma_commit_mc(k_empty + ks, mc_mask);
-          else tc::mma_commit(k_empty + ks);
-          tc::mma_commit(s_full + b);
+          commit(k_empty + ks);
+          commit(s_full + b);
         }
         __syncwarp();
       };
@@ -397,7 +416,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
         const int nt = s.je - s.jb;
         tc::mbar_wait(q_full, sg & 1);
         auto release_q = [&]() {   // last S of the segment issued: Q smem reusable once it lands
-          if (tc::elect_one()) tc::mma_commit(q_empty);
+          if (tc::elect_one()) commit(q_empty);
           __syncwarp();
         };
         issue_S(gi);
@@ -420,13 +439,17 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
 #pragma unroll
             for (int k = 0; k < 8; ++k) {   // O += P V; A = P from TMEM (bf16 pairs, 8 columns per K=16):
                                             // keys 64h..64h+63 sit in slot columns [64h, 64h+32)
-              if (!(a.dbg & 10))
-                tc::mma_bf16_ts(tO, tS(gt % 3) + (k >> 2) * 64 + (k & 3) * 8,
-                                tc::sw128_mnmajor_desc(va + k * 2048, kAttnBKV * 128), idO, (t | k) != 0);
+              if (!(a.dbg & 10)) {
+                if (CL > 1)   // B = this CTA's 64 head-dim columns of V (one 64-wide block)
+                  tc::mma_bf16_ts_cg2(tO, tS(gt % 3) + (k >> 2) * 64 + (k & 3) * 8,
+                                      tc::sw128_mnmajor_desc(va + k * 2048, kAttnBKV * 128), idO, (t | k) != 0);
+                else
+                  tc::mma_bf16_ts(tO, tS(gt % 3) + (k >> 2) * 64 + (k & 3) * 8,
+                                  tc::sw128_mnmajor_desc(va + k * 2048, kAttnBKV * 128), idO, (t | k) != 0);
+              }
             }
-            if (CL > 1) tc::mma_commit_mc(v_empty + (gt % VS), mc_mask);
-            else tc::mma_commit(v_empty + (gt % VS));
-            tc::mma_commit(pv_done + gt % 3);
+            commit(v_empty + (gt % VS));
+            commit(pv_done + gt % 3);
           }
           __syncwarp();
         }
@@ -446,6 +469,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
     const int row = quarter * 32 + lane;
     const uint32_t lane_off = uint32_t(quarter * 32) << 16;
     auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(2 + quarter) : "memory"); };
+    auto arrive_lead = [&](uint64_t* bar) {   // barriers the MMA issuer waits on live in the even CTA
+      if (CL > 1) tc::mbar_arrive_cluster(tc::mapa_shared(bar, 0));
+      else tc::mbar_arrive(bar);
+    };
     long long g = t0;
     int gi = 0, sg = 0;
     while (g < t1) {
@@ -470,7 +497,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
           m_used = 0.f;
           tc::tc_fence_before();
           __syncwarp();
-          if (lane == 0) tc::mbar_arrive(p_full + b);
+          if (lane == 0) arrive_lead(p_full + b);
           if (quarter == 0) ATTN_TRACE(5 + 2 * half, gt);
           continue;
         }
@@ -543,7 +570,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
         l += rs;
         tc::tc_fence_before();
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive(p_full + b);
+        if (lane == 0) arrive_lead(p_full + b);
         if (quarter == 0) ATTN_TRACE(5 + 2 * half, gt);
       }
       // end of segment: last PV landed -> O / (l_half0 + l_half1), this half's columns
@@ -593,7 +620,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
       }
       tc::tc_fence_before();
       pair_sync();   // xl reusable
-      if (lane == 0) tc::mbar_arrive(o_empty);
+      if (lane == 0) arrive_lead(o_empty);
       gi += nt;
       g = s.ge;
       ++sg;
@@ -604,7 +631,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
   else __syncthreads();
   if (warp == 0) {
     tc::tc_fence_after();
-    tc::tmem_dealloc(tmem, 512);
+    if (CL > 1) tc::tmem_dealloc_cg2(tmem, 512);
+    else tc::tmem_dealloc(tmem, 512);
   }
 }
 
@@ -688,8 +716,7 @@ inline bool attn_plan_init(AttnPlan& p, PFN_encodeTiled enc, int num_sms) {
   p.num_sms = num_sms;
   cudaFuncSetAttribute(attn_tc_kernel<128, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, AttnSmem<128>::total);
   cudaFuncSetAttribute(attn_tc_kernel<64, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, AttnSmem<64>::total);
-  cudaFuncSetAttribute(attn_tc_kernel<128, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, AttnSmem<128>::total);
-  cudaFuncSetAttribute(attn_tc_kernel<64, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, AttnSmem<64>::total);
+  cudaFuncSetAttribute(attn_tc_kernel<128, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, AttnSmem<128, 2>::total);
   p.ready = true;
   return true;
 }
@@ -727,9 +754,10 @@ inline bool tc_attention(cudaStream_t s, AttnPlan& p, const void* q, long long q
                          const void* Vbase, long long kv_rows, int d, int hd, long long total_tiles_hint,
                          const AttnTcArgs& a, const TickDesc* td, std::string* err, bool pdl = false) {
   const CUtensorMap* mq = attn_map(p, q, q_rows, d, kAttnBQ, err);
-  const int CL = attn_cluster();
+  const int CL = hd == 128 ? attn_cluster() : 1;
+  // pair: K boxes of 64 keys x 64 dims, V boxes of 128 keys x 64 dims (one half each)
   const CUtensorMap* mk = attn_map(p, Kbase, kv_rows, d, kAttnBKV / CL, err);
-  const CUtensorMap* mv = attn_map(p, Vbase, kv_rows, d, kAttnBKV / CL, err);
+  const CUtensorMap* mv = attn_map(p, Vbase, kv_rows, d, kAttnBKV, err);
   if (!mq || !mk || !mv) return false;
   const int QP = (a.QT + CL - 1) / CL;
   const long long units = (long long)a.n_entries * a.H * QP;                   // query-tile groups
@@ -750,10 +778,10 @@ inline bool tc_attention(cudaStream_t s, AttnPlan& p, const void* q, long long q
   cfg.numAttrs = pdl ? 2 : 1;
   cudaError_t e;
   cfg.gridDim = dim3(G * CL);
-  cfg.dynamicSmemBytes = hd == 128 ? AttnSmem<128>::total : AttnSmem<64>::total;
+  cfg.dynamicSmemBytes = CL == 2 ? AttnSmem<128, 2>::total : hd == 128 ? AttnSmem<128>::total : AttnSmem<64>::total;
   if (CL == 2)
     e = hd == 128 ? cudaLaunchKernelEx(&cfg, attn_tc_kernel<128, 2>, *mq, *mk, *mv, a, td)
-                  : cudaLaunchKernelEx(&cfg, attn_tc_kernel<64, 2>, *mq, *mk, *mv, a, td);
+                  : cudaErrorInvalidValue;
   else
     e = hd == 128 ? cudaLaunchKernelEx(&cfg, attn_tc_kernel<128, 1>, *mq, *mk, *mv, a, td)
                   : cudaLaunchKernelEx(&cfg, attn_tc_kernel<64, 1>, *mq, *mk, *mv, a, td);
@@ -768,7 +796,7 @@ inline bool tc_attention(cudaStream_t s, AttnPlan& p, const void* q, long long q
     }
     if (CL == 2)
       e = hd == 128 ? cudaLaunchKernelEx(&cfg, attn_combine_kernel<128, 2>, a, td, G)
-                    : cudaLaunchKernelEx(&cfg, attn_combine_kernel<64, 2>, a, td, G);
+                    : cudaErrorInvalidValue;
     else
       e = hd == 128 ? cudaLaunchKernelEx(&cfg, attn_combine_kernel<128, 1>, a, td, G)
                     : cudaLaunchKernelEx(&cfg, attn_combine_kernel<64, 1>, a, td, G);

@@ -13,6 +13,8 @@
 // The K reduction order is fixed (64-wide blocks, ascending), independent of M and
 // of the tile shape, so results are batch invariant.
 #pragma once
+#include <cstdio>
+#include <cstdlib>
 #include <string>
 #include <algorithm>
 #include <unordered_map>
@@ -144,6 +146,64 @@ __device__ __forceinline__ void gemm_epilogue_chunk(const EpiArgs& ep, int r, in
   }
 }
 
+// Stream-K (sk = 1): the tiles x k-blocks iteration space is split evenly over the
+// clusters (contiguous unit ranges), so M = 1560 shapes with few output tiles still keep
+// every SM on full-width tiles.  A cluster whose range ends inside a tile writes that
+// partial accumulator to its workspace slot and raises its flag; the cluster holding
+// the tile's last k-block adds the earlier partials (ascending cluster order: a fixed,
+// deterministic reduction order for a given shape) before the epilogue.  Each cluster
+// walks its range from the END, so partials are produced first and consumed last.
+struct GemmSk {
+  int on;
+  float* ws;      // [slot = cluster * MC + rank][BN / 32][8][128 rows][4] fp32 partials
+  int* flags;     // [slot] 1 = partial ready (reset to 0 by its consumer)
+};
+constexpr int kGemmSkSlotFloats = kGemmMaxBN * kGemmBM;   // 128 KB per slot
+
+struct GemmSeg {
+  int t, kb0, kb1;   // tile, k-block range [kb0, kb1)
+};
+struct GemmSegIter {
+  int sk, KB, tiles, cid, ncl, t_next;
+  long long u0, cur;
+  __device__ void init(int sk_, int KB_, int tiles_, int cid_, int ncl_) {
+    sk = sk_;
+    KB = KB_;
+    tiles = tiles_;
+    cid = cid_;
+    ncl = ncl_;
+    t_next = cid;
+    const long long U = (long long)tiles * KB;
+    u0 = U * cid / ncl;
+    cur = U * (cid + 1) / ncl;
+  }
+  __device__ bool next(GemmSeg& g) {
+    if (!sk) {
+      if (t_next >= tiles) return false;
+      g.t = t_next;
+      g.kb0 = 0;
+      g.kb1 = KB;
+      t_next += ncl;
+      return true;
+    }
+    if (cur <= u0) return false;
+    const long long e = cur;
+    const int t = int((e - 1) / KB);
+    const long long ts = (long long)t * KB;
+    const long long b = ts > u0 ? ts : u0;
+    g.t = t;
+    g.kb0 = int(b - ts);
+    g.kb1 = int(e - ts);
+    cur = b;
+    return true;
+  }
+  // cluster whose range holds unit u (same split as init)
+  __device__ int cluster_of(long long u) const {
+    const long long U = (long long)tiles * KB;
+    return int(((u + 1) * ncl + U - 1) / U) - 1;
+  }
+};
+
 // MC = CTAs per cluster along M (1 or 2).  MC = 2 is a CTA pair (tcgen05 cta_group::2):
 // the two CTAs hold consecutive m-blocks (A rows) and one half each of the BN W rows;
 // the even CTA issues M = 256 MMAs that read both halves in place and accumulate 128
@@ -154,7 +214,7 @@ template <int EPI, typename TOut, int MC>
 __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA,
                                                          const __grid_constant__ CUtensorMap tmB,
                                                          const __grid_constant__ CUtensorMap tmX, int M, int N, int K,
-                                                         int BN, EpiArgs ep) {
+                                                         int BN, EpiArgs ep, GemmSk sk) {
   // Residual epilogues stage the fp32 x tile in shared memory: TMA load issued as soon
   // as the epilogue warps reach the tile (overlapping the mainloop), in-place update,
   // TMA store.  128-byte swizzled 32-column boxes keep the row-per-thread smem accesses
@@ -186,6 +246,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
   const int cr = MC > 1 ? int(tc::cluster_ctarank()) : 0;
   const int cid = blockIdx.x / MC, ncl = gridDim.x / MC;
   const uint16_t mc_mask = uint16_t((1u << MC) - 1);
+  GemmSegIter segs;
+  segs.init(sk.on, kblocks, tiles, cid, ncl);
   if (threadIdx.x == 0) pdl_trigger();
 
   if (warp == 0 && lane == 0) {
@@ -235,22 +297,27 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
       // Weights never change: prefetch the first ring of W tiles before waiting for the
       // upstream kernel (PDL), then stream the activations.
       int pre = 0;
-      if (cid < tiles && MC == 1) {
-        const int nb0 = cid / num_mg;
-        pre = kblocks < kStages ? kblocks : kStages;
+      GemmSegIter it = segs;
+      GemmSeg g0;
+      if (MC == 1 && it.next(g0)) {
+        const int nb0 = g0.t / num_mg;
+        pre = g0.kb1 - g0.kb0 < kStages ? g0.kb1 - g0.kb0 : kStages;
         if (tc::elect_one()) {
-          for (int kb = 0; kb < pre; ++kb) {
-            tc::mbar_expect_tx(full + kb, bytes);
-            load_w(kb, kb, nb0);
+          for (int i = 0; i < pre; ++i) {
+            tc::mbar_expect_tx(full + i, bytes);
+            load_w(i, g0.kb0 + i, nb0);
           }
         }
         __syncwarp();
       }
       pdl_wait();
       int kg = 0;   // k-blocks loaded by this CTA (trace index)
-      for (int t = cid; t < tiles; t += ncl) {
+      it = segs;
+      GemmSeg g;
+      while (it.next(g)) {
+        const int t = g.t;
         const int mb = (t % num_mg) * MC + cr, nb = t / num_mg;
-        for (int kb = 0; kb < kblocks; ++kb, ++kg) {
+        for (int kb = g.kb0; kb < g.kb1; ++kb, ++kg) {
           if (pre > 0) {   // first tile, W already in flight for this stage
             if (tc::elect_one()) load_a(stage, kb, mb);
             --pre;
@@ -279,12 +346,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
       int acc = 0;
       uint32_t acc_phase = 0;
       int kg = 0, nt = 0;
-      for (int t = cid; t < tiles; t += ncl, ++nt) {
+      GemmSegIter it = segs;
+      GemmSeg g;
+      for (; it.next(g); ++nt) {
         tc::mbar_wait(tempty + acc, acc_phase ^ 1);
         if (lane == 0) GEMM_TRACE(2, nt);
         tc::tc_fence_after();
         const uint32_t d_tmem = tmem + uint32_t(acc * BN);
-        for (int kb = 0; kb < kblocks; ++kb, ++kg) {
+        for (int kb = g.kb0; kb < g.kb1; ++kb, ++kg) {
           tc::mbar_wait(full + stage, phase);
           if (lane == 0) GEMM_TRACE(1, kg);
           tc::tc_fence_after();
@@ -295,10 +364,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
             for (int k = 0; k < kGemmBK / 16; ++k) {
               if (MC > 1)
                 tc::mma_bf16_cg2(d_tmem, tc::sw128_kmajor_desc(a0 + k * 32), tc::sw128_kmajor_desc(b0 + k * 32), idesc,
-                                 (kb | k) != 0);
+                                 (kb - g.kb0 | k) != 0);
               else
                 tc::mma_bf16(d_tmem, tc::sw128_kmajor_desc(a0 + k * 32), tc::sw128_kmajor_desc(b0 + k * 32), idesc,
-                             (kb | k) != 0);
+                             (kb - g.kb0 | k) != 0);
             }
             if (MC > 1) tc::mma_commit_cg2_mc(empty + stage, mc_mask);
             else tc::mma_commit(empty + stage);
@@ -329,10 +398,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
     const int row = q * 32 + lane;      // row inside the tile
     int acc = 0;
     uint32_t acc_phase = 0;
-    int nt = 0;                         // tiles done by this CTA
-    for (int t = cid; t < tiles; t += ncl, ++nt) {
+    int nt = 0, nx = 0;                 // segments / residual tiles done by this CTA
+    GemmSegIter it = segs;
+    GemmSeg g;
+    for (; it.next(g); ++nt) {
+      const int t = g.t;
       const int mb = (t % num_mg) * MC + cr, nb = t / num_mg;
-      if (kResTMA && leader) {          // fetch the residual tile while the MMAs run
+      const bool partial = g.kb1 < kblocks;        // stream-K: hand the partial sum on
+      const bool fixup = !partial && g.kb0 > 0;    // stream-K: add the earlier partials
+      const int c_first = fixup ? it.cluster_of((long long)t * kblocks) : cid;
+      float* ws_mine = sk.ws + size_t(cid * MC + cr) * kGemmSkSlotFloats;
+      if (kResTMA && !partial && leader) {   // fetch the residual tile while the MMAs run
         tc::mbar_expect_tx(x_full, uint32_t(BN) * kGemmBM * 4);
         for (int c = 0; c < BN; c += 32)
           tc::tma_load_2d(sX + (c / 32) * (kGemmBM * 128), &tmX, x_full, nb * BN + c, mb * kGemmBM);
@@ -344,7 +420,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
       const int e_hi = ((row0 + kGemmBM - 1) < M ? row0 + kGemmBM - 1 : M - 1) / ep.L;
       const bool gate_smem = EPI == EPI_RES_GATE && e_hi <= e_lo + 1;
       asm volatile("bar.sync 3, 256;" ::: "memory");   // previous tile's readers done
-      for (int i = threadIdx.x - 128; i < BN; i += 256) {
+      for (int i = threadIdx.x - 128; i < (partial ? 0 : BN); i += 256) {
         const int col = nb * BN + i;
         const bool ok = col < N;
         sBias[i] = ok ? ep.bias[col] : 0.f;
@@ -354,15 +430,54 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
           if (e_hi > e_lo) sGate[kGemmMaxBN + i] = ok ? gm + ep.e0[size_t(e_hi) * 6 * N + ep.gate_row * N + col] : 0.f;
         }
       }
+      if (fixup && threadIdx.x == 128) {   // earlier clusters' partials of this tile are ready
+        for (int cc = c_first; cc < cid; ++cc) {
+          const int* f = sk.flags + cc * MC + cr;
+          int v = 0;
+          do {
+            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+          } while (v == 0);
+        }
+      }
       asm volatile("bar.sync 3, 256;" ::: "memory");
       tc::mbar_wait(tfull + acc, acc_phase);
       if (warp == 4 && lane == 0) GEMM_TRACE(4, nt);
       tc::tc_fence_after();
       const int r = mb * kGemmBM + row;
       const float* gsm = sGate + ((r < M ? r : M - 1) / ep.L > e_lo ? kGemmMaxBN : 0);
-      if (kResTMA) tc::mbar_wait(x_full, nt & 1);
+      if (kResTMA && !partial) tc::mbar_wait(x_full, (nx++) & 1);
       const uint32_t tbase = tmem + (uint32_t(q * 32) << 16) + uint32_t(acc * BN);
-      auto chunk = [&](const uint32_t(&v)[32], int c) {
+      auto chunk = [&](const uint32_t(&v0)[32], int c) {
+        if (partial) {   // [chunk][j][row][4]: a warp stores 32 rows x 16 B contiguously
+          float4* dst = reinterpret_cast<float4*>(ws_mine) + size_t(c / 32) * 8 * kGemmBM + row;
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            __stcg(dst + j * kGemmBM, make_float4(__uint_as_float(v0[4 * j]), __uint_as_float(v0[4 * j + 1]),
+                                                  __uint_as_float(v0[4 * j + 2]), __uint_as_float(v0[4 * j + 3])));
+          return;
+        }
+        uint32_t v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = v0[i];
+        if (fixup) {
+          float a[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) a[i] = 0.f;
+          for (int cc = c_first; cc < cid; ++cc) {   // partials in cluster (= k) order, then this tail
+            const float4* src = reinterpret_cast<const float4*>(sk.ws + size_t(cc * MC + cr) * kGemmSkSlotFloats) +
+                                size_t(c / 32) * 8 * kGemmBM + row;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float4 p = __ldcg(src + j * kGemmBM);
+              a[4 * j] += p.x;
+              a[4 * j + 1] += p.y;
+              a[4 * j + 2] += p.z;
+              a[4 * j + 3] += p.w;
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(a[i] + __uint_as_float(v[i]));
+        }
         const int c0 = nb * BN + c;
         if (kResTMA) {
           if (c0 + 32 <= N) {
@@ -427,7 +542,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
         if (MC > 1) tc::mbar_arrive_cluster(tc::mapa_shared(tempty + acc, 0));
         else tc::mbar_arrive(tempty + acc);
       }
-      if (kResTMA) {
+      if (partial) {   // publish: every thread's stores, then one release of the flag
+        __threadfence();
+        asm volatile("bar.sync 3, 256;" ::: "memory");
+        if (threadIdx.x == 128)
+          asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(sk.flags + cid * MC + cr), "r"(1) : "memory");
+      }
+      if (fixup) {     // consumed: re-arm the contributors' flags for the next launch
+        asm volatile("bar.sync 3, 256;" ::: "memory");
+        if (threadIdx.x == 128)
+          for (int cc = c_first; cc < cid; ++cc) sk.flags[cc * MC + cr] = 0;
+      }
+      if (kResTMA && !partial) {
         tc::fence_proxy_async_smem();   // generic-proxy smem writes -> visible to the TMA store
         asm volatile("bar.sync 2, 256;" ::: "memory");
         if (leader) {
@@ -459,11 +585,17 @@ typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_
                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
+struct GemmCfg {
+  int MC, BN, SK;   // cluster size (1 or CTA pair), tile width, stream-K
+};
+
 struct TmaGemmPlan {
   PFN_encodeTiled encode = nullptr;
   int num_sms = 148;
   std::unordered_map<std::string, CUtensorMap> maps;
-  std::unordered_map<std::string, std::pair<int, int>> tuned;   // "M:N:K:epi" -> (MC, BN)
+  std::unordered_map<std::string, GemmCfg> tuned;   // "M:N:K:epi" -> configuration
+  float* sk_ws = nullptr;                           // stream-K partial slots [num_sms][128 KB]
+  int* sk_flags = nullptr;                          // [num_sms], zero between launches
 };
 
 inline bool tc_gemm_enabled() { return true; }
@@ -489,6 +621,14 @@ inline bool tc_gemm_plan(TmaGemmPlan& p, std::string* err) {
   gemm_set_attr<EPI_RES_GATE, bf16, 1>(); gemm_set_attr<EPI_RES_GATE, bf16, 2>();
   gemm_set_attr<EPI_RES, bf16, 1>(); gemm_set_attr<EPI_RES, bf16, 2>();
   gemm_set_attr<EPI_STORE, float, 1>(); gemm_set_attr<EPI_STORE, float, 2>();
+  if (!p.sk_ws) {
+    if (cudaMalloc(&p.sk_ws, size_t(p.num_sms) * kGemmSkSlotFloats * sizeof(float)) != cudaSuccess ||
+        cudaMalloc(&p.sk_flags, size_t(p.num_sms) * sizeof(int)) != cudaSuccess ||
+        cudaMemset(p.sk_flags, 0, size_t(p.num_sms) * sizeof(int)) != cudaSuccess) {
+      *err = "stream-K workspace allocation failed";
+      return false;
+    }
+  }
   return true;
 }
 
@@ -571,7 +711,8 @@ inline bool& gemm_pdl_flag() {
 
 template <int EPI, typename TOut, int MC>
 inline cudaError_t gemm_launch(cudaStream_t s, int grid, const CUtensorMap& ma, const CUtensorMap& mb,
-                               const CUtensorMap& mx, int M, int N, int K, int BN, const EpiArgs& ep) {
+                               const CUtensorMap& mx, int M, int N, int K, int BN, const EpiArgs& ep,
+                               const GemmSk& sk) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kGemmThreads);
@@ -586,18 +727,19 @@ inline cudaError_t gemm_launch(cudaStream_t s, int grid, const CUtensorMap& ma, 
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = gemm_pdl_flag() ? 2 : 1;
-  return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<EPI, TOut, MC>, ma, mb, mx, M, N, K, BN, ep);
+  return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<EPI, TOut, MC>, ma, mb, mx, M, N, K, BN, ep, sk);
 }
 
 template <int MC>
 inline cudaError_t gemm_dispatch(cudaStream_t s, int grid, const CUtensorMap& ma, const CUtensorMap& mb,
-                                 const CUtensorMap& mx, int M, int N, int K, int BN, int epi, const EpiArgs& ep) {
+                                 const CUtensorMap& mx, int M, int N, int K, int BN, int epi, const EpiArgs& ep,
+                                 const GemmSk& sk) {
   switch (epi) {
-    case EPI_STORE: return gemm_launch<EPI_STORE, bf16, MC>(s, grid, ma, mb, mx, M, N, K, BN, ep);
-    case EPI_GELU: return gemm_launch<EPI_GELU, bf16, MC>(s, grid, ma, mb, mx, M, N, K, BN, ep);
-    case EPI_RES_GATE: return gemm_launch<EPI_RES_GATE, bf16, MC>(s, grid, ma, mb, mx, M, N, K, BN, ep);
-    case EPI_STORE_F32: return gemm_launch<EPI_STORE, float, MC>(s, grid, ma, mb, mx, M, N, K, BN, ep);
-    default: return gemm_launch<EPI_RES, bf16, MC>(s, grid, ma, mb, mx, M, N, K, BN, ep);
+    case EPI_STORE: return gemm_launch<EPI_STORE, bf16, MC>(s, grid, ma, mb, mx, M, N, K, BN, ep, sk);
+    case EPI_GELU: return gemm_launch<EPI_GELU, bf16, MC>(s, grid, ma, mb, mx, M, N, K, BN, ep, sk);
+    case EPI_RES_GATE: return gemm_launch<EPI_RES_GATE, bf16, MC>(s, grid, ma, mb, mx, M, N, K, BN, ep, sk);
+    case EPI_STORE_F32: return gemm_launch<EPI_STORE, float, MC>(s, grid, ma, mb, mx, M, N, K, BN, ep, sk);
+    default: return gemm_launch<EPI_RES, bf16, MC>(s, grid, ma, mb, mx, M, N, K, BN, ep, sk);
   }
 }
 
@@ -605,14 +747,19 @@ inline int tc_gemm_default_mc() {
   const char* e = getenv("SDV2_GEMM_MC");
   return e ? atoi(e) : 1;
 }
+inline int tc_gemm_default_sk() {
+  const char* e = getenv("SDV2_GEMM_SK");
+  return e ? atoi(e) : 0;
+}
 
 inline std::string gemm_key(int M, int N, int K, int epi) {
   return std::to_string(M) + ":" + std::to_string(N) + ":" + std::to_string(K) + ":" + std::to_string(epi);
 }
 
-// One launch with an explicit (cluster size, tile width) configuration.
+// One launch with an explicit (cluster size, tile width, stream-K) configuration.
 inline bool tc_gemm_cfg(cudaStream_t s, TmaGemmPlan& p, const void* A, const void* W, int M, int N, int K, int epi,
-                        const EpiArgs& ep, int MC, int BN, std::string* err) {
+                        const EpiArgs& ep, const GemmCfg& gc, std::string* err) {
+  const int MC = gc.MC, BN = gc.BN;
   const int num_m = (M + kGemmBM - 1) / kGemmBM;
   const bool res = (epi == EPI_RES_GATE || epi == EPI_RES);
   const CUtensorMap* ma = tc_map(p, A, M, K, kGemmBM, err);
@@ -621,10 +768,12 @@ inline bool tc_gemm_cfg(cudaStream_t s, TmaGemmPlan& p, const void* A, const voi
   const CUtensorMap* mx = res ? tc_map_res(p, ep.out, M, N, ep.ldo, err) : ma;
   if (!mx) return false;
   const int tiles = ((num_m + MC - 1) / MC) * ((N + BN - 1) / BN);
+  const long long work = gc.SK ? (long long)tiles * (K / kGemmBK) : tiles;   // stream-K: tile x k-block units
   const int slots = p.num_sms / MC;
-  const int grid = MC * (tiles < slots ? tiles : slots);
-  cudaError_t e = MC == 2 ? gemm_dispatch<2>(s, grid, *ma, *mb, *mx, M, N, K, BN, epi, ep)
-                          : gemm_dispatch<1>(s, grid, *ma, *mb, *mx, M, N, K, BN, epi, ep);
+  const int grid = MC * int(work < slots ? work : slots);
+  const GemmSk sk{gc.SK, p.sk_ws, p.sk_flags};
+  cudaError_t e = MC == 2 ? gemm_dispatch<2>(s, grid, *ma, *mb, *mx, M, N, K, BN, epi, ep, sk)
+                          : gemm_dispatch<1>(s, grid, *ma, *mb, *mx, M, N, K, BN, epi, ep, sk);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     *err = std::string("gemm_tc launch: ") + cudaGetErrorString(e);
@@ -646,30 +795,29 @@ inline bool tc_gemm_check(int N, int K, int epi, std::string* err) {
 }
 
 // Default configuration from the tile-balance model (used when a shape was not tuned).
-inline void tc_gemm_default_cfg(const TmaGemmPlan& p, int M, int N, int epi, int* MC, int* BN) {
+inline GemmCfg tc_gemm_default_cfg(const TmaGemmPlan& p, int M, int N, int epi) {
   const int num_m = (M + kGemmBM - 1) / kGemmBM;
-  *MC = (num_m >= 2 && tc_gemm_default_mc() == 2) ? 2 : 1;
+  GemmCfg c;
+  c.MC = (num_m >= 2 && tc_gemm_default_mc() == 2) ? 2 : 1;
+  c.SK = tc_gemm_default_sk();
   const bool res = (epi == EPI_RES_GATE || epi == EPI_RES);
-  *BN = tc_pick_bn(M, N, p.num_sms, *MC, res ? kResMaxBN : 256);
+  const int max_bn = res ? kResMaxBN : 256;
+  c.BN = c.SK ? std::min(max_bn, (N + 31) / 32 * 32) : tc_pick_bn(M, N, p.num_sms, c.MC, max_bn);
+  return c;
 }
 
 inline bool tc_gemm(cudaStream_t s, TmaGemmPlan& p, const void* A, const void* W, int M, int N, int K, int epi,
                     const EpiArgs& ep, std::string* err, int a_rows_alloc = 0) {
   (void)a_rows_alloc;
   if (!tc_gemm_check(N, K, epi, err)) return false;
-  int MC, BN;
   auto it = p.tuned.find(gemm_key(M, N, K, epi));
-  if (it != p.tuned.end()) {
-    MC = it->second.first;
-    BN = it->second.second;
-  } else {
-    tc_gemm_default_cfg(p, M, N, epi, &MC, &BN);
-  }
-  return tc_gemm_cfg(s, p, A, W, M, N, K, epi, ep, MC, BN, err);
+  const GemmCfg gc = it != p.tuned.end() ? it->second : tc_gemm_default_cfg(p, M, N, epi);
+  return tc_gemm_cfg(s, p, A, W, M, N, K, epi, ep, gc, err);
 }
 
 // Create-time autotuning of one GEMM shape on the real buffers: the best of
-// {MC = 1, 2} x the three best tile widths of the balance model, by CUDA-event time.
+// {MC = 1, 2} x (the three best tile widths of the balance model, or stream-K at the
+// widest tile), by CUDA-event time.
 inline bool tc_gemm_tune(cudaStream_t s, TmaGemmPlan& p, const void* A, const void* W, int M, int N, int K, int epi,
                          const EpiArgs& ep, std::string* err) {
   if (!tc_gemm_check(N, K, epi, err)) return false;
@@ -677,8 +825,9 @@ inline bool tc_gemm_tune(cudaStream_t s, TmaGemmPlan& p, const void* A, const vo
   if (p.tuned.count(key)) return true;
   const int num_m = (M + kGemmBM - 1) / kGemmBM;
   const bool res = (epi == EPI_RES_GATE || epi == EPI_RES);
-  std::vector<std::pair<int, int>> cands;
+  std::vector<GemmCfg> cands;
   for (int MC = 1; MC <= (num_m >= 2 ? 2 : 1); ++MC) {
+    cands.push_back({MC, std::min(res ? kResMaxBN : 256, (N + 31) / 32 * 32), 1});
     std::vector<std::pair<double, int>> ranked;
     const int num_mg = (num_m + MC - 1) / MC, slots = p.num_sms / MC;
     for (int bn = res ? kResMaxBN : 256; bn >= 64; bn -= 32) {
@@ -688,18 +837,18 @@ inline bool tc_gemm_tune(cudaStream_t s, TmaGemmPlan& p, const void* A, const vo
       ranked.push_back({-eff, -bn});
     }
     std::sort(ranked.begin(), ranked.end());
-    for (size_t i = 0; i < ranked.size() && i < 3; ++i) cands.push_back({MC, -ranked[i].second});
+    for (size_t i = 0; i < ranked.size() && i < 3; ++i) cands.push_back({MC, -ranked[i].second, 0});
   }
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   float best = 1e30f;
-  std::pair<int, int> best_cfg = cands.front();
+  GemmCfg best_cfg = cands.front();
   for (auto& c : cands) {
     for (int i = 0; i < 2; ++i)
-      if (!tc_gemm_cfg(s, p, A, W, M, N, K, epi, ep, c.first, c.second, err)) return false;
+      if (!tc_gemm_cfg(s, p, A, W, M, N, K, epi, ep, c, err)) return false;
     cudaEventRecord(a, s);
-    for (int i = 0; i < 5; ++i) tc_gemm_cfg(s, p, A, W, M, N, K, epi, ep, c.first, c.second, err);
+    for (int i = 0; i < 5; ++i) tc_gemm_cfg(s, p, A, W, M, N, K, epi, ep, c, err);
     cudaEventRecord(b, s);
     cudaEventSynchronize(b);
     float ms = 0.f;
@@ -712,6 +861,9 @@ inline bool tc_gemm_tune(cudaStream_t s, TmaGemmPlan& p, const void* A, const vo
   cudaEventDestroy(a);
   cudaEventDestroy(b);
   p.tuned[key] = best_cfg;
+  if (getenv("SDV2_VERBOSE"))
+    fprintf(stderr, "sdv2 gemm tune M=%d N=%d K=%d epi=%d -> MC=%d BN=%d SK=%d (%.1f us)\n", M, N, K, epi,
+            best_cfg.MC, best_cfg.BN, best_cfg.SK, best * 1e3f / 5.f);
   return cudaGetLastError() == cudaSuccess;
 }
 

@@ -430,7 +430,7 @@ sdv2_status attention(sdv2_handle* h, const AttnArgs& aa, int Mrows_entries, dou
         tiles += (long long)ta.H * ta.QT * ((Lk + kAttnBKV - 1) / kAttnBKV);
       }
       {
-        const int CL = attn_cluster(), QP = (ta.QT + CL - 1) / CL;   // decide on query-tile groups
+        const int CL = h->hd == 128 ? attn_cluster() : 1, QP = (ta.QT + CL - 1) / CL;   // decide on query-tile groups
         ta.per_unit = attn_pick_per_unit((long long)Mrows_entries * ta.H * QP, tiles * QP / ta.QT,
                                          h->aplan.num_sms / CL);
       }

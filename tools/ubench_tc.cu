@@ -35,6 +35,7 @@ __device__ __forceinline__ bool elect_one() {
 // mode 14: mode 9 (N = 256) alternating between 2 accumulators
 // mode 15 / 16: mode 8 / 9 issued by the whole converged warp through elect.sync
 // mode 17: mode 15 with one elect.sync around the 8 MMAs (not one per MMA)
+// mode 18: mode 17 with N = 64
 __global__ void __launch_bounds__(160, 1) ubench(int mode, long long* out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -55,12 +56,12 @@ __global__ void __launch_bounds__(160, 1) ubench(int mode, long long* out) {
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *slot;
-  const int NN = (mode == 7 || mode == 9 || mode == 14 || mode == 16) ? 256 : mode == 10 ? 64 : mode == 11 ? 192 : 128;
+  const int NN = (mode == 7 || mode == 9 || mode == 14 || mode == 16) ? 256 : (mode == 10 || mode == 18) ? 64 : mode == 11 ? 192 : 128;
   const int nacc = (mode == 12 || mode == 14) ? 2 : mode == 13 ? 4 : 1;
   const uint32_t idS = tc::idesc_bf16(128, NN);
   const uint32_t idO = tc::idesc_bf16(128, 128, true);
   long long t0 = clock64();
-  if (warp == 4 && mode == 17) {
+  if (warp == 4 && (mode == 17 || mode == 18)) {
     const uint32_t qa = tc::smem_u32(sA), ka = tc::smem_u32(sB);
     for (int it = 0; it < kIters; ++it) {
       if (elect_one()) {
@@ -178,8 +179,8 @@ int main(int argc, char** argv) {
                          "8 SS MMA N=64, no commits", "8 SS MMA N=192, no commits",
                          "8 SS MMA N=128, 2 accumulators", "8 SS MMA N=128, 4 accumulators",
                          "8 SS MMA N=256, 2 accumulators", "8 SS MMA N=128, warp + elect",
-                         "8 SS MMA N=256, warp + elect", "8 SS MMA N=128, one elect"};
-  for (int mode = 0; mode < 18; ++mode) {
+                         "8 SS MMA N=256, warp + elect", "8 SS MMA N=128, one elect", "8 SS MMA N=64, one elect"};
+  for (int mode = 0; mode < 19; ++mode) {
     for (int rep = 0; rep < 2; ++rep) ubench<<<grid, 160, smem>>>(mode, d);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
