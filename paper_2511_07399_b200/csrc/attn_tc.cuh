@@ -637,52 +637,79 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
 }
 
 // Merge the partial units (split between consecutive CTAs) in CTA order:
-// O = sum_k 2^(m_k - M) O_k / sum_k 2^(m_k - M) l_k.  One CTA per unit; a warp per row,
-// lanes across the head dim (coalesced 512 B row reads).
+// O = sum_k 2^(m_k - M) O_k / sum_k 2^(m_k - M) l_k.  16 CTAs per unit, a warp per row,
+// lanes across the head dim (coalesced 512 B row reads); every contribution of a row is
+// loaded before any is used (the merge is latency-bound: one round trip per row).
+constexpr int kAttnCombineRowsPerCTA = 8;
 template <int HD, int CL>
 __global__ void __launch_bounds__(256) attn_combine_kernel(AttnTcArgs a, const TickDesc* __restrict__ td, int G) {
   pdl_wait();
   pdl_trigger();
   constexpr int PL = HD / 32;   // columns per lane
+  constexpr int kGroups = kAttnBQ / kAttnCombineRowsPerCTA;
   AttnGeo geo;
   geo.init(a, td, CL);
-  const int pu = blockIdx.x / CL, cr = blockIdx.x % CL;   // query-tile group unit, member
+  const int rg = blockIdx.x % kGroups, ub = blockIdx.x / kGroups;
+  const int pu = ub / CL, cr = ub % CL;   // query-tile group unit, member
   const int e = pu / (a.H * geo.QP), w = pu % (a.H * geo.QP);
   if (e >= a.n_entries || geo.J[e] == 0) return;
   const long long off = geo.off[e] + (long long)w * geo.J[e];
   const int cf = geo.cta_of(off, G), cl = geo.cta_of(off + geo.J[e] - 1, G);
   if (a.per_unit || cf == cl) return;   // one cluster covered the whole unit and wrote the final output
   const int h = w / geo.QP, q0 = ((w % geo.QP) * CL + cr) * kAttnBQ;
-  if (q0 >= a.L) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row = rg * kAttnCombineRowsPerCTA + warp;
+  const int qr = q0 + row;
+  if (qr >= a.L) return;
   const int slot_f = geo.start(cf, G) < off ? 1 : 0;
-  for (int row = warp; row < kAttnBQ; row += 8) {
-    const int qr = q0 + row;
-    if (qr >= a.L) break;
-    float M = -INFINITY;
-    for (int cc = cf; cc <= cl; ++cc) {
-      const int slot = cc == cf ? slot_f : 0;
-      M = fmaxf(M, a.part_ml[((size_t(cc * CL + cr) * 2 + slot) * kAttnBQ + row) * 2]);
-    }
-    float den = 0.f, acc[PL];
+  constexpr int kMaxC = 4;   // contributions held in registers (more: second pass)
+  const int nc = cl - cf + 1;
+  float mk[kMaxC], lk[kMaxC], pv[kMaxC][PL];
 #pragma unroll
-    for (int i = 0; i < PL; ++i) acc[i] = 0.f;
-    for (int cc = cf; cc <= cl; ++cc) {
-      const int slot = cc == cf ? slot_f : 0;
-      const size_t base = (size_t(cc * CL + cr) * 2 + slot) * kAttnBQ + row;
-      const float wgt = exp2f(a.part_ml[base * 2] - M);
-      den += wgt * a.part_ml[base * 2 + 1];
+  for (int k = 0; k < kMaxC; ++k) {
+    if (k < nc) {
+      const int cc = cf + k;
+      const size_t base = (size_t(cc * CL + cr) * 2 + (k == 0 ? slot_f : 0)) * kAttnBQ + row;
+      const float2 ml = __ldcg(reinterpret_cast<const float2*>(a.part_ml) + base);
+      mk[k] = ml.x;
+      lk[k] = ml.y;
       const float* po = a.part_o + base * HD + lane * PL;
 #pragma unroll
-      for (int i = 0; i < PL; ++i) acc[i] += wgt * po[i];
+      for (int i = 0; i < PL; ++i) pv[k][i] = __ldcg(po + i);
     }
-    const float inv = 1.f / den;
-    bf16* orow = reinterpret_cast<bf16*>(a.o) + size_t(e * a.L + qr) * a.ldo + h * HD + lane * PL;
+  }
+  float M = -INFINITY;
 #pragma unroll
-    for (int i = 0; i < PL; i += 2) {
-      __nv_bfloat162 b2 = __floats2bfloat162_rn(acc[i] * inv, acc[i + 1] * inv);
-      *reinterpret_cast<__nv_bfloat162*>(orow + i) = b2;
+  for (int k = 0; k < kMaxC; ++k)
+    if (k < nc) M = fmaxf(M, mk[k]);
+  for (int cc = cf + kMaxC; cc <= cl; ++cc)
+    M = fmaxf(M, __ldcg(a.part_ml + ((size_t(cc * CL + cr) * 2) * kAttnBQ + row) * 2));
+  float den = 0.f, acc[PL];
+#pragma unroll
+  for (int i = 0; i < PL; ++i) acc[i] = 0.f;
+#pragma unroll
+  for (int k = 0; k < kMaxC; ++k) {
+    if (k < nc) {
+      const float wgt = exp2f(mk[k] - M);
+      den += wgt * lk[k];
+#pragma unroll
+      for (int i = 0; i < PL; ++i) acc[i] += wgt * pv[k][i];
     }
+  }
+  for (int cc = cf + kMaxC; cc <= cl; ++cc) {   // rare: a unit spread over > 4 CTAs
+    const size_t base = (size_t(cc * CL + cr) * 2) * kAttnBQ + row;
+    const float wgt = exp2f(__ldcg(a.part_ml + base * 2) - M);
+    den += wgt * __ldcg(a.part_ml + base * 2 + 1);
+    const float* po = a.part_o + base * HD + lane * PL;
+#pragma unroll
+    for (int i = 0; i < PL; ++i) acc[i] += wgt * __ldcg(po + i);
+  }
+  const float inv = 1.f / den;
+  bf16* orow = reinterpret_cast<bf16*>(a.o) + size_t(e * a.L + qr) * a.ldo + h * HD + lane * PL;
+#pragma unroll
+  for (int i = 0; i < PL; i += 2) {
+    __nv_bfloat162 b2 = __floats2bfloat162_rn(acc[i] * inv, acc[i + 1] * inv);
+    *reinterpret_cast<__nv_bfloat162*>(orow + i) = b2;
   }
 }
 
@@ -786,7 +813,7 @@ inline bool tc_attention(cudaStream_t s, AttnPlan& p, const void* q, long long q
     e = hd == 128 ? cudaLaunchKernelEx(&cfg, attn_tc_kernel<128, 1>, *mq, *mk, *mv, a, td)
                   : cudaLaunchKernelEx(&cfg, attn_tc_kernel<64, 1>, *mq, *mk, *mv, a, td);
   if (e == cudaSuccess && !a.per_unit) {
-    cfg.gridDim = dim3(unsigned(units * CL));
+    cfg.gridDim = dim3(unsigned(units * CL * (kAttnBQ / kAttnCombineRowsPerCTA)));
     cfg.blockDim = dim3(256);
     cfg.dynamicSmemBytes = 0;
     cfg.numAttrs = 0;

@@ -66,15 +66,30 @@ __global__ void __launch_bounds__(256) norm_mod2_kernel(const float* __restrict_
   const int r = blockIdx.x * 2 + sub;
   const bool ok = r < rows;
   const float* xr = x + size_t(ok ? r : 0) * d;
-  float4 v[NV];
+  const int e = (ok ? r : 0) / L;
+  float4 v[NV], A[NV], B[NV];
   float s = 0.f, ss = 0.f;
+  // every load is issued up front: the row of x and the modulation vectors (scale,
+  // shift, per-entry offsets) do not depend on each other, one memory round trip total
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
     const int c = (i * kRowThreads + t) * 4;
     v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (c < d && ok) v[i] = __ldcs(reinterpret_cast<const float4*>(xr + c));
-    s += v[i].x + v[i].y + v[i].z + v[i].w;
+    A[i] = B[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (c < d && ok) {
+      v[i] = __ldcs(reinterpret_cast<const float4*>(xr + c));
+      A[i] = __ldg(reinterpret_cast<const float4*>(m.modA + m.sc_off + c));
+      B[i] = __ldg(reinterpret_cast<const float4*>(m.modA + m.sh_off + c));
+      if (m.eA) {
+        const float4 ea = __ldg(reinterpret_cast<const float4*>(m.eA + size_t(e) * m.estride + m.esc_off + c));
+        const float4 eb = __ldg(reinterpret_cast<const float4*>(m.eA + size_t(e) * m.estride + m.esh_off + c));
+        A[i].x += ea.x; A[i].y += ea.y; A[i].z += ea.z; A[i].w += ea.w;
+        B[i].x += eb.x; B[i].y += eb.y; B[i].z += eb.z; B[i].w += eb.w;
+      }
+    }
   }
+#pragma unroll
+  for (int i = 0; i < NV; ++i) s += v[i].x + v[i].y + v[i].z + v[i].w;
   float mu = 0.f;
   if (center) {   // two-pass LayerNorm statistics (row in registers)
     float dummy = 0.f;
@@ -93,23 +108,13 @@ __global__ void __launch_bounds__(256) norm_mod2_kernel(const float* __restrict_
   row_sum2(ss, dummy2, &red[1][0][0], sub);
   const float inv = rsqrtf(ss / float(d) + eps);
   if (!ok) return;
-  const int e = r / L;
   TA* orow = out + size_t(r) * d;
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
     const int c = (i * kRowThreads + t) * 4;
-    if (c < d) {
-      float4 A = __ldg(reinterpret_cast<const float4*>(m.modA + m.sc_off + c));
-      float4 B = __ldg(reinterpret_cast<const float4*>(m.modA + m.sh_off + c));
-      if (m.eA) {
-        const float4 ea = __ldg(reinterpret_cast<const float4*>(m.eA + size_t(e) * m.estride + m.esc_off + c));
-        const float4 eb = __ldg(reinterpret_cast<const float4*>(m.eA + size_t(e) * m.estride + m.esh_off + c));
-        A.x += ea.x; A.y += ea.y; A.z += ea.z; A.w += ea.w;
-        B.x += eb.x; B.y += eb.y; B.z += eb.z; B.w += eb.w;
-      }
-      store4(orow + c, (v[i].x - mu) * inv * (m.a0 + A.x) + B.x, (v[i].y - mu) * inv * (m.a0 + A.y) + B.y,
-             (v[i].z - mu) * inv * (m.a0 + A.z) + B.z, (v[i].w - mu) * inv * (m.a0 + A.w) + B.w);
-    }
+    if (c < d)
+      store4(orow + c, (v[i].x - mu) * inv * (m.a0 + A[i].x) + B[i].x, (v[i].y - mu) * inv * (m.a0 + A[i].y) + B[i].y,
+             (v[i].z - mu) * inv * (m.a0 + A[i].z) + B[i].z, (v[i].w - mu) * inv * (m.a0 + A[i].w) + B[i].w);
   }
 }
 
@@ -180,14 +185,44 @@ __global__ void __launch_bounds__(256) qkv_post2_kernel(const TA* __restrict__ q
   const TA* kr = qr + d;
   const TA* vr = qr + 2 * d;
   const int units = d / UN;
-  float q[kMaxU][UN], k[kMaxU][UN];
+  // everything that does not depend on the row statistics is loaded before the
+  // reduction (q, k, v, the gains, the entry's positions and the RoPE table entries):
+  // the kernel is latency-bound at 2 rows per CTA, so one round trip instead of three
+  const int e = rr / L, tau = rr % L;
+  const int f = tau / (hn * wn), ph = (tau / wn) % hn, pw = tau % wn;
+  const EntryDesc& E = td->e[e];
+  const int pt = E.pos[f];
+  constexpr bool kPre = kMaxU <= 3;   // wide rows (d = 5120): gains / RoPE loaded late (registers)
+  constexpr int kP = kPre ? kMaxU : 1;
+  float q[kMaxU][UN], k[kMaxU][UN], vv[kMaxU][UN], gqv[kP][UN], gkv[kP][UN];
+  float cs[kP][UN / 2], sn[kP][UN / 2];
   float sq = 0.f, sk = 0.f;
+  const int half = hd / 2;
 #pragma unroll
   for (int i = 0; i < kMaxU; ++i) {
     const int u = i * kRowThreads + t;
     if (u < units && ok) {
-      U::load(qr + u * UN, q[i]);
-      U::load(kr + u * UN, k[i]);
+      const int c0 = u * UN;
+      U::load(qr + c0, q[i]);
+      U::load(kr + c0, k[i]);
+      U::load(vr + c0, vv[i]);
+      if constexpr (kPre) {
+#pragma unroll
+        for (int j = 0; j < UN; j += 4) {
+          const float4 a4 = __ldg(reinterpret_cast<const float4*>(gq + c0 + j));
+          const float4 b4 = __ldg(reinterpret_cast<const float4*>(gk + c0 + j));
+          gqv[i][j] = a4.x; gqv[i][j + 1] = a4.y; gqv[i][j + 2] = a4.z; gqv[i][j + 3] = a4.w;
+          gkv[i][j] = b4.x; gkv[i][j + 1] = b4.y; gkv[i][j + 2] = b4.z; gkv[i][j + 3] = b4.w;
+        }
+#pragma unroll
+        for (int j = 0; j < UN; j += 2) rope_cs(R, ((c0 + j) >> 1) % half, pt, ph, pw, cs[i][j / 2], sn[i][j / 2]);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < kMaxU; ++i) {
+    const int u = i * kRowThreads + t;
+    if (u < units && ok) {
 #pragma unroll
       for (int j = 0; j < UN; ++j) {
         sq += q[i][j] * q[i][j];
@@ -198,13 +233,8 @@ __global__ void __launch_bounds__(256) qkv_post2_kernel(const TA* __restrict__ q
   row_sum2(sq, sk, &red[0][0], sub);
   if (!ok) return;
   const float iq = rsqrtf(sq / float(d) + eps), ik = rsqrtf(sk / float(d) + eps);
-  const int e = rr / L, tau = rr % L;
-  const EntryDesc& E = td->e[e];
-  const int f = tau / (hn * wn), ph = (tau / wn) % hn, pw = tau % wn;
-  const int pt = E.pos[f];
   const size_t lane_base = size_t(e) * S * L * d;
   const size_t wrow = lane_base + (size_t(E.write_slot) * L + tau) * d;
-  const int half = hd / 2;
 #pragma unroll
   for (int i = 0; i < kMaxU; ++i) {
     const int u = i * kRowThreads + t;
@@ -213,21 +243,28 @@ __global__ void __launch_bounds__(256) qkv_post2_kernel(const TA* __restrict__ q
     float qo[UN], ko[UN], kn[UN];
 #pragma unroll
     for (int j = 0; j < UN; j += 2) {
-      const int c = c0 + j, pair = (c >> 1) % half;
-      float cs, sn;
-      rope_cs(R, pair, pt, ph, pw, cs, sn);
-      const float q0 = __ldg(gq + c) * q[i][j] * iq, q1 = __ldg(gq + c + 1) * q[i][j + 1] * iq;
-      const float k0 = __ldg(gk + c) * k[i][j] * ik, k1 = __ldg(gk + c + 1) * k[i][j + 1] * ik;
-      qo[j] = q0 * cs - q1 * sn;
-      qo[j + 1] = q0 * sn + q1 * cs;
-      ko[j] = k0 * cs - k1 * sn;
-      ko[j + 1] = k0 * sn + k1 * cs;
+      float c_, s_, gq0, gq1, gk0, gk1;
+      if constexpr (kPre) {
+        c_ = cs[i][j / 2];
+        s_ = sn[i][j / 2];
+        gq0 = gqv[i][j]; gq1 = gqv[i][j + 1]; gk0 = gkv[i][j]; gk1 = gkv[i][j + 1];
+      } else {
+        rope_cs(R, ((c0 + j) >> 1) % half, pt, ph, pw, c_, s_);
+        gq0 = __ldg(gq + c0 + j); gq1 = __ldg(gq + c0 + j + 1);
+        gk0 = __ldg(gk + c0 + j); gk1 = __ldg(gk + c0 + j + 1);
+      }
+      const float q0 = gq0 * q[i][j] * iq, q1 = gq1 * q[i][j + 1] * iq;
+      const float k0 = gk0 * k[i][j] * ik, k1 = gk1 * k[i][j + 1] * ik;
+      qo[j] = q0 * c_ - q1 * s_;
+      qo[j + 1] = q0 * s_ + q1 * c_;
+      ko[j] = k0 * c_ - k1 * s_;
+      ko[j + 1] = k0 * s_ + k1 * c_;
       kn[j] = k0;
       kn[j + 1] = k1;
     }
     U::store(qout + size_t(rr) * d + c0, qo);
     U::store(Kc + wrow + c0, ko);
-    U::copy(Vc + wrow + c0, vr + c0);
+    U::store(Vc + wrow + c0, vv[i]);
     if (E.refresh_mask) {
       for (int s = 0; s < 32; ++s) {
         if (!(E.refresh_mask & (1 << s))) continue;
@@ -242,7 +279,7 @@ __global__ void __launch_bounds__(256) qkv_post2_kernel(const TA* __restrict__ q
         }
         const size_t srow = lane_base + (size_t(s) * L + tau) * d;
         U::store(Kc + srow + c0, ka);
-        U::copy(Vc + srow + c0, vr + c0);
+        U::store(Vc + srow + c0, vv[i]);
       }
     }
   }
@@ -262,13 +299,24 @@ __global__ void __launch_bounds__(256) rms_rows2_kernel(TA* __restrict__ y, cons
   const bool ok = r < rows;
   TA* yr = y + size_t(ok ? r : 0) * d;
   const int units = d / UN;
-  float v[kMaxU][UN];
+  float v[kMaxU][UN], gv[kMaxU][UN];
   float ss = 0.f, dummy = 0.f;
 #pragma unroll
   for (int i = 0; i < kMaxU; ++i) {
     const int u = i * kRowThreads + t;
     if (u < units && ok) {
       U::load(yr + u * UN, v[i]);
+#pragma unroll
+      for (int j = 0; j < UN; j += 4) {
+        const float4 g4 = __ldg(reinterpret_cast<const float4*>(g + u * UN + j));
+        gv[i][j] = g4.x; gv[i][j + 1] = g4.y; gv[i][j + 2] = g4.z; gv[i][j + 3] = g4.w;
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < kMaxU; ++i) {
+    const int u = i * kRowThreads + t;
+    if (u < units && ok) {
 #pragma unroll
       for (int j = 0; j < UN; ++j) ss += v[i][j] * v[i][j];
     }
@@ -281,7 +329,7 @@ __global__ void __launch_bounds__(256) rms_rows2_kernel(TA* __restrict__ y, cons
     const int u = i * kRowThreads + t;
     if (u < units) {
 #pragma unroll
-      for (int j = 0; j < UN; ++j) v[i][j] = __ldg(g + u * UN + j) * v[i][j] * inv;
+      for (int j = 0; j < UN; ++j) v[i][j] = gv[i][j] * v[i][j] * inv;
       U::store(yr + u * UN, v[i]);
     }
   }

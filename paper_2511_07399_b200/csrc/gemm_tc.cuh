@@ -155,6 +155,8 @@ __device__ __forceinline__ void gemm_epilogue_chunk(const EpiArgs& ep, int r, in
 // walks its range from the END, so partials are produced first and consumed last.
 struct GemmSk {
   int on;
+  int x_late;     // residual epilogues, one tile per cluster: stage the x tile in the (then
+                  // idle) operand ring after the last MMA instead of a dedicated buffer
   float* ws;      // [slot = cluster * MC + rank][BN / 32][8][128 rows][4] fp32 partials
   int* flags;     // [slot] 1 = partial ready (reset to 0 by its consumer)
 };
@@ -223,12 +225,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int BNl = BN / MC;                  // W rows held by this CTA
-  const int kStages = gemm_stages(BN, kResTMA, BNl);
+  const bool x_late = kResTMA && sk.x_late;   // x tile lives in the operand ring (see GemmSk)
+  const int kStages = gemm_stages(BN, kResTMA && !x_late, BNl);
   const int kSmemB = BNl * kGemmBK * 2;     // multiple of 1024 (BNl multiple of 16... 8 rows x 128 B)
   uint8_t* sA = smem;
   uint8_t* sB = smem + kStages * kGemmSmemA;
-  uint8_t* sX = sB + kStages * kSmemB;      // [BN/32][128 rows][32 fp32], 16 KB per box
-  uint64_t* full = reinterpret_cast<uint64_t*>(sX + (kResTMA ? BN * kGemmBM * 4 : 0));
+  uint8_t* sX = x_late ? smem : sB + kStages * kSmemB;   // [BN/32][128 rows][32 fp32], 16 KB per box
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + kStages * kSmemB + (kResTMA && !x_late ? BN * kGemmBM * 4 : 0));
   uint64_t* empty = full + kStages;
   uint64_t* tfull = empty + kStages;
   uint64_t* tempty = tfull + 2;
@@ -408,7 +411,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
       const bool fixup = !partial && g.kb0 > 0;    // stream-K: add the earlier partials
       const int c_first = fixup ? it.cluster_of((long long)t * kblocks) : cid;
       float* ws_mine = sk.ws + size_t(cid * MC + cr) * kGemmSkSlotFloats;
-      if (kResTMA && !partial && leader) {   // fetch the residual tile while the MMAs run
+      if (kResTMA && !x_late && !partial && leader) {   // fetch the residual tile while the MMAs run
         tc::mbar_expect_tx(x_full, uint32_t(BN) * kGemmBM * 4);
         for (int c = 0; c < BN; c += 32)
           tc::tma_load_2d(sX + (c / 32) * (kGemmBM * 128), &tmX, x_full, nb * BN + c, mb * kGemmBM);
@@ -445,6 +448,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
       tc::tc_fence_after();
       const int r = mb * kGemmBM + row;
       const float* gsm = sGate + ((r < M ? r : M - 1) / ep.L > e_lo ? kGemmMaxBN : 0);
+      if (kResTMA && x_late && !partial && leader) {   // last MMA done: the operand ring is free
+        tc::mbar_expect_tx(x_full, uint32_t(BN) * kGemmBM * 4);
+        for (int c = 0; c < BN; c += 32)
+          tc::tma_load_2d(sX + (c / 32) * (kGemmBM * 128), &tmX, x_full, nb * BN + c, mb * kGemmBM);
+      }
       if (kResTMA && !partial) tc::mbar_wait(x_full, (nx++) & 1);
       const uint32_t tbase = tmem + (uint32_t(q * 32) << 16) + uint32_t(acc * BN);
       auto chunk = [&](const uint32_t(&v0)[32], int c) {
@@ -771,7 +779,8 @@ inline bool tc_gemm_cfg(cudaStream_t s, TmaGemmPlan& p, const void* A, const voi
   const long long work = gc.SK ? (long long)tiles * (K / kGemmBK) : tiles;   // stream-K: tile x k-block units
   const int slots = p.num_sms / MC;
   const int grid = MC * int(work < slots ? work : slots);
-  const GemmSk sk{gc.SK, p.sk_ws, p.sk_flags};
+  // residual x tile staged in the operand ring when no cluster gets a second tile
+  const GemmSk sk{gc.SK, (!gc.SK && tiles <= slots) ? 1 : 0, p.sk_ws, p.sk_flags};
   cudaError_t e = MC == 2 ? gemm_dispatch<2>(s, grid, *ma, *mb, *mx, M, N, K, BN, epi, ep, sk)
                           : gemm_dispatch<1>(s, grid, *ma, *mb, *mx, M, N, K, BN, epi, ep, sk);
   if (e == cudaSuccess) e = cudaGetLastError();
@@ -844,15 +853,31 @@ inline bool tc_gemm_tune(cudaStream_t s, TmaGemmPlan& p, const void* A, const vo
   cudaEventCreate(&b);
   float best = 1e30f;
   GemmCfg best_cfg = cands.front();
+  // each candidate: 8 launches replayed from a CUDA graph (device time only; a host
+  // launch loop would be host-bound for the short M = 1560 GEMMs and rank noise)
+  constexpr int kReps = 8;
   for (auto& c : cands) {
     for (int i = 0; i < 2; ++i)
       if (!tc_gemm_cfg(s, p, A, W, M, N, K, epi, ep, c, err)) return false;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    bool ok = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+    for (int i = 0; ok && i < kReps; ++i) ok = tc_gemm_cfg(s, p, A, W, M, N, K, epi, ep, c, err);
+    if (cudaStreamEndCapture(s, &graph) != cudaSuccess || !ok ||
+        cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
+      if (graph) cudaGraphDestroy(graph);
+      *err = "gemm tune: graph capture failed";
+      return false;
+    }
+    cudaGraphLaunch(exec, s);
     cudaEventRecord(a, s);
-    for (int i = 0; i < 5; ++i) tc_gemm_cfg(s, p, A, W, M, N, K, epi, ep, c, err);
+    cudaGraphLaunch(exec, s);
     cudaEventRecord(b, s);
     cudaEventSynchronize(b);
     float ms = 0.f;
     cudaEventElapsedTime(&ms, a, b);
+    cudaGraphExecDestroy(exec);
+    cudaGraphDestroy(graph);
     if (ms < best) {
       best = ms;
       best_cfg = c;
@@ -863,7 +888,7 @@ inline bool tc_gemm_tune(cudaStream_t s, TmaGemmPlan& p, const void* A, const vo
   p.tuned[key] = best_cfg;
   if (getenv("SDV2_VERBOSE"))
     fprintf(stderr, "sdv2 gemm tune M=%d N=%d K=%d epi=%d -> MC=%d BN=%d SK=%d (%.1f us)\n", M, N, K, epi,
-            best_cfg.MC, best_cfg.BN, best_cfg.SK, best * 1e3f / 5.f);
+            best_cfg.MC, best_cfg.BN, best_cfg.SK, best * 1e3f / kReps);
   return cudaGetLastError() == cudaSuccess;
 }
 
