@@ -5,17 +5,19 @@
 // Work unit = (entry e, head h, 128-query tile).  Keys are one contiguous row range of
 // the lane (valid slots are always a prefix, so no gather and no slot mask; only the
 // ragged key tail is masked).  The (unit, 128-key tile) space is split evenly over
-// exactly one CTA per SM ("stream-K"): a CTA walks its contiguous tile range, which
-// covers whole units in the middle and at most one partial unit at each end; partial
-// units leave (unnormalised O, running max, sum) in a scratch slot and are merged by
-// attn_combine_kernel in a fixed CTA order (deterministic).  This removes the wave
-// quantisation of 156 units on 148 SMs (1.3B, 480p, n = 1).
+// exactly one CTA per SM ("stream-K"): a CTA owns a contiguous tile range, whole units
+// in the middle and at most one piece of a unit at each end.  Ranges are walked from
+// the end, so a unit shared by CTAs c' < c is first handed on by c' ((O, m, l) piece in
+// a scratch slot + release flag) and last finished by c, which merges the pieces in CTA
+// order (deterministic) and writes the output: no separate merge kernel.  This removes
+// the wave quantisation of 156 units on 148 SMs (1.3B, 480p, n = 1).
 //
-// Per key tile g:  S_g = Q K_g^T (tcgen05.mma M=128 N=128 K=hd, D in TMEM, double
-// buffered) -> softmax (4 warps, one query row per thread, tcgen05.ld, exp2, lazy
-// rescale of O in TMEM when the row max grows by > 2^8) -> P_g (bf16, 128-byte
-// swizzled smem = UMMA K-major A) -> O += P_g V_g (tcgen05.mma N=hd, V MN-major).
-// Warp roles (192 threads): 0 TMA, 1 MMA issuer, 2..5 softmax / correction / epilogue.
+// Per key tile t:  S_t = Q K_t^T (tcgen05.mma M=128 N=128 K=hd into one of 3 rotating
+// TMEM slots) -> softmax (8 warps: TMEM lane quarter x key half; the two warps of a row
+// agree on the row max each tile; exp2 on the MUFU plus a degree-3 polynomial on the
+// FMA pipe; lazy rescale of O in TMEM when the max grows by > 2^8) -> P_t (bf16,
+// written over S_t in TMEM) -> O += P_t V_t (tcgen05.mma, A from TMEM, V MN-major).
+// Warp roles (352 threads): 0 TMA Q/K, 10 TMA V, 1 MMA issuer, 2..9 softmax / epilogue.
 #pragma once
 #include <string>
 #include <unordered_map>
@@ -52,8 +54,9 @@ struct AttnTcArgs {
   int ldo;
   int H, QT;           // heads, query tiles per entry
   int n_entries;       // entries covered (active prefix)
-  float* part_o;       // [G][2][128][HD] fp32 partial (unnormalised) O
-  float* part_ml;      // [G][2][128][2] running max (log2 domain), sum
+  float* part_o;       // [G][2 halves][HD/8 granules][128 rows][4] fp32 partial (unnormalised) O
+  float* part_ml;      // [G][128][2] running max (log2 domain), sum
+  int* flags;          // [G] partial ready (1), reset by the CTA that merges it
   int per_unit;        // 1: one CTA per unit (grid = units, no merge); 0: stream-K
   int dbg;             // test hook only (pipeline timing): bit 0 skips the softmax math,
                        // bit 1 the MMAs, bit 2 the K/V loads, bit 3 the PV MMAs, bit 4 the
@@ -68,7 +71,7 @@ struct AttnTcArgs {
       a.trace[(t) * 16 + (ev)] = clock64();                                \
   } while (0)
 
-// Stream-K geometry shared by the attention and the combine kernels.
+// Stream-K geometry of the attention kernel.
 struct AttnGeo {
   long long off[kMaxSteps + 1];   // tile offset of entry e's first unit
   int J[kMaxSteps];               // key tiles per unit of entry e
@@ -275,31 +278,34 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
   auto tS = [&](int b) { return tmem + 128u + uint32_t(b) * 128u; };
 
   // Segment iteration: [gs, ge) of global tiles inside one unit.
+  // Segment = the part of one unit inside [t0, t1).  Segments are visited from the END
+  // of the range: a unit shared with the previous CTA (whose range ends inside it) is
+  // then produced first over there and finished last here, where its pieces are merged.
   struct Seg {
     int e, h, q0, jb, je, J;
-    long long ge;
+    long long gs, ustart;   // first global tile of the segment / of its unit
   };
-  auto seg_at = [&](long long g) {
+  auto seg_before = [&](long long ge_) {   // segment ending at global tile ge_ (exclusive)
     Seg s;
     int w, j;
-    geo.locate(g, s.e, w, j);
+    geo.locate(ge_ - 1, s.e, w, j);
     s.h = w / geo.QP;
     s.q0 = ((w % geo.QP) * CL + cr) * kAttnBQ;
     s.J = geo.J[s.e];
-    s.jb = j;
-    const long long unit_end = g - j + s.J;
-    s.ge = unit_end < t1 ? unit_end : t1;
-    s.je = j + int(s.ge - g);
+    s.je = j + 1;
+    s.ustart = ge_ - 1 - j;
+    s.gs = s.ustart > t0 ? s.ustart : t0;
+    s.jb = int(s.gs - s.ustart);
     return s;
   };
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     {   // whole warp walks the loop; one elected lane issues
-      long long g = t0;
+      long long g = t1;
       int gi = 0, sg = 0;   // local tile counter, segment counter
-      while (g < t1) {
-        const Seg s = seg_at(g);
+      while (g > t0) {
+        const Seg s = seg_before(g);
         const int col = s.h * HD;
         const int kv_row = a.kv_row0 + (a.cross ? (td->e[s.e].pver & 1) : s.e) * a.kv_lane_rows;
         if (sg > 0) tc::mbar_wait(q_empty, (sg - 1) & 1);
@@ -337,7 +343,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
           }
           __syncwarp();
         }
-        g = s.ge;
+        g = s.gs;
         ++sg;
       }
     }
@@ -346,10 +352,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
     // V tiles are consumed one MMA phase later than K: an own producer keeps the K
     // prefetch from waiting on V slots.
     {
-      long long g = t0;
+      long long g = t1;
       int gi = 0;
-      while (g < t1) {
-        const Seg s = seg_at(g);
+      while (g > t0) {
+        const Seg s = seg_before(g);
         const int col = s.h * HD;
         const int kv_row = a.kv_row0 + (a.cross ? (td->e[s.e].pver & 1) : s.e) * a.kv_lane_rows;
         for (int j = s.jb; j < s.je; ++j, ++gi) {
@@ -372,7 +378,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
           }
           __syncwarp();
         }
-        g = s.ge;
+        g = s.gs;
       }
     }
   } else if (warp == 1) {
@@ -409,10 +415,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
         }
         __syncwarp();
       };
-      long long g = t0;
+      long long g = t1;
       int gi = 0, sg = 0;
-      while (g < t1) {
-        const Seg s = seg_at(g);
+      while (g > t0) {
+        const Seg s = seg_before(g);
         const int nt = s.je - s.jb;
         tc::mbar_wait(q_full, sg & 1);
         auto release_q = [&]() {   // last S of the segment issued: Q smem reusable once it lands
@@ -454,7 +460,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
           __syncwarp();
         }
         gi += nt;
-        g = s.ge;
+        g = s.gs;
         ++sg;
       }
     }
@@ -473,10 +479,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
       if (CL > 1) tc::mbar_arrive_cluster(tc::mapa_shared(bar, 0));
       else tc::mbar_arrive(bar);
     };
-    long long g = t0;
+    long long g = t1;
     int gi = 0, sg = 0;
-    while (g < t1) {
-      const Seg s = seg_at(g);
+    while (g > t0) {
+      const Seg s = seg_before(g);
       const int nt = s.je - s.jb;
       const int Lk = a.cross ? a.Lk_cross : td->e[s.e].nvalid * a.L;
       float m_used = -INFINITY;   // row max the current P / O are relative to (log2 domain)
@@ -580,49 +586,99 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
       tc::tc_fence_after();
       pair_sync();
       const float lt = l + xl[(half ^ 1) * 128 + row];
-      const bool full = (s.jb == 0 && s.je == s.J);
-      const int slot = (g == t0) ? 0 : 1;
+      const bool partial = s.je < s.J;               // head / middle piece of a unit: hand on
+      const bool finisher = !partial && s.jb > 0;    // tail piece: merge the earlier pieces
+      const int slot = c * CL + cr;
       const int qr = s.q0 + row;
-      const float inv = full ? 1.f / lt : 1.f;
+      // partial layout [slot][half][granule j][row][4]: a warp moves 32 rows x 16 B at once
+      auto part_at = [&](int sl, int j) {
+        return reinterpret_cast<float4*>(a.part_o) + (size_t(sl * 2 + half) * (HO / 4) + j) * kAttnBQ + row;
+      };
+      int c_first = c;
+      float wown = 1.f, den = lt, Mfin = m_used;
+      if (finisher) {   // pieces of this unit from CTAs c_first .. c-1 (their first-visited segment)
+        c_first = geo.cta_of(s.ustart, G);
+        if (warp == 2 && lane == 0) {
+          for (int cc = c_first; cc < c; ++cc) {
+            const int* f = a.flags + cc * CL + cr;
+            int v = 0;
+            do {
+              asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+            } while (v == 0);
+          }
+        }
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        float M = m_used;
+        for (int cc = c_first; cc < c; ++cc) M = fmaxf(M, __ldcg(a.part_ml + (size_t(cc * CL + cr) * kAttnBQ + row) * 2));
+        Mfin = M;
+        wown = m_used == -INFINITY ? 0.f : ex2(m_used - M);
+        den = lt * wown;
+        for (int cc = c_first; cc < c; ++cc) {
+          const float2 ml = __ldcg(reinterpret_cast<const float2*>(a.part_ml) + size_t(cc * CL + cr) * kAttnBQ + row);
+          den += (ml.x == -INFINITY ? 0.f : ex2(ml.x - M)) * ml.y;
+        }
+      }
+      const float inv = partial ? 1.f : 1.f / den;
       bf16* orow = reinterpret_cast<bf16*>(a.o) + size_t(s.e * a.L + qr) * a.ldo + s.h * HD + half * HO;
-      float* prow = a.part_o + ((size_t(c * CL + cr) * 2 + slot) * kAttnBQ + row) * HD + half * HO;
 #pragma unroll
       for (int cc = 0; cc < HO / 32; ++cc) {
         uint32_t r0[32];
         tc::tmem_ld32(tO + lane_off + half * HO + cc * 32, r0);
         tc::tmem_ld_wait();
         float o[32];
+        if (partial) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) o[i] = __uint_as_float(r0[i]) * inv;
-        if (full) {
-          if (qr < a.L) {
-            uint32_t pk[16];
+          for (int jj = 0; jj < 8; ++jj)
+            __stcg(part_at(slot, cc * 8 + jj), make_float4(__uint_as_float(r0[4 * jj]), __uint_as_float(r0[4 * jj + 1]),
+                                                          __uint_as_float(r0[4 * jj + 2]),
+                                                          __uint_as_float(r0[4 * jj + 3])));
+          continue;
+        }
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              __nv_bfloat162 b2 = __floats2bfloat162_rn(o[2 * i], o[2 * i + 1]);
-              pk[i] = *reinterpret_cast<uint32_t*>(&b2);
+        for (int i = 0; i < 32; ++i) o[i] = __uint_as_float(r0[i]) * wown;
+        if (finisher) {
+          const float M = Mfin;
+          for (int k = c_first; k < c; ++k) {
+            const float mk = __ldcg(a.part_ml + (size_t(k * CL + cr) * kAttnBQ + row) * 2);
+            const float wk = mk == -INFINITY ? 0.f : ex2(mk - M);
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) {
+              const float4 p4 = __ldcg(part_at(k * CL + cr, cc * 8 + jj));
+              o[4 * jj] += wk * p4.x;
+              o[4 * jj + 1] += wk * p4.y;
+              o[4 * jj + 2] += wk * p4.z;
+              o[4 * jj + 3] += wk * p4.w;
             }
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-              reinterpret_cast<uint4*>(orow + cc * 32)[i] =
-                  make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
           }
-        } else {
+        }
+        if (qr < a.L) {
+          uint32_t pk[16];
 #pragma unroll
-          for (int i = 0; i < 8; ++i)
-            reinterpret_cast<float4*>(prow + cc * 32)[i] = make_float4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
+          for (int i = 0; i < 16; ++i) {
+            __nv_bfloat162 b2 = __floats2bfloat162_rn(o[2 * i] * inv, o[2 * i + 1] * inv);
+            pk[i] = *reinterpret_cast<uint32_t*>(&b2);
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            reinterpret_cast<uint4*>(orow + cc * 32)[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
         }
       }
-      if (!full && half == 0) {
-        float* ml = a.part_ml + ((size_t(c * CL + cr) * 2 + slot) * kAttnBQ + row) * 2;
-        ml[0] = m_used;
-        ml[1] = lt;
+      if (partial) {   // publish the piece: (m, l) of the row, then one release of the flag
+        if (half == 0) __stcg(reinterpret_cast<float2*>(a.part_ml) + size_t(slot) * kAttnBQ + row, make_float2(m_used, lt));
+        __threadfence();
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        if (warp == 2 && lane == 0) asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(a.flags + slot), "r"(1) : "memory");
+      }
+      if (finisher) {   // merged: re-arm the contributors' flags for the next launch
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        if (warp == 2 && lane == 0)
+          for (int cc = c_first; cc < c; ++cc) a.flags[cc * CL + cr] = 0;
       }
       tc::tc_fence_before();
       pair_sync();   // xl reusable
       if (lane == 0) arrive_lead(o_empty);
       gi += nt;
-      g = s.ge;
+      g = s.gs;
       ++sg;
     }
   }
@@ -636,101 +692,24 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
   }
 }
 
-// Merge the partial units (split between consecutive CTAs) in CTA order:
-// O = sum_k 2^(m_k - M) O_k / sum_k 2^(m_k - M) l_k.  16 CTAs per unit, a warp per row,
-// lanes across the head dim (coalesced 512 B row reads); every contribution of a row is
-// loaded before any is used (the merge is latency-bound: one round trip per row).
-constexpr int kAttnCombineRowsPerCTA = 8;
-template <int HD, int CL>
-__global__ void __launch_bounds__(256) attn_combine_kernel(AttnTcArgs a, const TickDesc* __restrict__ td, int G) {
-  pdl_wait();
-  pdl_trigger();
-  constexpr int PL = HD / 32;   // columns per lane
-  constexpr int kGroups = kAttnBQ / kAttnCombineRowsPerCTA;
-  AttnGeo geo;
-  geo.init(a, td, CL);
-  const int rg = blockIdx.x % kGroups, ub = blockIdx.x / kGroups;
-  const int pu = ub / CL, cr = ub % CL;   // query-tile group unit, member
-  const int e = pu / (a.H * geo.QP), w = pu % (a.H * geo.QP);
-  if (e >= a.n_entries || geo.J[e] == 0) return;
-  const long long off = geo.off[e] + (long long)w * geo.J[e];
-  const int cf = geo.cta_of(off, G), cl = geo.cta_of(off + geo.J[e] - 1, G);
-  if (a.per_unit || cf == cl) return;   // one cluster covered the whole unit and wrote the final output
-  const int h = w / geo.QP, q0 = ((w % geo.QP) * CL + cr) * kAttnBQ;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int row = rg * kAttnCombineRowsPerCTA + warp;
-  const int qr = q0 + row;
-  if (qr >= a.L) return;
-  const int slot_f = geo.start(cf, G) < off ? 1 : 0;
-  constexpr int kMaxC = 4;   // contributions held in registers (more: second pass)
-  const int nc = cl - cf + 1;
-  float mk[kMaxC], lk[kMaxC], pv[kMaxC][PL];
-#pragma unroll
-  for (int k = 0; k < kMaxC; ++k) {
-    if (k < nc) {
-      const int cc = cf + k;
-      const size_t base = (size_t(cc * CL + cr) * 2 + (k == 0 ? slot_f : 0)) * kAttnBQ + row;
-      const float2 ml = __ldcg(reinterpret_cast<const float2*>(a.part_ml) + base);
-      mk[k] = ml.x;
-      lk[k] = ml.y;
-      const float* po = a.part_o + base * HD + lane * PL;
-#pragma unroll
-      for (int i = 0; i < PL; ++i) pv[k][i] = __ldcg(po + i);
-    }
-  }
-  float M = -INFINITY;
-#pragma unroll
-  for (int k = 0; k < kMaxC; ++k)
-    if (k < nc) M = fmaxf(M, mk[k]);
-  for (int cc = cf + kMaxC; cc <= cl; ++cc)
-    M = fmaxf(M, __ldcg(a.part_ml + ((size_t(cc * CL + cr) * 2) * kAttnBQ + row) * 2));
-  float den = 0.f, acc[PL];
-#pragma unroll
-  for (int i = 0; i < PL; ++i) acc[i] = 0.f;
-#pragma unroll
-  for (int k = 0; k < kMaxC; ++k) {
-    if (k < nc) {
-      const float wgt = exp2f(mk[k] - M);
-      den += wgt * lk[k];
-#pragma unroll
-      for (int i = 0; i < PL; ++i) acc[i] += wgt * pv[k][i];
-    }
-  }
-  for (int cc = cf + kMaxC; cc <= cl; ++cc) {   // rare: a unit spread over > 4 CTAs
-    const size_t base = (size_t(cc * CL + cr) * 2) * kAttnBQ + row;
-    const float wgt = exp2f(__ldcg(a.part_ml + base * 2) - M);
-    den += wgt * __ldcg(a.part_ml + base * 2 + 1);
-    const float* po = a.part_o + base * HD + lane * PL;
-#pragma unroll
-    for (int i = 0; i < PL; ++i) acc[i] += wgt * __ldcg(po + i);
-  }
-  const float inv = 1.f / den;
-  bf16* orow = reinterpret_cast<bf16*>(a.o) + size_t(e * a.L + qr) * a.ldo + h * HD + lane * PL;
-#pragma unroll
-  for (int i = 0; i < PL; i += 2) {
-    __nv_bfloat162 b2 = __floats2bfloat162_rn(acc[i] * inv, acc[i + 1] * inv);
-    *reinterpret_cast<__nv_bfloat162*>(orow + i) = b2;
-  }
-}
-
 // ------------------------------------------------------------------ host side
 struct AttnPlan {
   PFN_encodeTiled encode = nullptr;
   int num_sms = 148;
   std::unordered_map<std::string, CUtensorMap> maps;
   bool ready = false;
+  int* flags = nullptr;   // [num_sms] split-unit hand-off flags (zero between launches)
 };
 
 inline bool tc_attn_enabled() { return true; }
 
-// Stream-K (even tile split + merge) vs one CTA per unit: compare rounds of tiles,
-// charging each unit boundary / merge about one tile of fixed cost.
+// Stream-K (even tile split, in-kernel merge of split units) vs one CTA per unit: one
+// CTA per unit whenever the units fit in one wave (nothing to merge), else stream-K
+// (measured: 156 cross-attention units of 4 key tiles 19.1 us stream-K vs 20.6 us in
+// two waves; self-attention 86 vs 135 us).
 inline int attn_pick_per_unit(long long units, long long tiles, int num_sms) {
-  const long long J = units ? (tiles + units - 1) / units : 1;
-  if (J <= 8) return 1;     // short key ranges (cross-attention): merge cost dominates
-  const double per_unit = double((units + num_sms - 1) / num_sms) * double(J + 1);
-  const double streamk = double((tiles + num_sms - 1) / num_sms) + 4.0;
-  return per_unit <= streamk ? 1 : 0;
+  (void)tiles;
+  return units <= num_sms ? 1 : 0;
 }
 
 inline int attn_cluster() {
@@ -744,6 +723,11 @@ inline bool attn_plan_init(AttnPlan& p, PFN_encodeTiled enc, int num_sms) {
   cudaFuncSetAttribute(attn_tc_kernel<128, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, AttnSmem<128>::total);
   cudaFuncSetAttribute(attn_tc_kernel<64, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, AttnSmem<64>::total);
   cudaFuncSetAttribute(attn_tc_kernel<128, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, AttnSmem<128, 2>::total);
+  if (!p.flags) {
+    if (cudaMalloc(&p.flags, size_t(num_sms) * sizeof(int)) != cudaSuccess ||
+        cudaMemset(p.flags, 0, size_t(num_sms) * sizeof(int)) != cudaSuccess)
+      return false;
+  }
   p.ready = true;
   return true;
 }
@@ -779,7 +763,9 @@ inline const CUtensorMap* attn_map(AttnPlan& p, const void* base, long long rows
 // (host estimate of the unit x key-tile space) only sizes the grid: min(SMs, tiles).
 inline bool tc_attention(cudaStream_t s, AttnPlan& p, const void* q, long long q_rows, const void* Kbase,
                          const void* Vbase, long long kv_rows, int d, int hd, long long total_tiles_hint,
-                         const AttnTcArgs& a, const TickDesc* td, std::string* err, bool pdl = false) {
+                         const AttnTcArgs& a_in, const TickDesc* td, std::string* err, bool pdl = false) {
+  AttnTcArgs a = a_in;
+  a.flags = p.flags;
   const CUtensorMap* mq = attn_map(p, q, q_rows, d, kAttnBQ, err);
   const int CL = hd == 128 ? attn_cluster() : 1;
   // pair: K boxes of 64 keys x 64 dims, V boxes of 128 keys x 64 dims (one half each)
@@ -812,22 +798,6 @@ inline bool tc_attention(cudaStream_t s, AttnPlan& p, const void* q, long long q
   else
     e = hd == 128 ? cudaLaunchKernelEx(&cfg, attn_tc_kernel<128, 1>, *mq, *mk, *mv, a, td)
                   : cudaLaunchKernelEx(&cfg, attn_tc_kernel<64, 1>, *mq, *mk, *mv, a, td);
-  if (e == cudaSuccess && !a.per_unit) {
-    cfg.gridDim = dim3(unsigned(units * CL * (kAttnBQ / kAttnCombineRowsPerCTA)));
-    cfg.blockDim = dim3(256);
-    cfg.dynamicSmemBytes = 0;
-    cfg.numAttrs = 0;
-    if (pdl) {
-      cfg.attrs = at + 1;
-      cfg.numAttrs = 1;
-    }
-    if (CL == 2)
-      e = hd == 128 ? cudaLaunchKernelEx(&cfg, attn_combine_kernel<128, 2>, a, td, G)
-                    : cudaErrorInvalidValue;
-    else
-      e = hd == 128 ? cudaLaunchKernelEx(&cfg, attn_combine_kernel<128, 1>, a, td, G)
-                    : cudaLaunchKernelEx(&cfg, attn_combine_kernel<64, 1>, a, td, G);
-  }
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     *err = std::string("attn_tc launch: ") + cudaGetErrorString(e);

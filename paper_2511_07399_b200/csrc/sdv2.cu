@@ -447,7 +447,6 @@ sdv2_status attention(sdv2_handle* h, const AttnArgs& aa, int Mrows_entries, dou
         ta.kv_row0 = bl * h->n * h->S * h->L;
         ta.kv_lane_rows = h->S * h->L;
       }
-      ++h->launches;   // + the combine kernel
       return tc_attention(h->stream, h->aplan, aa.q, h->Mmax, Kb, Vb, kv_rows, h->d, h->hd, tiles, ta, h->td_dev,
                           &h->err, h->pdl) ? SDV2_OK : SDV2_E_CUDA;
     }
