@@ -302,12 +302,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
       int pre = 0;
       GemmSegIter it = segs;
       GemmSeg g0;
-      if (MC == 1 && it.next(g0)) {
+      if (it.next(g0)) {
         const int nb0 = g0.t / num_mg;
         pre = g0.kb1 - g0.kb0 < kStages ? g0.kb1 - g0.kb0 : kStages;
         if (tc::elect_one()) {
           for (int i = 0; i < pre; ++i) {
-            tc::mbar_expect_tx(full + i, bytes);
+            if (cr == 0) tc::mbar_expect_tx(full + i, bytes);   // pair: the even CTA counts both
             load_w(i, g0.kb0 + i, nb0);
           }
         }
