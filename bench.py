@@ -304,7 +304,9 @@ def run_ours(args, cfg):
                 "share_of_step": p["ms"] / (prof_steps * statistics.mean(step_ms)),
                 "classes": {k: {"ms_per_step": v["ms"] / prof_steps,
                                 "tflops": (v["flops"] / (v["ms"] / 1e3) / 1e12) if v["ms"] > 0 else None}
-                            for k, v in prof.items() if v["launches"]}}
+                            for k, v in prof.items() if v["launches"] and k in ("gemm", "self_attn", "cross_attn")},
+                "block_ms": prof["blocks"]["ms"] / max(1, prof["blocks"]["launches"]),
+                "stage_extras_ms_per_step": prof["stage_extras"]["ms"] / prof_steps}
     # ---- CPU oracle baseline (bounded sample, rank 0 only)
     cpu = None
     if not args.no_cpu_baseline:

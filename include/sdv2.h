@@ -125,11 +125,16 @@ typedef struct {
 
 /* Per-kernel-class device time (CUDA events around each launch on the handle's
  * stream) and algorithmic work, accumulated while profiling is enabled.
- * Classes: 0 projection GEMMs, 1 self-attention, 2 cross-attention, 3 other. */
+ * Classes: 0 projection GEMMs, 1 self-attention, 2 cross-attention, 3 other,
+ * 4 whole DiT blocks (one span per local block and call: the per-block stage time the
+ * partition balances), 5 stage extras outside the blocks (rank 0: noise
+ * controller + patch / time embedding; last rank: head + x0 + output).  Spans of
+ * classes 4/5 contain the launches of classes 0-3. */
+#define SDV2_PROFILE_CLASSES 6
 typedef struct {
-  int64_t launches[4];
-  double ms[4];
-  double flops[4];
+  int64_t launches[SDV2_PROFILE_CLASSES];
+  double ms[SDV2_PROFILE_CLASSES];
+  double flops[SDV2_PROFILE_CLASSES];
 } sdv2_profile;
 
 /* Cache metadata of one (local block, lane) after the last call (test introspection). */

@@ -634,6 +634,7 @@ sdv2_status tick_body(sdv2_handle* h, int na, int par) {
   const int rows = na * h->L;
   const bool first = h->rank == 0, last = h->rank == h->K - 1;
   if (first) {
+    ProfScope ps(h, 5, 0.0);
     // motion-aware noise controller then the step-0 blend on all SMs
     launch_k(h->pdl, motion_kernel, dim3(1), dim3(1024), 0, h->stream, h->lat_in, h->prev_frame, h->ctrl, h->st.sig, h->st.sign, h->td_dev,
                                             h->scfg, h->CTHW, h->hh * h->ww, h->T);
@@ -671,10 +672,14 @@ sdv2_status tick_body(sdv2_handle* h, int na, int par) {
   } else {
     CK(cudaMemcpyAsync(h->packet_base, h->act_io[0][par], h->st.bytes, cudaMemcpyDeviceToDevice, h->stream));
   }
-  for (int b = 0; b < h->nb; ++b) TRY(run_block<TA>(h, b, rows, na));
+  for (int b = 0; b < h->nb; ++b) {
+    ProfScope ps(h, 4, 0.0);
+    TRY(run_block<TA>(h, b, rows, na));
+  }
   if (!last) {
     CK(cudaMemcpyAsync(h->act_io[1][par], h->packet_base, h->st.bytes, cudaMemcpyDeviceToDevice, h->stream));
   } else {
+    ProfScope ps(h, 5, 0.0);
     // head (C.7): a = N(x)(1 + mod_h[1] + e) + mod_h[0] + e; y = a W_h^T + b_h (fp32 out);
     // then unpatchify + x0 + output / re-noise (C.8, O5)
     ModArgs m{};

@@ -131,9 +131,11 @@ def stage_io_tensors(stage, workspace):
     return io
 
 
-def run_pipelined(stage, transport: StageTransport, chunks, out_cb, num_calls: int, on_call=None):
+def run_pipelined(stage, transport: StageTransport, chunks, out_cb, num_calls: int, on_call=None, after_call=None):
     """Drive num_calls stage-ticks on this rank.  chunks(c) -> device/host pointer of the
-    chunk admitted at call c (rank 0 only); out_cb(c) -> output pointer (last rank)."""
+    chunk admitted at call c (rank 0 only); out_cb(c) -> output pointer (last rank).
+    on_call(c) runs before call c (its inputs already ordered on the stage stream, no
+    transport op outstanding); after_call(c, out_chunk) right after it is enqueued."""
     import contextlib
     stream = getattr(stage, "stream", None)
     ctx = transport.torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()
@@ -147,6 +149,8 @@ def run_pipelined(stage, transport: StageTransport, chunks, out_cb, num_calls: i
             oc = stage.denoise_chunk(chunks(c) if transport.rank == 0 else None,
                                      out_cb(c) if transport.rank == transport.world - 1 else None)
             outs.append(oc)
+            if after_call:
+                after_call(c, oc)
             transport.post(c, num_calls)
         transport.wait()
     return outs
@@ -161,62 +165,255 @@ def balanced_ranges(num_blocks: int, world: int, block_ms: float, first_extra_ms
 
 
 # ------------------------------------------------------------------------- bench
+def _pp_backend():
+    """NCCL over NVLink for the real multi-GPU run.  SDV2_PP_BACKEND=gloo moves the same
+    packets through host staging, so the bench logic runs with several ranks on one GPU."""
+    return os.environ.get("SDV2_PP_BACKEND", "nccl")
+
+
+def _gather(dist, vals, backend):
+    """all_gather of a small float vector (one row per rank)."""
+    import torch
+    dev = "cuda" if backend == "nccl" else "cpu"
+    t = torch.tensor(vals, dtype=torch.float64, device=dev)
+    out = [torch.empty_like(t) for _ in range(dist.get_world_size())]
+    dist.all_gather(out, t)
+    return [o.cpu().tolist() for o in out]
+
+
+def _stage_weights(md, blocks, device):
+    """Seeded weights of the global tensors + this stage's blocks, generated straight onto
+    the GPU tensor by tensor for large models (no full fp32 host copy)."""
+    import torch
+    import synthgen as sg
+    from concurrent.futures import ThreadPoolExecutor
+    names = [n for n in sg.all_tensor_names(md)
+             if not n.startswith("blocks.") or int(n.split(".")[1]) in set(blocks)]
+    big = md.dim >= 4096
+
+    def one(n):
+        a = sg.gen_tensor(md, n, 0)
+        return torch.from_numpy(a).to(device) if big else a
+
+    with ThreadPoolExecutor(max_workers=8) as ex:
+        return dict(zip(names, ex.map(one, names)))
+
+
 def run_pipeline_bench(args, cfg):
-    """bench.py --gpus N under torchrun: one rank per GPU, NCCL over NVLink."""
+    """bench.py --gpus N under torchrun: one rank per GPU, blocks split by the exact
+    min-max partition of MEASURED per-block and stage-extra times, stage
+    packets moved with NCCL send/recv over NVLink.  One continuous stream of calls:
+      calibration (provisional uniform split, per-class event profile) -> re-partition
+      -> fill (TTFF) -> warm-up -> timed (device-resident inputs; barrier + sync on both
+      sides; max over ranks) -> e2e (pinned host chunk in on rank 0, host out on the last
+      rank) -> per-kernel-class profile."""
     import torch
     import torch.distributed as dist
     import synthgen as sg
     from . import build as B
     from .sdv2 import SDV2_BF16, Stage
+    sys_path_root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    import sys
+    if sys_path_root not in sys.path:
+        sys.path.insert(0, sys_path_root)
+    from bench import ClockSampler, METRIC, chunk_frames_px, measured_peaks
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    backend = _pp_backend()
+    dev_index = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev_index)
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev_index}"))
+    else:
+        dist.init_process_group("gloo")
+    host_staging = backend != "nccl"
     if local == 0:
         B.build()
     dist.barrier()
     md, g, sd = cfg.model, cfg.geom, cfg.stream
     if world > md.num_blocks:
         raise SystemExit("more stages than DiT blocks")
-    # Stage split: blocks are shape-identical, so one measured block time; extras of the
-    # first / last stage (controller, embeddings / head) are small at these shapes.
-    ranges, _ = balanced_ranges(md.num_blocks, world, 1.0, 0.05, 0.05)
-    b0, b1 = ranges[rank]
-    W = sg.gen_weights(md, seed=0, blocks=range(b0, b1))
-    stage = Stage(md, g, W, precision=SDV2_BF16, pipeline=(world, rank, b0, b1), device=local)
-    del W
-    io = stage_io_tensors(stage, stage.workspace)
-    tr = StageTransport(rank, world, io)
-    stage.reset_stream(sd, sg.gen_prompt(md, 0))
+    n, K = g.steps, world
     ls = sg.LatentStream(md.latent_channels, g.latent_h, g.latent_w, seed=1)
     R = 16
-    dev_chunks = [torch.from_numpy(ls.chunk(X, g.chunk_frames)).cuda() for X in range(R)]
-    out_dev = torch.empty(dev_chunks[0].shape, dtype=torch.float32, device="cuda")
-    fill = g.steps * world
-    # warm-up (fills the pipeline, includes TTFF ticks)
-    run_pipelined(stage, tr, lambda c: dev_chunks[c % R].data_ptr(), lambda c: out_dev.data_ptr(),
-                  fill + args.warmup)
-    torch.cuda.synchronize()
+    host_chunks = [ls.chunk(X, g.chunk_frames) for X in range(R)]
+    dev_chunks = [torch.from_numpy(c).to(f"cuda:{dev_index}") for c in host_chunks]
+    out_dev = torch.empty(dev_chunks[0].shape, dtype=torch.float32, device=f"cuda:{dev_index}")
+    prompt = sg.gen_prompt(md, 0)
+    fill = n * K
+
+    def make_stage(ranges):
+        b0, b1 = ranges[rank]
+        W = _stage_weights(md, range(b0, b1), f"cuda:{dev_index}")
+        st = Stage(md, g, W, precision=SDV2_BF16, pipeline=(world, rank, b0, b1), device=dev_index)
+        del W
+        torch.cuda.empty_cache()
+        st.reset_stream(sd, prompt)
+        tr = StageTransport(rank, world, stage_io_tensors(st, st.workspace), host_staging=host_staging,
+                            device=dev_index)
+        return st, tr
+
+    def ptr_in(c):
+        return dev_chunks[c % R].data_ptr()
+
+    # ---- calibration on a provisional uniform split (P:231-233: balance by measured time)
+    ranges0, _ = balanced_ranges(md.num_blocks, world, 1.0, 0.0, 0.0)
+    stage, tr = make_stage(ranges0)
+    cal_calls = fill + 6
+
+    def cal_on(c):
+        if c == fill:
+            stage.profile_enable(True)
+
+    run_pipelined(stage, tr, ptr_in, lambda c: out_dev.data_ptr(), cal_calls, on_call=cal_on)
+    prof = stage.profile_read()
+    stage.profile_enable(False)
+    ncal = cal_calls - fill
+    nbl = ranges0[rank][1] - ranges0[rank][0]
+    blk = prof["blocks"]["ms"] / max(1, prof["blocks"]["launches"])
+    ext = prof["stage_extras"]["ms"] / ncal
+    rows = _gather(dist, [blk, ext, nbl], backend)
+    block_ms = sum(r[0] for r in rows) / world
+    first_extra, last_extra = rows[0][1], rows[-1][1]
+    ranges, stage_max = balanced_ranges(md.num_blocks, world, block_ms, first_extra, last_extra)
+    balance = {"block_ms": block_ms, "first_extra_ms": first_extra, "last_extra_ms": last_extra,
+               "provisional": ranges0, "predicted_stage_ms": stage_max}
+    if ranges != ranges0:
+        stage.close()
+        del stage, tr
+        torch.cuda.empty_cache()
+        stage, tr = make_stage(ranges)
+    else:
+        stage.reset_stream(sd, prompt)
+        tr = StageTransport(rank, world, stage_io_tensors(stage, stage.workspace), host_staging=host_staging,
+                            device=dev_index)
+    stream = stage.stream
     dist.barrier()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record()
-    outs = run_pipelined(stage, tr, lambda c: dev_chunks[c % R].data_ptr(), lambda c: out_dev.data_ptr(),
-                         args.steps)
-    ev1.record()
-    torch.cuda.synchronize()
-    ms = torch.tensor([ev0.elapsed_time(ev1)], device="cuda")
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+
+    # ---- one continuous run: fill (TTFF) | warm-up | timed | e2e | profile
+    c_t = fill + args.warmup
+    c_e = c_t + args.steps
+    e2e_steps = max(8, min(args.steps, 64))
+    c_p = c_e + e2e_steps
+    prof_steps = max(4, min(args.steps, 32))
+    total = c_p + prof_steps
+    pin_in = [torch.from_numpy(h).pin_memory() for h in host_chunks]
+    pin_out = torch.empty(host_chunks[0].shape, dtype=torch.float32).pin_memory()
+
+    def ev():
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(stream)
+        return e
+
+    T = {"first_out": None, "steps": []}
+    clk = ClockSampler(dev_index)
+    launches = [0, 0]
+
+    def sync_barrier():
+        torch.cuda.synchronize(dev_index)
+        dist.barrier()
+
+    def on_call(c):
+        if c == 0:
+            sync_barrier()
+            T["t0"] = ev()
+        elif c == c_t:
+            sync_barrier()
+            clk.start()
+            launches[0] = stage.tick_info()["kernel_launches"]
+            T["ta"] = ev()
+            T["prev"] = T["ta"]
+        elif c == c_e:
+            T["tb"] = ev()
+            launches[1] = stage.tick_info()["kernel_launches"]
+            sync_barrier()
+            T["clocks"] = clk.stop()
+            T["ea"] = ev()
+        elif c == c_p:
+            T["eb"] = ev()
+            sync_barrier()
+            stage.profile_enable(True)
+
+    def after_call(c, oc):
+        if oc >= 0 and T["first_out"] is None:
+            T["first_out"] = ev()
+        if c_t <= c < c_e:
+            e = ev()
+            T["steps"].append((T["prev"], e))
+            T["prev"] = e
+
+    def chunk_ptr(c):
+        return pin_in[c % R].data_ptr() if c_e <= c < c_p else ptr_in(c)
+
+    def out_ptr(c):
+        return pin_out.data_ptr() if c_e <= c < c_p else out_dev.data_ptr()
+
+    outs = run_pipelined(stage, tr, chunk_ptr, out_ptr, total, on_call=on_call, after_call=after_call)
+    torch.cuda.synchronize(dev_index)
+    prof = stage.profile_read()
+    stage.profile_enable(False)
+    timed_ms = T["ta"].elapsed_time(T["tb"])
+    e2e_ms = T["ea"].elapsed_time(T["eb"])
+    ttff = T["t0"].elapsed_time(T["first_out"]) if T["first_out"] is not None else -1.0
+    step_ms = [a.elapsed_time(b) for a, b in T["steps"]]
+    outs_timed = sum(1 for c in range(c_t, c_e) if outs[c] >= 0)
+    outs_e2e = sum(1 for c in range(c_e, c_p) if outs[c] >= 0)
+    clocks = T["clocks"]
+    reasons = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    mine = [timed_ms, e2e_ms, ttff, float(outs_timed), float(outs_e2e), float(launches[1] - launches[0]),
+            float(clocks.get("sm_mhz") or 0.0), float(clocks.get("sm_max_mhz") or 0.0),
+            prof["gemm"]["ms"], prof["gemm"]["flops"], prof["gemm"]["launches"],
+            prof["self_attn"]["ms"], prof["self_attn"]["flops"], prof["cross_attn"]["ms"],
+            prof["cross_attn"]["flops"]] + [1.0 if r in clocks.get("reasons", []) else 0.0 for r in reasons]
+    allr = _gather(dist, mine, backend)
+    steps_all = _gather(dist, step_ms, backend)
     dist.barrier()
-    total_ms = ms.item()
     if rank == 0:
-        chunks_out = args.steps            # one clean chunk per stage-tick in steady state
-        value = 4 * g.chunk_frames * chunks_out / (total_ms / 1e3)
-        print(json.dumps({
-            "metric": "output FPS, TTFF and p99 chunk latency at 1/2/4/8 B200; GEMM tensor-pipe %",
-            "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": cfg.name, "parallelism": f"pp{world}", "block_ranges": ranges}}))
+        max_ms = max(r[0] for r in allr)
+        max_e2e = max(r[1] for r in allr)
+        last = allr[-1]
+        px = chunk_frames_px(cfg)
+        value = px * last[3] / (max_ms / 1e3)
+        tick = [max(col) for col in zip(*steps_all)]
+        lat = [sum(tick[i:i + n * K]) for i in range(0, len(tick) - n * K + 1)]
+        peaks, src = measured_peaks()
+        gm = max(r[8] for r in allr)          # slowest rank's GEMM class (kernels only)
+        gr = max(range(world), key=lambda i: allr[i][8])
+        g_ms, g_fl, g_n = allr[gr][8], allr[gr][9], allr[gr][10]
+        achieved = g_fl / (g_ms / 1e3) / 1e12 if g_ms > 0 else 0.0
+        peak = peaks["bf16_tflops_sustained"]
+        res = {
+            "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": cfg.name, "latent": [md.latent_channels, g.chunk_frames, g.latent_h, g.latent_w],
+                       "tokens_per_chunk": g.tokens_per_chunk(md), "steps_n": n, "sink_chunks": g.sink_chunks,
+                       "window_chunks": g.window_chunks, "blocks": md.num_blocks, "dim": md.dim,
+                       "parallelism": f"pp{world}", "transport": backend, "block_ranges": ranges,
+                       "balance": balance, "px_frames_per_chunk": px,
+                       "l2": "per-step working set >> L2 (stage weights + KV lanes streamed each step)"},
+            "latent_chunks_per_s": last[3] / (max_ms / 1e3),
+            "ttff_ms": last[2],
+            "ttff_with_buffering_ms": {"16fps": last[2] + 1e3 * px / 16.0, "30fps": last[2] + 1e3 * px / 30.0},
+            "latency_ms": {"p50": float(np.percentile(lat, 50)), "p99": float(np.percentile(lat, 99)),
+                           "max": float(np.max(lat)), "definition": f"sum of {n * K} consecutive stage-ticks "
+                           "(per-tick time = max over ranks)"} if lat else None,
+            "e2e": {"value": px * last[4] / (max_e2e / 1e3), "unit": "frames/s",
+                    "h2d_bytes_per_step": host_chunks[0].nbytes, "d2h_bytes_per_step": host_chunks[0].nbytes},
+            "gpu_launches": int(sum(r[5] for r in allr)),
+            "roofline": {"bound": "tensor", "kernel": "gemm", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "peak_source": f"{src} bf16_tflops_sustained",
+                         "per_launch_ms": g_ms / max(1, g_n), "flops_per_launch": g_fl / max(1, g_n),
+                         "rank": gr, "note": "projection GEMMs of the slowest stage, per-launch CUDA events"},
+            "cpu_baseline": None,
+            "clocks": {"sm_mhz": statistics.median([r[6] for r in allr]), "sm_max_mhz": max(r[7] for r in allr),
+                       "reasons": [reasons[i] for i in range(4) if any(r[15 + i] for r in allr)],
+                       "per_rank_sm_mhz": [r[6] for r in allr]},
+        }
+        del gm
+        print(json.dumps(res))
     stage.close()
+    dist.barrier()
     dist.destroy_process_group()

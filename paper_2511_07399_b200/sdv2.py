@@ -64,7 +64,7 @@ class TickInfoC(ctypes.Structure):
 
 
 class ProfileC(ctypes.Structure):
-    _fields_ = [("launches", ctypes.c_int64 * 4), ("ms", ctypes.c_double * 4), ("flops", ctypes.c_double * 4)]
+    _fields_ = [("launches", ctypes.c_int64 * 6), ("ms", ctypes.c_double * 6), ("flops", ctypes.c_double * 6)]
 
 
 class CacheStateC(ctypes.Structure):
@@ -316,8 +316,8 @@ class Stage:
     def profile_read(self):
         p = ProfileC()
         _check(self.L.sdv2_profile_read(self.h, ctypes.byref(p)), self.h)
-        names = ("gemm", "self_attn", "cross_attn", "other")
-        return {names[i]: {"launches": p.launches[i], "ms": p.ms[i], "flops": p.flops[i]} for i in range(4)}
+        names = ("gemm", "self_attn", "cross_attn", "other", "blocks", "stage_extras")
+        return {names[i]: {"launches": p.launches[i], "ms": p.ms[i], "flops": p.flops[i]} for i in range(6)}
 
     def stage_io(self, parity: int):
         io = StageIOC()
