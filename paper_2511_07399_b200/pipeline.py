@@ -44,6 +44,7 @@ class StageTransport:
         self.device = device
         self.pending = []
         self._stage = {}
+        self.base = 0                   # stage calls made before the current run (buffer parity)
 
     def _buf(self, t):
         """Tensor used on the wire (a host copy when staging through the host)."""
@@ -60,7 +61,7 @@ class StageTransport:
         K, r = self.world, self.rank
         ops, post = [], []
         if c >= 0:
-            cur = self.io(c & 1)
+            cur = self.io((self.base + c) & 1)
             if r < K - 1 and cur["act_out"].numel():
                 src = cur["act_out"]
                 wire = self._buf(src)
@@ -74,7 +75,7 @@ class StageTransport:
                 if wire is not src:
                     wire.copy_(src)
                 ops.append(dist.P2POp(dist.isend, wire, 0))
-        nxt = self.io((c + 1) & 1)
+        nxt = self.io((self.base + c + 1) & 1)
         if c + 1 >= num_calls:
             return ops, post
         if r > 0 and nxt["act_in"].numel():
@@ -135,8 +136,15 @@ def run_pipelined(stage, transport: StageTransport, chunks, out_cb, num_calls: i
     """Drive num_calls stage-ticks on this rank.  chunks(c) -> device/host pointer of the
     chunk admitted at call c (rank 0 only); out_cb(c) -> output pointer (last rank).
     on_call(c) runs before call c (its inputs already ordered on the stage stream, no
-    transport op outstanding); after_call(c, out_chunk) right after it is enqueued."""
+    transport op outstanding); after_call(c, out_chunk) right after it is enqueued.
+
+    Every transfer of a run is matched inside the run, so the pipeline is drained when
+    it returns (a barrier between runs is safe; a barrier inside one would deadlock:
+    rank s waits for rank s-1's call c before its own call c).  Ring-closure packets
+    whose consumer call lies beyond the run are not sent; rank 0 then re-noises from
+    its previous ring buffer (timing-equivalent; numerics tests use one run)."""
     import contextlib
+    transport.base = getattr(stage, "calls", 0)
     stream = getattr(stage, "stream", None)
     ctx = transport.torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()
     with ctx:   # NCCL waits and host-staging copies are ordered on the stage's stream
@@ -260,16 +268,13 @@ def run_pipeline_bench(args, cfg):
     # ---- calibration on a provisional uniform split (balance by measured time)
     ranges0, _ = balanced_ranges(md.num_blocks, world, 1.0, 0.0, 0.0)
     stage, tr = make_stage(ranges0)
-    cal_calls = fill + 6
-
-    def cal_on(c):
-        if c == fill:
-            stage.profile_enable(True)
-
-    run_pipelined(stage, tr, ptr_in, lambda c: out_dev.data_ptr(), cal_calls, on_call=cal_on)
+    run_pipelined(stage, tr, ptr_in, lambda c: out_dev.data_ptr(), fill)
+    ncal = 6
+    stage.profile_enable(True)
+    base = stage.calls
+    run_pipelined(stage, tr, lambda c: ptr_in(base + c), lambda c: out_dev.data_ptr(), ncal)
     prof = stage.profile_read()
     stage.profile_enable(False)
-    ncal = cal_calls - fill
     nbl = ranges0[rank][1] - ranges0[rank][0]
     blk = prof["blocks"]["ms"] / max(1, prof["blocks"]["launches"])
     ext = prof["stage_extras"]["ms"] / ncal
@@ -291,13 +296,9 @@ def run_pipeline_bench(args, cfg):
     stream = stage.stream
     dist.barrier()
 
-    # ---- one continuous run: fill (TTFF) | warm-up | timed | e2e | profile
-    c_t = fill + args.warmup
-    c_e = c_t + args.steps
-    e2e_steps = max(8, min(args.steps, 64))
-    c_p = c_e + e2e_steps
-    prof_steps = max(4, min(args.steps, 32))
-    total = c_p + prof_steps
+    # ---- phases, each a drained run bracketed by sync + barrier:
+    #      fill (TTFF) + warm-up | timed (device-resident inputs) | e2e (pinned host in /
+    #      out) | per-kernel-class profile
     pin_in = [torch.from_numpy(h).pin_memory() for h in host_chunks]
     pin_out = torch.empty(host_chunks[0].shape, dtype=torch.float32).pin_memory()
 
@@ -306,62 +307,62 @@ def run_pipeline_bench(args, cfg):
         e.record(stream)
         return e
 
-    T = {"first_out": None, "steps": []}
-    clk = ClockSampler(dev_index)
-    launches = [0, 0]
-
     def sync_barrier():
         torch.cuda.synchronize(dev_index)
         dist.barrier()
 
-    def on_call(c):
-        if c == 0:
-            sync_barrier()
-            T["t0"] = ev()
-        elif c == c_t:
-            sync_barrier()
-            clk.start()
-            launches[0] = stage.tick_info()["kernel_launches"]
-            T["ta"] = ev()
-            T["prev"] = T["ta"]
-        elif c == c_e:
-            T["tb"] = ev()
-            launches[1] = stage.tick_info()["kernel_launches"]
-            sync_barrier()
-            T["clocks"] = clk.stop()
-            T["ea"] = ev()
-        elif c == c_p:
-            T["eb"] = ev()
-            sync_barrier()
-            stage.profile_enable(True)
+    def dev_out(c):
+        return out_dev.data_ptr()
 
-    def after_call(c, oc):
+    T = {"first_out": None}
+
+    def first_out(c, oc):
         if oc >= 0 and T["first_out"] is None:
             T["first_out"] = ev()
-        if c_t <= c < c_e:
-            e = ev()
-            T["steps"].append((T["prev"], e))
-            T["prev"] = e
 
-    def chunk_ptr(c):
-        return pin_in[c % R].data_ptr() if c_e <= c < c_p else ptr_in(c)
+    sync_barrier()
+    t0 = ev()
+    run_pipelined(stage, tr, ptr_in, dev_out, fill + args.warmup, after_call=first_out)
+    sync_barrier()
+    ttff = t0.elapsed_time(T["first_out"]) if T["first_out"] is not None else -1.0
 
-    def out_ptr(c):
-        return pin_out.data_ptr() if c_e <= c < c_p else out_dev.data_ptr()
+    base = stage.calls
+    step_ev = []
+    clk = ClockSampler(dev_index)
+    clk.start()
+    l0 = stage.tick_info()["kernel_launches"]
+    sync_barrier()
+    ta = ev()
+    outs = run_pipelined(stage, tr, lambda c: ptr_in(base + c), dev_out, args.steps,
+                         after_call=lambda c, oc: step_ev.append(ev()))
+    tb = ev()
+    sync_barrier()
+    clocks = clk.stop()
+    launches = stage.tick_info()["kernel_launches"] - l0
+    timed_ms = ta.elapsed_time(tb)
+    step_ms = [a.elapsed_time(b) for a, b in zip([ta] + step_ev[:-1], step_ev)]
+    outs_timed = sum(1 for oc in outs if oc >= 0)
 
-    outs = run_pipelined(stage, tr, chunk_ptr, out_ptr, total, on_call=on_call, after_call=after_call)
+    e2e_steps = max(8, min(args.steps, 64))
+    base = stage.calls
+    sync_barrier()
+    ea = ev()
+    outs_e = run_pipelined(stage, tr, lambda c: pin_in[(base + c) % R].data_ptr(), lambda c: pin_out.data_ptr(),
+                           e2e_steps)
+    eb = ev()
+    sync_barrier()
+    e2e_ms = ea.elapsed_time(eb)
+    outs_e2e = sum(1 for oc in outs_e if oc >= 0)
+
+    prof_steps = max(4, min(args.steps, 32))
+    base = stage.calls
+    stage.profile_enable(True)
+    run_pipelined(stage, tr, lambda c: ptr_in(base + c), dev_out, prof_steps)
     torch.cuda.synchronize(dev_index)
     prof = stage.profile_read()
     stage.profile_enable(False)
-    timed_ms = T["ta"].elapsed_time(T["tb"])
-    e2e_ms = T["ea"].elapsed_time(T["eb"])
-    ttff = T["t0"].elapsed_time(T["first_out"]) if T["first_out"] is not None else -1.0
-    step_ms = [a.elapsed_time(b) for a, b in T["steps"]]
-    outs_timed = sum(1 for c in range(c_t, c_e) if outs[c] >= 0)
-    outs_e2e = sum(1 for c in range(c_e, c_p) if outs[c] >= 0)
-    clocks = T["clocks"]
     reasons = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-    mine = [timed_ms, e2e_ms, ttff, float(outs_timed), float(outs_e2e), float(launches[1] - launches[0]),
+    mine = [timed_ms, e2e_ms, ttff, float(outs_timed), float(outs_e2e), float(launches),
             float(clocks.get("sm_mhz") or 0.0), float(clocks.get("sm_max_mhz") or 0.0),
             prof["gemm"]["ms"], prof["gemm"]["flops"], prof["gemm"]["launches"],
             prof["self_attn"]["ms"], prof["self_attn"]["flops"], prof["cross_attn"]["ms"],
@@ -375,7 +376,9 @@ def run_pipeline_bench(args, cfg):
         last = allr[-1]
         px = chunk_frames_px(cfg)
         value = px * last[3] / (max_ms / 1e3)
-        tick = [max(col) for col in zip(*steps_all)]
+        # rank s starts s ticks late (pipeline refill after the barrier): per-tick time
+        # = max over ranks, aligned on the global tick, the refill ticks dropped
+        tick = [max(col) for col in zip(*[r[K - 1 - i:len(r) - i] for i, r in enumerate(steps_all)])]
         lat = [sum(tick[i:i + n * K]) for i in range(0, len(tick) - n * K + 1)]
         peaks, src = measured_peaks()
         gm = max(r[8] for r in allr)          # slowest rank's GEMM class (kernels only)
@@ -394,6 +397,9 @@ def run_pipeline_bench(args, cfg):
                        "balance": balance, "px_frames_per_chunk": px,
                        "l2": "per-step working set >> L2 (stage weights + KV lanes streamed each step)"},
             "latent_chunks_per_s": last[3] / (max_ms / 1e3),
+            "steady_state": {"tick_ms_median": float(np.median(tick)) if tick else None,
+                             "frames_per_s": px * 1e3 / float(np.median(tick)) if tick else None,
+                             "note": f"value includes the {K - 1}-tick refill after the opening barrier"},
             "ttff_ms": last[2],
             "ttff_with_buffering_ms": {"16fps": last[2] + 1e3 * px / 16.0, "30fps": last[2] + 1e3 * px / 30.0},
             "latency_ms": {"p50": float(np.percentile(lat, 50)), "p99": float(np.percentile(lat, 99)),

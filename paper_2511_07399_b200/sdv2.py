@@ -285,6 +285,7 @@ class Stage:
                         sd.s_max, sd.ema_lambda, sd.sink_tau, sd.seed)
         p = np.ascontiguousarray(prompt, dtype=np.float32)
         _check(self.L.sdv2_reset_stream(self.h, ctypes.byref(c), ctypes.c_void_p(p.ctypes.data)), self.h)
+        self.calls = 0
 
     def set_prompt(self, prompt: np.ndarray):
         p = np.ascontiguousarray(prompt, dtype=np.float32)
@@ -299,6 +300,7 @@ class Stage:
             self.stream.wait_stream(cur)
         _check(self.L.sdv2_denoise_chunk(self.h, ctypes.c_void_p(chunk_ptr) if chunk_ptr else None,
                                          ctypes.c_void_p(out_ptr) if out_ptr else None, ctypes.byref(oc)), self.h)
+        self.calls = getattr(self, "calls", 0) + 1
         return oc.value
 
     def tick_info(self):
