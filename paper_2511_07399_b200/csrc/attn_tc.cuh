@@ -220,6 +220,17 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
   float* xm = reinterpret_cast<float*>(bar + 32);   // [2 tile parity][2 halves][128] row-max exchange
   float* xl = xm + 512;                             // [2 halves][128] row-sum exchange at segment end
 
+  // test hook: CTA-level wall stamps (globaltimer ns) [4096 + cta * 4 + {0 entry, 1 set up,
+  // 2 first S issued, 3 exit}]
+#define ATTN_CTA_STAMP(ev)                                                                  \
+  do {                                                                                      \
+    if (a.trace != nullptr && blockIdx.x < 1024) {                                          \
+      unsigned long long t_;                                                                \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                \
+      a.trace[4096 + blockIdx.x * 4 + (ev)] = (long long)t_;                                \
+    }                                                                                       \
+  } while (0)
+  if (threadIdx.x == 0) ATTN_CTA_STAMP(0);
   pdl_wait();      // q, K/V lanes and o are produced / consumed by the neighbouring kernels
   pdl_trigger();
   AttnGeo geo;
@@ -270,6 +281,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
   if (CL > 1) tc::cluster_sync();   // peer barriers initialised before any remote arrive
   else __syncthreads();
   tc::tc_fence_after();
+  if (threadIdx.x == 0) ATTN_CTA_STAMP(1);
   const uint32_t tmem = *tmem_slot;
   // TMEM: O (HD columns) | S0 | S1 | S2 (128 fp32 columns each, from column 128).  One O
   // accumulator per row: the two softmax warps of a row (key halves) agree on the row
@@ -396,6 +408,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
         const int ks = gg % KS;        // K smem stage
         tc::mbar_wait(k_full + ks, (gg / KS) & 1);
         ATTN_TRACE(3, gg);
+        if (gg == 0 && lane == 0) ATTN_CTA_STAMP(2);
         tc::tc_fence_after();
         const uint32_t ka = tc::smem_u32(sK + ks * SM::KV);
         if (tc::elect_one()) {
@@ -690,6 +703,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
     if (CL > 1) tc::tmem_dealloc_cg2(tmem, 512);
     else tc::tmem_dealloc(tmem, 512);
   }
+  if (threadIdx.x == 0) ATTN_CTA_STAMP(3);
 }
 
 // ------------------------------------------------------------------ host side

@@ -44,6 +44,16 @@ constexpr int kResMaxBN = 192;   // residual epilogues: keep >= 3 stages next to
 
 // Pipeline trace (test hook): event `ev` of k-block / tile index `i` of CTA 0 and 1
 // (CTA 1 at +4096): [i * 8 + ev], i < 512.
+// CTA wall stamps (globaltimer ns, test hook): [8192 + cta * 4 + {0 entry, 1 set up,
+// 2 first tile's accumulator complete (epilogue saw it), 3 exit}].
+#define GEMM_CTA_STAMP(ev)                                                              \
+  do {                                                                                  \
+    if (ep.trace != nullptr && blockIdx.x < 1024) {                                     \
+      unsigned long long t_;                                                            \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                            \
+      ep.trace[8192 + blockIdx.x * 4 + (ev)] = (long long)t_;                           \
+    }                                                                                   \
+  } while (0)
 #define GEMM_TRACE(ev, i)                                                               \
   do {                                                                                  \
     if (ep.trace != nullptr && blockIdx.x < 2 && (i) < 512)                             \
@@ -251,7 +261,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
   const uint16_t mc_mask = uint16_t((1u << MC) - 1);
   GemmSegIter segs;
   segs.init(sk.on, kblocks, tiles, cid, ncl);
-  if (threadIdx.x == 0) pdl_trigger();
+  if (threadIdx.x == 0) {
+    GEMM_CTA_STAMP(0);
+    pdl_trigger();
+  }
 
   if (warp == 0 && lane == 0) {
     tc::tma_prefetch_desc(&tmA);
@@ -276,6 +289,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
   if (MC > 1) tc::cluster_sync();   // peer barriers initialised before any multicast
   else __syncthreads();
   tc::tc_fence_after();
+  if (threadIdx.x == 0) GEMM_CTA_STAMP(1);
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
@@ -445,6 +459,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
       asm volatile("bar.sync 3, 256;" ::: "memory");
       tc::mbar_wait(tfull + acc, acc_phase);
       if (warp == 4 && lane == 0) GEMM_TRACE(4, nt);
+      if (warp == 4 && lane == 0 && nt == 0) GEMM_CTA_STAMP(2);
       tc::tc_fence_after();
       const int r = mb * kGemmBM + row;
       const float* gsm = sGate + ((r < M ? r : M - 1) / ep.L > e_lo ? kGemmMaxBN : 0);
@@ -586,6 +601,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
     if (MC > 1) tc::tmem_dealloc_cg2(tmem, 512);
     else tc::tmem_dealloc(tmem, 512);
   }
+  if (threadIdx.x == 0) GEMM_CTA_STAMP(3);
 }
 
 // ------------------------------------------------------------------ host side
@@ -824,29 +840,32 @@ inline bool tc_gemm(cudaStream_t s, TmaGemmPlan& p, const void* A, const void* W
   return tc_gemm_cfg(s, p, A, W, M, N, K, epi, ep, gc, err);
 }
 
-// Create-time autotuning of one GEMM shape on the real buffers: the best of
-// {MC = 1, 2} x (the three best tile widths of the balance model, or stream-K at the
-// widest tile), by CUDA-event time.
-inline bool tc_gemm_tune(cudaStream_t s, TmaGemmPlan& p, const void* A, const void* W, int M, int N, int K, int epi,
-                         const EpiArgs& ep, std::string* err) {
+// Create-time autotuning of one GEMM shape on the real buffers: every (MC = 1, 2) x
+// tile width, plus stream-K at the three best tile widths of the balance model, by
+// CUDA-event time.  The timed launches cycle through the weights of the different
+// local blocks (Ws[0..nW)) so, as in a real step, the weights stream from HBM instead
+// of sitting in L2 after the first launch.
+inline bool tc_gemm_tune(cudaStream_t s, TmaGemmPlan& p, const void* A, const void* const* Ws, int nW, int M, int N,
+                         int K, int epi, const EpiArgs& ep, std::string* err) {
   if (!tc_gemm_check(N, K, epi, err)) return false;
   const std::string key = gemm_key(M, N, K, epi);
   if (p.tuned.count(key)) return true;
   const int num_m = (M + kGemmBM - 1) / kGemmBM;
   const bool res = (epi == EPI_RES_GATE || epi == EPI_RES);
   std::vector<GemmCfg> cands;
+  const int max_bn = std::min(res ? kResMaxBN : 256, (N + 31) / 32 * 32);
   for (int MC = 1; MC <= (num_m >= 2 ? 2 : 1); ++MC) {
-    cands.push_back({MC, std::min(res ? kResMaxBN : 256, (N + 31) / 32 * 32), 1});
     std::vector<std::pair<double, int>> ranked;
     const int num_mg = (num_m + MC - 1) / MC, slots = p.num_sms / MC;
-    for (int bn = res ? kResMaxBN : 256; bn >= 64; bn -= 32) {
+    for (int bn = max_bn; bn >= 64; bn -= 32) {
+      cands.push_back({MC, bn, 0});
       const int num_n = (N + bn - 1) / bn, tiles = num_mg * num_n, waves = (tiles + slots - 1) / slots;
       const double eff = double(N) / double(num_n * bn) * double(num_m) / double(num_mg * MC) * double(tiles) /
                          double(waves * slots);
       ranked.push_back({-eff, -bn});
     }
     std::sort(ranked.begin(), ranked.end());
-    for (size_t i = 0; i < ranked.size() && i < 3; ++i) cands.push_back({MC, -ranked[i].second, 0});
+    for (size_t i = 0; i < ranked.size() && i < 2; ++i) cands.push_back({MC, -ranked[i].second, 1});
   }
   cudaEvent_t a, b;
   cudaEventCreate(&a);
@@ -858,11 +877,11 @@ inline bool tc_gemm_tune(cudaStream_t s, TmaGemmPlan& p, const void* A, const vo
   constexpr int kReps = 8;
   for (auto& c : cands) {
     for (int i = 0; i < 2; ++i)
-      if (!tc_gemm_cfg(s, p, A, W, M, N, K, epi, ep, c, err)) return false;
+      if (!tc_gemm_cfg(s, p, A, Ws[i % nW], M, N, K, epi, ep, c, err)) return false;
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     bool ok = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
-    for (int i = 0; ok && i < kReps; ++i) ok = tc_gemm_cfg(s, p, A, W, M, N, K, epi, ep, c, err);
+    for (int i = 0; ok && i < kReps; ++i) ok = tc_gemm_cfg(s, p, A, Ws[i % nW], M, N, K, epi, ep, c, err);
     if (cudaStreamEndCapture(s, &graph) != cudaSuccess || !ok ||
         cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
       if (graph) cudaGraphDestroy(graph);
@@ -878,6 +897,8 @@ inline bool tc_gemm_tune(cudaStream_t s, TmaGemmPlan& p, const void* A, const vo
     cudaEventElapsedTime(&ms, a, b);
     cudaGraphExecDestroy(exec);
     cudaGraphDestroy(graph);
+    if (getenv("SDV2_VERBOSE") && atoi(getenv("SDV2_VERBOSE")) > 1)
+      fprintf(stderr, "  cand MC=%d BN=%d SK=%d %.1f us\n", c.MC, c.BN, c.SK, ms * 1e3f / kReps);
     if (ms < best) {
       best = ms;
       best_cfg = c;

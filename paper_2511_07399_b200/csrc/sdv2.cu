@@ -15,6 +15,7 @@
 #include <cstring>
 #include <string>
 #include <vector>
+#include <map>
 
 #include "../../include/sdv2.h"
 #include "ctl.h"
@@ -895,18 +896,28 @@ sdv2_status sdv2_create(const sdv2_model_desc* md, const sdv2_geometry* g, const
       const int M = na * h->L;
       EpiArgs ep{};
       ep.L = h->L; ep.mod = B.mod; ep.e0 = h->st.e0; ep.gate_row = 2;
-      struct Sh { const void* A; const void* W; int N, K, epi; void* out; int ldo; const float* bias; } shapes[] = {
-          {h->a, B.wqkv, 3 * d, d, EPI_STORE, h->qkv, 3 * d, B.bqkv},
-          {h->o, B.wo, d, d, EPI_RES_GATE, h->st.x, d, B.bo},
-          {h->a, B.wcq, d, d, EPI_STORE, h->q, d, B.bcq},
-          {h->o, B.wco, d, d, EPI_RES, h->st.x, d, B.bco},
-          {h->a, B.w1, h->F, d, EPI_GELU, h->hbuf, h->F, B.b1},
-          {h->hbuf, B.w2, d, h->F, EPI_RES_GATE, h->st.x, d, B.b2},
-          {h->a, h->head_w_tw, h->P, d, EPI_STORE_F32, h->yh, h->P, h->gw[G_HEAD_B]},
+      // weights of every local block (the timed launches cycle through them)
+      const int nW = h->nb;
+      std::vector<const void*> wl[6];
+      for (int b = 0; b < nW; ++b) {
+        const BlockW& Bb = h->bw[b];
+        const void* ws[6] = {Bb.wqkv, Bb.wo, Bb.wcq, Bb.wco, Bb.w1, Bb.w2};
+        for (int k = 0; k < 6; ++k) wl[k].push_back(ws[k]);
+      }
+      const void* head_w[1] = {h->head_w_tw};
+      struct Sh { const void* A; const void* const* W; int nW, N, K, epi; void* out; int ldo; const float* bias; } shapes[] = {
+          {h->a, wl[0].data(), nW, 3 * d, d, EPI_STORE, h->qkv, 3 * d, B.bqkv},
+          {h->o, wl[1].data(), nW, d, d, EPI_RES_GATE, h->st.x, d, B.bo},
+          {h->a, wl[2].data(), nW, d, d, EPI_STORE, h->q, d, B.bcq},
+          {h->o, wl[3].data(), nW, d, d, EPI_RES, h->st.x, d, B.bco},
+          {h->a, wl[4].data(), nW, h->F, d, EPI_GELU, h->hbuf, h->F, B.b1},
+          {h->hbuf, wl[5].data(), nW, d, h->F, EPI_RES_GATE, h->st.x, d, B.b2},
+          {h->a, head_w, 1, h->P, d, EPI_STORE_F32, h->yh, h->P, h->gw[G_HEAD_B]},
       };
       for (auto& sh : shapes) {
         ep.out = sh.out; ep.ldo = sh.ldo; ep.bias = sh.bias;
-        if (!tc_gemm_tune(h->stream, h->gplan, sh.A, sh.W, M, sh.N, sh.K, sh.epi, ep, &h->err)) return fail(SDV2_E_CUDA);
+        if (!tc_gemm_tune(h->stream, h->gplan, sh.A, sh.W, sh.nW, M, sh.N, sh.K, sh.epi, ep, &h->err))
+          return fail(SDV2_E_CUDA);
       }
     }
     if (cudaStreamSynchronize(h->stream) != cudaSuccess) return fail(SDV2_E_CUDA);
@@ -1094,13 +1105,25 @@ sdv2_status sdv2_profile_enable(sdv2_handle* h, int32_t enable) {
 sdv2_status sdv2_profile_read(sdv2_handle* h, sdv2_profile* out) {
   if (!h || !out) return SDV2_E_INVALID;
   CK(cudaStreamSynchronize(h->stream));
+  // SDV2_PROF_DETAIL=1: per (class, work) breakdown on stderr (one line per GEMM shape)
+  const bool detail = getenv("SDV2_PROF_DETAIL") != nullptr;
+  std::map<std::pair<int, double>, std::pair<int, double>> det;
   for (auto& r : h->prof_recs) {
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, r.a, r.b));
     h->prof_acc.launches[r.cls] += 1;
     h->prof_acc.ms[r.cls] += ms;
     h->prof_acc.flops[r.cls] += r.flops;
+    if (detail) {
+      auto& d = det[{r.cls, r.flops}];
+      d.first += 1;
+      d.second += ms;
+    }
   }
+  for (auto& kv : det)
+    fprintf(stderr, "sdv2 prof class %d work %.4g: %d launches, avg %.2f us, %.0f TFLOP/s\n", kv.first.first,
+            kv.first.second, kv.second.first, kv.second.second * 1e3 / kv.second.first,
+            kv.second.first * kv.first.second / (kv.second.second * 1e-3) / 1e12);
   h->prof_recs.clear();
   h->ev_next = 0;
   *out = h->prof_acc;
@@ -1143,13 +1166,23 @@ extern "C" sdv2_status sdv2_debug_gemm(const void* A, const void* W, const float
   // SDV2_GEMM_TRACE=<file>: clock64 stamps of CTAs 0 and 1 (pipeline analysis)
   const char* trace_path = getenv("SDV2_GEMM_TRACE");
   static long long* trace = nullptr;
-  const size_t tn = 2 * 4096;
+  const size_t tn = 2 * 4096 + 1024 * 4;
   if (trace_path) {
     if (!trace && cudaMalloc(&trace, tn * sizeof(long long)) != cudaSuccess) return SDV2_E_CUDA;
     cudaMemsetAsync(trace, 0, tn * sizeof(long long), static_cast<cudaStream_t>(stream));
     ep.trace = trace;
   }
-  if (!tc_gemm(static_cast<cudaStream_t>(stream), plan, A, W, M, N, K, epi, ep, &err)) {
+  // SDV2_GEMM_CFG="MC,BN,SK": explicit configuration (else the default balance model)
+  bool ok;
+  if (const char* cfg = getenv("SDV2_GEMM_CFG")) {
+    GemmCfg gc{1, 128, 0};
+    sscanf(cfg, "%d,%d,%d", &gc.MC, &gc.BN, &gc.SK);
+    ok = tc_gemm_check(N, K, epi, &err) &&
+         tc_gemm_cfg(static_cast<cudaStream_t>(stream), plan, A, W, M, N, K, epi, ep, gc, &err);
+  } else {
+    ok = tc_gemm(static_cast<cudaStream_t>(stream), plan, A, W, M, N, K, epi, ep, &err);
+  }
+  if (!ok) {
     fprintf(stderr, "sdv2_debug_gemm: %s\n", err.c_str());
     return SDV2_E_CUDA;
   }
@@ -1158,9 +1191,14 @@ extern "C" sdv2_status sdv2_debug_gemm(const void* A, const void* W, const float
     cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
     cudaMemcpy(h.data(), trace, tn * sizeof(long long), cudaMemcpyDeviceToHost);
     if (FILE* f = fopen(trace_path, "w")) {
-      for (size_t i = 0; i < tn / 8; ++i) {
+      for (size_t i = 0; i < 8192 / 8; ++i) {
         for (int e = 0; e < 8; ++e) fprintf(f, "%lld%c", h[i * 8 + e], e == 7 ? '\n' : ',');
       }
+      fclose(f);
+    }
+    if (FILE* f = fopen((std::string(trace_path) + ".cta").c_str(), "w")) {
+      for (int t = 0; t < 1024; ++t)
+        for (int e = 0; e < 4; ++e) fprintf(f, "%lld%c", h[8192 + t * 4 + e], e == 3 ? '\n' : ',');
       fclose(f);
     }
   }
@@ -1213,8 +1251,8 @@ extern "C" sdv2_status sdv2_debug_attention(const void* q, const void* K, const 
   const char* trace_path = getenv("SDV2_ATTN_TRACE");
   static long long* trace = nullptr;
   if (trace_path) {
-    if (!trace && cudaMalloc(&trace, 256 * 16 * sizeof(long long)) != cudaSuccess) return SDV2_E_CUDA;
-    cudaMemsetAsync(trace, 0, 256 * 16 * sizeof(long long), s);
+    if (!trace && cudaMalloc(&trace, (256 * 16 + 1024 * 4) * sizeof(long long)) != cudaSuccess) return SDV2_E_CUDA;
+    cudaMemsetAsync(trace, 0, (256 * 16 + 1024 * 4) * sizeof(long long), s);
     ta.trace = trace;
   }
   if (!tc_attention(s, ap, q, Lq, K, V, Lk, H * hd, hd, tiles, ta, static_cast<const TickDesc*>(scratch), &err)) {
@@ -1222,13 +1260,18 @@ extern "C" sdv2_status sdv2_debug_attention(const void* q, const void* K, const 
     return SDV2_E_CUDA;
   }
   if (trace_path) {
-    std::vector<long long> h(256 * 16);
+    std::vector<long long> h(256 * 16 + 1024 * 4);
     cudaStreamSynchronize(s);
     cudaMemcpy(h.data(), trace, h.size() * sizeof(long long), cudaMemcpyDeviceToHost);
     if (FILE* f = fopen(trace_path, "w")) {
       for (int t = 0; t < 256; ++t) {
         for (int e = 0; e < 16; ++e) fprintf(f, "%lld%c", h[t * 16 + e], e == 15 ? '\n' : ',');
       }
+      fclose(f);
+    }
+    if (FILE* f = fopen((std::string(trace_path) + ".cta").c_str(), "w")) {
+      for (int t = 0; t < 1024; ++t)
+        for (int e = 0; e < 4; ++e) fprintf(f, "%lld%c", h[4096 + t * 4 + e], e == 3 ? '\n' : ',');
       fclose(f);
     }
   }
