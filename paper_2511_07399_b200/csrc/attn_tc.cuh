@@ -231,8 +231,6 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
     }                                                                                       \
   } while (0)
   if (threadIdx.x == 0) ATTN_CTA_STAMP(0);
-  pdl_wait();      // q, K/V lanes and o are produced / consumed by the neighbouring kernels
-  pdl_trigger();
   AttnGeo geo;
   geo.init(a, td, CL);
   const int G = gridDim.x / CL, c = blockIdx.x / CL;   // cluster (query-tile group) index
@@ -281,6 +279,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
   if (CL > 1) tc::cluster_sync();   // peer barriers initialised before any remote arrive
   else __syncthreads();
   tc::tc_fence_after();
+  // Barrier init, descriptor prefetch and TMEM allocation above overlap the upstream
+  // kernel's tail (PDL; the upstream is an element-wise kernel that holds no TMEM).
+  pdl_wait();      // q, K/V lanes and o are produced / consumed by the neighbouring kernels
+  pdl_trigger();
   if (threadIdx.x == 0) ATTN_CTA_STAMP(1);
   const uint32_t tmem = *tmem_slot;
   // TMEM: O (HD columns) | S0 | S1 | S2 (128 fp32 columns each, from column 128).  One O

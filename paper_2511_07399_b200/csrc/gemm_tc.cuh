@@ -72,25 +72,33 @@ __device__ __forceinline__ void gemm_epilogue_chunk(const EpiArgs& ep, int r, in
     float acc[32];
     const uint32_t sb = tc::smem_u32(sbias);
 #pragma unroll
-    for (int i = 0; i < 32; i += 4) {
+    for (int i = 0; i < 32; i += 4) {   // bias add on the packed f32x2 pipe
       const float4 b = tc::ld_shared_f4(sb + i * 4);
-      acc[i] = __uint_as_float(v[i]) + b.x;
-      acc[i + 1] = __uint_as_float(v[i + 1]) + b.y;
-      acc[i + 2] = __uint_as_float(v[i + 2]) + b.z;
-      acc[i + 3] = __uint_as_float(v[i + 3]) + b.w;
+      const float2 s0 = __fadd2_rn(make_float2(__uint_as_float(v[i]), __uint_as_float(v[i + 1])), make_float2(b.x, b.y));
+      const float2 s1 =
+          __fadd2_rn(make_float2(__uint_as_float(v[i + 2]), __uint_as_float(v[i + 3])), make_float2(b.z, b.w));
+      acc[i] = s0.x;
+      acc[i + 1] = s0.y;
+      acc[i + 2] = s1.x;
+      acc[i + 3] = s1.y;
     }
     if (EPI == EPI_STORE || EPI == EPI_GELU) {
       if constexpr (sizeof(TOut) == 2) {
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          float a0 = acc[2 * i], a1 = acc[2 * i + 1];
-          if (EPI == EPI_GELU) {
-            a0 = gelu_tanh_fast(a0);
-            a1 = gelu_tanh_fast(a1);
-          }
-          __nv_bfloat162 h2 = __floats2bfloat162_rn(a0, a1);
+          float2 a = make_float2(acc[2 * i], acc[2 * i + 1]);
+          if (EPI == EPI_GELU && !(ep.dbg & 2)) a = gelu_tanh_fast2(a);
+          __nv_bfloat162 h2 = __floats2bfloat162_rn(a.x, a.y);
           pk[i] = *reinterpret_cast<uint32_t*>(&h2);
+        }
+        if (ep.dbg & 8) {   // test hook: each thread stores its row segment directly
+          if (r < M) {
+            uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<TOut*>(ep.out) + size_t(r) * ep.ldo + c0);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) o[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+          }
+          return;
         }
         const uint32_t st0 = tc::smem_u32(stage);
 #pragma unroll
@@ -102,7 +110,7 @@ __device__ __forceinline__ void gemm_epilogue_chunk(const EpiArgs& ep, int r, in
         for (int i = 0; i < 4; ++i) {
           const int rr = i * 8 + (lane >> 2), seg = lane & 3;
           const uint4 w = tc::ld_shared_v4(st0 + (rr * 4 + (seg ^ ((rr >> 1) & 3))) * 16);
-          if (r_warp0 + rr < M)
+          if (r_warp0 + rr < M && !(ep.dbg & 1))
             *reinterpret_cast<uint4*>(reinterpret_cast<TOut*>(ep.out) + size_t(r_warp0 + rr) * ep.ldo + c0 + seg * 8) = w;
         }
         __syncwarp();
@@ -512,10 +520,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
               const uint32_t px = xrow + ((u ^ (row & 7)) << 4);
-              float4 xv = tc::ld_shared_f4(px);
+              // x += g * (acc + b) on the packed f32x2 pipe
+              const float4 xv = tc::ld_shared_f4(px);
               const float4 bb = tc::ld_shared_f4(bias4 + u * 16);
-              float a0 = __uint_as_float(v[4 * u]) + bb.x, a1 = __uint_as_float(v[4 * u + 1]) + bb.y;
-              float a2 = __uint_as_float(v[4 * u + 2]) + bb.z, a3 = __uint_as_float(v[4 * u + 3]) + bb.w;
+              float2 a01 = __fadd2_rn(make_float2(__uint_as_float(v[4 * u]), __uint_as_float(v[4 * u + 1])),
+                                      make_float2(bb.x, bb.y));
+              float2 a23 = __fadd2_rn(make_float2(__uint_as_float(v[4 * u + 2]), __uint_as_float(v[4 * u + 3])),
+                                      make_float2(bb.z, bb.w));
+              float2 x01, x23;
               if (EPI == EPI_RES_GATE) {
                 float4 g;
                 if (gate_smem) {
@@ -524,17 +536,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
                   const float4 ga = __ldg(gm + u), gb = __ldg(ge + u);
                   g = make_float4(ga.x + gb.x, ga.y + gb.y, ga.z + gb.z, ga.w + gb.w);
                 }
-                a0 *= g.x;
-                a1 *= g.y;
-                a2 *= g.z;
-                a3 *= g.w;
+                x01 = __ffma2_rn(make_float2(g.x, g.y), a01, make_float2(xv.x, xv.y));
+                x23 = __ffma2_rn(make_float2(g.z, g.w), a23, make_float2(xv.z, xv.w));
+              } else {
+                x01 = __fadd2_rn(make_float2(xv.x, xv.y), a01);
+                x23 = __fadd2_rn(make_float2(xv.z, xv.w), a23);
               }
-              xv.x += a0;
-              xv.y += a1;
-              xv.z += a2;
-              xv.w += a3;
-              tc::st_shared_v4(px, make_uint4(__float_as_uint(xv.x), __float_as_uint(xv.y), __float_as_uint(xv.z),
-                                              __float_as_uint(xv.w)));
+              tc::st_shared_v4(px, make_uint4(__float_as_uint(x01.x), __float_as_uint(x01.y), __float_as_uint(x23.x),
+                                              __float_as_uint(x23.y)));
             }
           }
         } else if (c0 < N) {
@@ -857,7 +866,7 @@ inline bool tc_gemm_tune(cudaStream_t s, TmaGemmPlan& p, const void* A, const vo
   for (int MC = 1; MC <= (num_m >= 2 ? 2 : 1); ++MC) {
     std::vector<std::pair<double, int>> ranked;
     const int num_mg = (num_m + MC - 1) / MC, slots = p.num_sms / MC;
-    for (int bn = max_bn; bn >= 64; bn -= 32) {
+    for (int bn = max_bn; bn >= std::min(64, max_bn); bn -= 32) {   // narrow N (head): BN = 32
       cands.push_back({MC, bn, 0});
       const int num_n = (N + bn - 1) / bn, tiles = num_mg * num_n, waves = (tiles + slots - 1) / slots;
       const double eff = double(N) / double(num_n * bn) * double(num_m) / double(num_mg * MC) * double(tiles) /
@@ -866,6 +875,10 @@ inline bool tc_gemm_tune(cudaStream_t s, TmaGemmPlan& p, const void* A, const vo
     }
     std::sort(ranked.begin(), ranked.end());
     for (size_t i = 0; i < ranked.size() && i < 2; ++i) cands.push_back({MC, -ranked[i].second, 1});
+  }
+  if (cands.empty()) {
+    *err = "gemm tune: no candidate configuration";
+    return false;
   }
   cudaEvent_t a, b;
   cudaEventCreate(&a);

@@ -161,6 +161,8 @@ struct EpiArgs {
   int gate_row;         // 2 (g1) or 5 (g2)
   int L;                // rows per entry
   long long* trace;     // test hook only (tc GEMM): clock64 stamps of CTA 0 / 1, nullptr = off
+  int dbg;              // test hook only (tc GEMM epilogue timing): bit 0 no global stores,
+                        // bit 1 no GELU, bit 2 one TMEM load in flight; 0 in the product path
 };
 
 __device__ __forceinline__ float gelu_tanh(float z) {
@@ -171,6 +173,19 @@ __device__ __forceinline__ float gelu_tanh_fast(float z) {
   float t;
   asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.7978845608028654f * (z + 0.044715f * z * z * z)));
   return 0.5f * z * (1.f + t);
+}
+
+// Packed pair variant (sm_100 f32x2 FMA pipe): 0.5 z (1 + tanh(z (c + 0.044715 c z^2))).
+__device__ __forceinline__ float2 gelu_tanh_fast2(float2 z) {
+  const float c = 0.7978845608028654f;
+  const float2 u = __fmul2_rn(z, z);
+  const float2 p = __ffma2_rn(u, make_float2(0.044715f * c, 0.044715f * c), make_float2(c, c));
+  const float2 a = __fmul2_rn(z, p);
+  float2 t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t.x) : "f"(a.x));
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t.y) : "f"(a.y));
+  const float2 h = __fmul2_rn(z, make_float2(0.5f, 0.5f));
+  return __ffma2_rn(h, t, h);
 }
 
 template <typename TOut, int EPI>

@@ -1172,6 +1172,7 @@ extern "C" sdv2_status sdv2_debug_gemm(const void* A, const void* W, const float
     cudaMemsetAsync(trace, 0, tn * sizeof(long long), static_cast<cudaStream_t>(stream));
     ep.trace = trace;
   }
+  ep.dbg = getenv("SDV2_GEMM_DBG") ? atoi(getenv("SDV2_GEMM_DBG")) : 0;
   // SDV2_GEMM_CFG="MC,BN,SK": explicit configuration (else the default balance model)
   bool ok;
   if (const char* cfg = getenv("SDV2_GEMM_CFG")) {

@@ -121,10 +121,11 @@ def lib():
     """Load libsdv2.so (raises if it has not been built: no fallback exists)."""
     global _LIB
     if _LIB is None:
-        if not os.path.exists(LIB_PATH):
-            raise RuntimeError(f"{LIB_PATH} is missing: run `python -m paper_2511_07399_b200.build` "
+        path = os.environ.get("SDV2_LIB_PATH", LIB_PATH)   # A/B builds of the same library
+        if not os.path.exists(path):
+            raise RuntimeError(f"{path} is missing: run `python -m paper_2511_07399_b200.build` "
                                "(the hot path has no CPU fallback)")
-        _LIB = _declare(ctypes.CDLL(LIB_PATH))
+        _LIB = _declare(ctypes.CDLL(path))
     return _LIB
 
 
