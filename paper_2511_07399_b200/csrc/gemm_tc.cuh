@@ -29,11 +29,19 @@ namespace sdv2 {
 constexpr int kGemmBM = 128, kGemmBK = 64, kGemmMaxStages = 8, kGemmMaxBN = 256;
 constexpr int kGemmSmemA = kGemmBM * kGemmBK * 2;        // 16 KB
 constexpr int kGemmSmem = 227 * 1024;                    // whole SM: as many stages as fit
-constexpr int kGemmThreads = 384;                        // 4 control warps + 8 epilogue warps
+// 4 control warps + kGemmEpiWG epilogue warpgroups (each drains every kGemmEpiWG-th
+// 32-column chunk of the accumulator).  Measured on the 1.3B step (tools/ab.sh): 2
+// warpgroups 451 fps, 3 (128-register cap) 446, 4 (96 registers, spills) 415.
+#ifndef SDV2_GEMM_EPI_WG
+#define SDV2_GEMM_EPI_WG 2
+#endif
+constexpr int kGemmEpiWG = SDV2_GEMM_EPI_WG;
+constexpr int kGemmEpiThreads = 128 * kGemmEpiWG;
+constexpr int kGemmThreads = 128 + kGemmEpiThreads;
 
 // Stages of the TMA->MMA ring for a tile width: the ring must cover the L2/HBM latency
 // (about 1-2 us) at the MMA rate, so use all of shared memory.
-constexpr int kGemmEpiVec = 3 * kGemmMaxBN * 4 + 8 * 2048;   // bias + 2 gate vectors per tile, 8 x 2 KB store staging
+constexpr int kGemmEpiVec = 3 * kGemmMaxBN * 4 + 4 * kGemmEpiWG * 2048;   // bias + 2 gate vectors per tile, 2 KB store staging per epilogue warp
 // BNl = W rows held per CTA (BN, or BN / 2 for a CTA pair).
 __host__ __device__ inline int gemm_stages(int BN, bool res_tma, int BNl) {
   const int xs = res_tma ? BN * kGemmBM * 4 : 0;     // staged fp32 residual tile
@@ -257,7 +265,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(x_full + 1);
   float* sBias = reinterpret_cast<float*>(x_full + 2);   // [BN] bias, then [2][BN] gate sums
   float* sGate = sBias + kGemmMaxBN;
-  uint4* sStage = reinterpret_cast<uint4*>(sGate + 2 * kGemmMaxBN);   // [8 epilogue warps][128] x 16 B
+  uint4* sStage = reinterpret_cast<uint4*>(sGate + 2 * kGemmMaxBN);   // [epilogue warps][128] x 16 B
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int num_m = (M + kGemmBM - 1) / kGemmBM, num_n = (N + BN - 1) / BN;
@@ -283,7 +291,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
     }
     for (int s = 0; s < 2; ++s) {
       tc::mbar_init(tfull + s, 1);
-      tc::mbar_init(tempty + s, 8 * MC); // pair: both CTAs' epilogue warps free the accumulator
+      tc::mbar_init(tempty + s, 4 * kGemmEpiWG * MC); // pair: both CTAs' epilogue warps free the accumulator
     }
     tc::mbar_init(x_full, 1);
     if (kResTMA) tc::tma_prefetch_desc(&tmX);
@@ -418,7 +426,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
   } else if (warp >= 4) {
     pdl_wait();                         // epilogue reads x / gates produced upstream
     const int q = warp & 3;             // TMEM lane quarter accessible by this warp
-    const int wg = (warp - 4) >> 2;     // epilogue warpgroup: 32-column chunks c % 2 == wg
+    const int wg = (warp - 4) >> 2;     // epilogue warpgroup: 32-column chunks c % kGemmEpiWG == wg
     const bool leader = (warp == 4 && lane == 0);
     const int row = q * 32 + lane;      // row inside the tile
     int acc = 0;
@@ -444,8 +452,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
       const int e_lo = (row0 < M ? row0 : M - 1) / ep.L;
       const int e_hi = ((row0 + kGemmBM - 1) < M ? row0 + kGemmBM - 1 : M - 1) / ep.L;
       const bool gate_smem = EPI == EPI_RES_GATE && e_hi <= e_lo + 1;
-      asm volatile("bar.sync 3, 256;" ::: "memory");   // previous tile's readers done
-      for (int i = threadIdx.x - 128; i < (partial ? 0 : BN); i += 256) {
+      asm volatile("bar.sync 3, %0;" ::"n"(kGemmEpiThreads) : "memory");   // previous tile's readers done
+      for (int i = threadIdx.x - 128; i < (partial ? 0 : BN); i += kGemmEpiThreads) {
         const int col = nb * BN + i;
         const bool ok = col < N;
         sBias[i] = ok ? ep.bias[col] : 0.f;
@@ -464,7 +472,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
           } while (v == 0);
         }
       }
-      asm volatile("bar.sync 3, 256;" ::: "memory");
+      asm volatile("bar.sync 3, %0;" ::"n"(kGemmEpiThreads) : "memory");
       tc::mbar_wait(tfull + acc, acc_phase);
       if (warp == 4 && lane == 0) GEMM_TRACE(4, nt);
       if (warp == 4 && lane == 0 && nt == 0) GEMM_CTA_STAMP(2);
@@ -552,21 +560,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
         }
       };
       // two TMEM chunks in flight: the next 32 columns load while this chunk is processed
-      uint32_t va[32], vb[32];
-      int c = wg * 32;
-      if (c < BN) tc::tmem_ld32(tbase + c, va);
-      while (c < BN) {
+      // one 32-column TMEM load in flight per warp (keeping a second one in flight measured
+      // no faster and costs the 32 registers a third epilogue warpgroup needs)
+      constexpr int CS = 32 * kGemmEpiWG;   // column stride between this warpgroup's chunks
+      for (int c = wg * 32; c < BN; c += CS) {
+        uint32_t va[32];
+        tc::tmem_ld32(tbase + c, va);
         tc::tmem_ld_wait_dep(va);
         if (warp == 4 && lane == 0 && c == 0) GEMM_TRACE(6, nt);
-        if (c + 64 < BN) tc::tmem_ld32(tbase + c + 64, vb);
         chunk(va, c);
         if (warp == 4 && lane == 0 && c == 0) GEMM_TRACE(7, nt);
-        c += 64;
-        if (c >= BN) break;
-        tc::tmem_ld_wait_dep(vb);
-        if (c + 64 < BN) tc::tmem_ld32(tbase + c + 64, va);
-        chunk(vb, c);
-        c += 64;
       }
       tc::tc_fence_before();
       __syncwarp();
@@ -576,18 +579,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
       }
       if (partial) {   // publish: every thread's stores, then one release of the flag
         __threadfence();
-        asm volatile("bar.sync 3, 256;" ::: "memory");
+        asm volatile("bar.sync 3, %0;" ::"n"(kGemmEpiThreads) : "memory");
         if (threadIdx.x == 128)
           asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(sk.flags + cid * MC + cr), "r"(1) : "memory");
       }
       if (fixup) {     // consumed: re-arm the contributors' flags for the next launch
-        asm volatile("bar.sync 3, 256;" ::: "memory");
+        asm volatile("bar.sync 3, %0;" ::"n"(kGemmEpiThreads) : "memory");
         if (threadIdx.x == 128)
           for (int cc = c_first; cc < cid; ++cc) sk.flags[cc * MC + cr] = 0;
       }
       if (kResTMA && !partial) {
         tc::fence_proxy_async_smem();   // generic-proxy smem writes -> visible to the TMA store
-        asm volatile("bar.sync 2, 256;" ::: "memory");
+        asm volatile("bar.sync 2, %0;" ::"n"(kGemmEpiThreads) : "memory");
         if (leader) {
           for (int c = 0; c < BN; c += 32)
             tc::tma_store_2d(&tmX, sX + (c / 32) * (kGemmBM * 128), nb * BN + c, mb * kGemmBM);
