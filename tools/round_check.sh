@@ -12,4 +12,5 @@ for c in wan13_512_4step wan14_480p_4step; do
   timeout 600 python bench.py --config $c --steps 20 --no-cpu-baseline > gpurun_out/bench_${c}_${tag}.json 2> gpurun_out/bench_${c}_${tag}.err
 done
 bash tools/ncu_bench.sh ${tag} "gemm_tc|attn_tc|qkv_post|norm_mod"
+bash tools/pp_bench_check.sh 30 > gpurun_out/pp2_${tag}.json 2> gpurun_out/pp2_${tag}.err
 tail -3 gpurun_out/pytest_gpu_${tag}.log; cut -c1-600 gpurun_out/bench_${tag}.json; cut -c1-300 gpurun_out/bench_*_${tag}.json
