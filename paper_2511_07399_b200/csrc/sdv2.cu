@@ -940,7 +940,13 @@ sdv2_status sdv2_reset_stream(sdv2_handle* h, const sdv2_stream_desc* sd, const 
   if (!(sd->motion_sigma > 0.f) || sd->motion_k < 0 || sd->motion_k >= 63) return SDV2_E_INVALID;
   if (sd->sink_tau < -1.f || sd->sink_tau > 1.f) return SDV2_E_INVALID;
   if (sd->rope_reset_frames < std::max(h->m, h->W) * h->T || sd->rope_reset_frames + h->T > 4096) return SDV2_E_INVALID;
+  // captured call graphs bake the stream constants in as kernel arguments: keep them only
+  // if this reset leaves those constants unchanged
+  const StreamCfg old_cfg = h->scfg;
+  const RopeTabs old_rt = h->rt;
+  const int old_T_reset = h->T_reset;
   h->T_reset = sd->rope_reset_frames;
+  std::memset(&h->scfg, 0, sizeof(h->scfg));
   for (int j = 0; j < kMaxSteps; ++j) h->scfg.t[j] = j < h->n ? sd->timesteps[j] : 0.f;
   h->scfg.n = h->n;
   h->scfg.k = sd->motion_k;
@@ -983,6 +989,14 @@ sdv2_status sdv2_reset_stream(sdv2_handle* h, const sdv2_stream_desc* sd, const 
     h->rt.cw_cos = h->rope + o_wcs; h->rt.cw_sin = h->rope + o_wsn;
     h->rt.ct = h->ct; h->rt.ch = h->ch; h->rt.cw = h->cw; h->rt.t_off = t_off;
     CK(cudaStreamSynchronize(h->stream));   // the host table vector dies here
+  }
+  if (old_T_reset != h->T_reset || std::memcmp(&old_cfg, &h->scfg, sizeof(StreamCfg)) != 0 ||
+      std::memcmp(&old_rt, &h->rt, sizeof(RopeTabs)) != 0) {
+    for (auto& g : h->graph_exec)
+      if (g) {
+        cudaGraphExecDestroy(g);
+        g = nullptr;
+      }
   }
   // zero lanes, controller state
   const size_t kv = size_t(h->nb) * h->n * h->S * h->L * h->d * h->ta;

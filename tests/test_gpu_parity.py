@@ -106,3 +106,36 @@ def test_graph_replay_equals_eager(tiny_ref, prec):
         assert np.array_equal(g_outs[X], e_outs[X]), X
     for X in range(cfg.num_chunks):
         assert rel_l2(g_outs[X], recs[X]["out"]) <= TOL[prec]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("prec", [SDV2_FP32, SDV2_BF16])
+def test_reset_with_new_stream_constants_drops_stale_graphs(prec, monkeypatch):
+    """Captured call graphs bake stream constants (timesteps, seed, T_reset) in as kernel
+    arguments: re-using a handle with a different stream descriptor must give exactly
+    the output of a fresh handle with that descriptor (no stale graph replay)."""
+    import dataclasses
+    import torch
+    from paper_2511_07399_b200.sdv2 import Stage
+    monkeypatch.setenv("SDV2_TUNE", "0")   # same GEMM configuration in both handles
+    cfg = sg.CONFIGS["tiny"]
+    W, chunks, prompts = tiny_inputs(cfg)
+    sd2 = dataclasses.replace(cfg.stream, seed=cfg.stream.seed + 17, rope_reset_frames=cfg.stream.rope_reset_frames + 2)
+    fresh, _, _ = run_gpu(cfg, W, chunks, prompts, prec, tap=False, stream_desc=sd2)
+    stage = Stage(cfg.model, cfg.geom, W, precision=prec)
+    out = torch.zeros(chunks[0].shape, dtype=torch.float32, device="cuda")
+    for sd in (cfg.stream, sd2):
+        stage.reset_stream(sd, prompts[0])
+        got = {}
+        starts = [0, *cfg.prompt_switch]
+        for c, v in enumerate(chunks):
+            if c in starts and c > 0:
+                stage.set_prompt(prompts[starts.index(c)])
+            oc = stage.denoise_chunk(torch.from_numpy(v).cuda().data_ptr(), out.data_ptr())
+            torch.cuda.synchronize()
+            if oc >= 0:
+                got[oc] = out.cpu().numpy().copy()
+    stage.close()
+    assert sorted(got) == sorted(fresh)
+    for X in fresh:
+        assert np.array_equal(got[X], fresh[X]), X

@@ -30,8 +30,10 @@ def launch_table(path):
 
 KEYS = [("gpu__time_duration.sum", "duration"), ("launch__grid_size", "grid"),
         ("launch__registers_per_thread", "regs"), ("dram__bytes_read.sum", "DRAM rd"),
-        ("dram__bytes_write.sum", "DRAM wr"), ("sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
-                                              "tensor(TMEM/UTC) active %"),
+        ("dram__bytes_write.sum", "DRAM wr"),
+        ("sm__ops_path_tensor_op_utchmma_src_bf16_dst_fp32_sparsity_off.avg.pct_of_peak_sustained_elapsed",
+         "tensor pipe (UTC bf16 HMMA ops) % of peak"),
+        ("sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "TMEM/UTC active %"),
         ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM %"),
         ("gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed", "mem %"),
         ("sm__warps_active.avg.pct_of_peak_sustained_active", "occupancy %")]
