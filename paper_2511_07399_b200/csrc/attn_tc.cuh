@@ -157,6 +157,10 @@ __device__ __forceinline__ float2 ex2_poly2(uint64_t x2) {
                      __uint_as_float(__float_as_uint(pv.y) + (__float_as_uint(tv.y) << 23)));
 }
 
+// Pairs i with bit (i % 8) set use the FMA-pipe polynomial: 0xA4 = {2, 5, 7}, 3/8 of them.
+#ifndef SDV2_ATTN_POLY_MASK
+#define SDV2_ATTN_POLY_MASK 0xA4
+#endif
 // P = 2^(s * scale - m) for one thread's HC scores -> bf16 pairs in pk, returns the row
 // sum.  POLY: pairs with i % 8 in {2, 5, 7} (3/8) use ex2_poly2 instead of the MUFU.
 template <int HC, bool POLY>
@@ -166,7 +170,7 @@ __device__ __forceinline__ float p_row(const float* sv, uint32_t* pk, uint64_t s
   for (int i = 0; i < HC / 2; ++i) {
     const uint64_t x2 = ffma2(f2pack(sv[2 * i], sv[2 * i + 1]), sc2, nm2);
     float2 pp;
-    if (POLY && ((i & 7) == 2 || (i & 7) == 5 || (i & 7) == 7)) {
+    if (POLY && ((SDV2_ATTN_POLY_MASK >> (i & 7)) & 1)) {
       pp = ex2_poly2(x2);
     } else {
       const float2 x = f2unpack(x2);

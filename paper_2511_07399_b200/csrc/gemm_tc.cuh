@@ -623,6 +623,9 @@ typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_
 
 struct GemmCfg {
   int MC, BN, SK;   // cluster size (1 or CTA pair), tile width, stream-K
+  int XE = 0;       // residual epilogue with one tile per cluster: fetch the x tile into its
+                    // own buffer while the MMAs run (fewer stages) instead of into the
+                    // operand ring after the last MMA
 };
 
 struct TmaGemmPlan {
@@ -808,7 +811,7 @@ inline bool tc_gemm_cfg(cudaStream_t s, TmaGemmPlan& p, const void* A, const voi
   const int slots = p.num_sms / MC;
   const int grid = MC * int(work < slots ? work : slots);
   // residual x tile staged in the operand ring when no cluster gets a second tile
-  const GemmSk sk{gc.SK, (!gc.SK && tiles <= slots) ? 1 : 0, p.sk_ws, p.sk_flags};
+  const GemmSk sk{gc.SK, (!gc.SK && !gc.XE && tiles <= slots) ? 1 : 0, p.sk_ws, p.sk_flags};
   cudaError_t e = MC == 2 ? gemm_dispatch<2>(s, grid, *ma, *mb, *mx, M, N, K, BN, epi, ep, sk)
                           : gemm_dispatch<1>(s, grid, *ma, *mb, *mx, M, N, K, BN, epi, ep, sk);
   if (e == cudaSuccess) e = cudaGetLastError();
@@ -871,6 +874,7 @@ inline bool tc_gemm_tune(cudaStream_t s, TmaGemmPlan& p, const void* A, const vo
     const int num_mg = (num_m + MC - 1) / MC, slots = p.num_sms / MC;
     for (int bn = max_bn; bn >= std::min(64, max_bn); bn -= 32) {   // narrow N (head): BN = 32
       cands.push_back({MC, bn, 0});
+      if (res && ((num_m + MC - 1) / MC) * ((N + bn - 1) / bn) <= slots) cands.push_back({MC, bn, 0, 1});
       const int num_n = (N + bn - 1) / bn, tiles = num_mg * num_n, waves = (tiles + slots - 1) / slots;
       const double eff = double(N) / double(num_n * bn) * double(num_m) / double(num_mg * MC) * double(tiles) /
                          double(waves * slots);
@@ -914,7 +918,7 @@ inline bool tc_gemm_tune(cudaStream_t s, TmaGemmPlan& p, const void* A, const vo
     cudaGraphExecDestroy(exec);
     cudaGraphDestroy(graph);
     if (getenv("SDV2_VERBOSE") && atoi(getenv("SDV2_VERBOSE")) > 1)
-      fprintf(stderr, "  cand MC=%d BN=%d SK=%d %.1f us\n", c.MC, c.BN, c.SK, ms * 1e3f / kReps);
+      fprintf(stderr, "  cand MC=%d BN=%d SK=%d XE=%d %.1f us\n", c.MC, c.BN, c.SK, c.XE, ms * 1e3f / kReps);
     if (ms < best) {
       best = ms;
       best_cfg = c;
@@ -924,8 +928,8 @@ inline bool tc_gemm_tune(cudaStream_t s, TmaGemmPlan& p, const void* A, const vo
   cudaEventDestroy(b);
   p.tuned[key] = best_cfg;
   if (getenv("SDV2_VERBOSE"))
-    fprintf(stderr, "sdv2 gemm tune M=%d N=%d K=%d epi=%d -> MC=%d BN=%d SK=%d (%.1f us)\n", M, N, K, epi,
-            best_cfg.MC, best_cfg.BN, best_cfg.SK, best * 1e3f / kReps);
+    fprintf(stderr, "sdv2 gemm tune M=%d N=%d K=%d epi=%d -> MC=%d BN=%d SK=%d XE=%d (%.1f us)\n", M, N, K, epi,
+            best_cfg.MC, best_cfg.BN, best_cfg.SK, best_cfg.XE, best * 1e3f / kReps);
   return cudaGetLastError() == cudaSuccess;
 }
 
