@@ -361,12 +361,33 @@ def run_pipeline_bench(args, cfg):
     torch.cuda.synchronize(dev_index)
     prof = stage.profile_read()
     stage.profile_enable(False)
+    # ---- stage hand-off link rate (SURVEY §8(d) NVLink): ranks 0 -> 1 send the act packet
+    # size back to back; device time on the sending stream, vs 900 GB/s per direction
+    link = None
+    act_bytes = int(tr.io(0)["act_out"].numel()) if world > 1 else 0
+    if world > 1 and act_bytes and rank in (0, 1):
+        dev = f"cuda:{dev_index}" if backend == "nccl" else "cpu"
+        buf = torch.empty(act_bytes, dtype=torch.uint8, device=dev)
+        reps = 20
+        with torch.cuda.stream(stream):
+            for i in range(reps + 3):
+                if i == 3:
+                    l0 = ev()
+                if rank == 0:
+                    dist.send(buf, 1)
+                else:
+                    dist.recv(buf, 0)
+            l1 = ev()
+        torch.cuda.synchronize(dev_index)
+        ms_link = l0.elapsed_time(l1)
+        link = [act_bytes * reps / (ms_link / 1e3) / 1e9 if ms_link > 0 else 0.0, float(act_bytes)]
     reasons = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
     mine = [timed_ms, e2e_ms, ttff, float(outs_timed), float(outs_e2e), float(launches),
             float(clocks.get("sm_mhz") or 0.0), float(clocks.get("sm_max_mhz") or 0.0),
             prof["gemm"]["ms"], prof["gemm"]["flops"], prof["gemm"]["launches"],
             prof["self_attn"]["ms"], prof["self_attn"]["flops"], prof["cross_attn"]["ms"],
-            prof["cross_attn"]["flops"]] + [1.0 if r in clocks.get("reasons", []) else 0.0 for r in reasons]
+            prof["cross_attn"]["flops"]] + [1.0 if r in clocks.get("reasons", []) else 0.0 for r in reasons] + \
+           (link if link else [0.0, 0.0])
     allr = _gather(dist, mine, backend)
     steps_all = _gather(dist, step_ms, backend)
     dist.barrier()
@@ -414,6 +435,10 @@ def run_pipeline_bench(args, cfg):
                          "per_launch_ms": g_ms / max(1, g_n), "flops_per_launch": g_fl / max(1, g_n),
                          "rank": gr, "note": "projection GEMMs of the slowest stage, per-launch CUDA events"},
             "cpu_baseline": None,
+            "stage_handoff": {"bytes_per_tick": allr[0][20], "GBps_rank0_to_1": allr[0][19], "peak_GBps": 900.0,
+                              "frac": allr[0][19] / 900.0, "transport": backend,
+                              "note": "back-to-back send of one act packet, device time on the sending stream"}
+            if world > 1 else None,
             "clocks": {"sm_mhz": statistics.median([r[6] for r in allr]), "sm_max_mhz": max(r[7] for r in allr),
                        "reasons": [reasons[i] for i in range(4) if any(r[15 + i] for r in allr)],
                        "per_rank_sm_mhz": [r[6] for r in allr]},
