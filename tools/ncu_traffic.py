@@ -18,7 +18,7 @@ def val(r, k):
     v = float(r[i].replace(",", ""))
     u = units[i]
     return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-3, "us": 1.0, "usecond": 1.0,
-                "msecond": 1e3}.get(u, 1.0)
+                "msecond": 1e3, "ms": 1e3, "nsecond": 1e-3}.get(u, 1.0)
 
 
 UTC = "sm__ops_path_tensor_op_utchmma_src_bf16_dst_fp32_sparsity_off.avg.pct_of_peak_sustained_elapsed"
