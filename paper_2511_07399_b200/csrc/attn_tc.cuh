@@ -58,6 +58,8 @@ struct AttnTcArgs {
   float* part_ml;      // [G][128][2] running max (log2 domain), sum
   int* flags;          // [G] partial ready (1), reset by the CTA that merges it
   int per_unit;        // 1: one CTA per unit (grid = units, no merge); 0: stream-K
+  int rr;              // stream-K only: deal whole units round-robin first (R = units / CTAs
+                       // full rounds), stream-K split only the tiles of the last partial round
   int dbg;             // test hook only (pipeline timing): bit 0 skips the softmax math,
                        // bit 1 the MMAs, bit 2 the K/V loads, bit 3 the PV MMAs, bit 4 the
                        // S MMAs; 0 in the product path
@@ -77,6 +79,9 @@ struct AttnGeo {
   int J[kMaxSteps];               // key tiles per unit of entry e
   long long T;                    // total tiles
   int QP;                         // query-tile groups per head (CL query tiles per group)
+  long long ubase[kMaxSteps + 1]; // first unit of entry e
+  long long Tr = 0;               // first tile of the stream-K split (after R whole rounds)
+  int R = 0;                      // whole-unit rounds dealt round-robin
   __device__ void init(const AttnTcArgs& a, const TickDesc* td, int CL) {
     QP = (a.QT + CL - 1) / CL;
     off[0] = 0;
@@ -90,6 +95,24 @@ struct AttnGeo {
       off[e + 1] = off[e] + (long long)a.H * QP * j;
     }
     T = off[kMaxSteps];
+    ubase[0] = 0;
+    for (int e = 0; e < kMaxSteps; ++e) ubase[e + 1] = ubase[e] + (J[e] > 0 ? (long long)a.H * QP : 0);
+  }
+  // Hybrid schedule over G CTAs: R = units / G rounds of whole units (unit c + k G for CTA
+  // c: the G concurrently running units are consecutive, so they share a few heads' K/V in
+  // L2), then the tiles of the remaining units split evenly (stream-K).
+  // One round is always left to the split, so the split covers >= G units: every CTA gets
+  // a non-empty range (the merge waits on every CTA between a unit's first and last
+  // owner) and a unit is cut into at most two pieces (cheap merges).
+  __device__ void plan(bool rr, int G) {
+    R = rr ? int(ubase[kMaxSteps] / G) - 1 : 0;
+    if (R < 0) R = 0;
+    Tr = R > 0 ? unit_lo((long long)R * G) : 0;
+  }
+  __device__ long long unit_lo(long long u) const {   // first tile of unit u (u <= units)
+    int e = 0;
+    while (e < kMaxSteps - 1 && u >= ubase[e + 1]) ++e;
+    return u >= ubase[kMaxSteps] ? T : off[e] + (u - ubase[e]) * J[e];
   }
   // unit containing global tile g -> (e, unit-in-entry w, tile j)
   __device__ void locate(long long g, int& e, int& w, int& j) const {
@@ -99,8 +122,12 @@ struct AttnGeo {
     w = int(r / J[e]);
     j = int(r % J[e]);
   }
-  __device__ long long start(int c, int G) const { return (T * c) / G; }
-  __device__ int cta_of(long long g, int G) const { return int(((g + 1) * G + T - 1) / T) - 1; }
+  // stream-K split of the tiles [Tr, T)
+  __device__ long long start(int c, int G) const { return Tr + ((T - Tr) * c) / G; }
+  __device__ int cta_of(long long g, int G) const {
+    const long long Ts = T - Tr;
+    return int(((g - Tr + 1) * G + Ts - 1) / Ts) - 1;
+  }
 };
 
 constexpr int kAttnThreads = 352;   // warp 0 TMA Q+K, 1 MMA, 2..9 softmax (two key halves), 10 TMA V
@@ -248,10 +275,25 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
     t0 = geo.off[e] + (long long)w * geo.J[e];
     t1 = t0 + geo.J[e];
   } else {
+    geo.plan(a.rr != 0, G);
     t0 = geo.start(c, G);
     t1 = geo.start(c + 1, G);
   }
-  if (t0 >= t1) return;
+  if (t0 >= t1 && geo.R == 0) return;
+  // Work ranges of this CTA, each walked from its end: range 0 = its stream-K tile range,
+  // ranges 1..R = its whole units c + (r - 1) G.  seg_before clamps to the current t0.
+  const long long tail_lo = t0, tail_hi = t1;
+  const int nrg = 1 + geo.R;
+  auto range_of = [&](int rg, long long& lo, long long& hi) {
+    if (rg == 0) {
+      lo = tail_lo;
+      hi = tail_hi;
+    } else {
+      const long long u = c + (long long)(rg - 1) * G;
+      lo = geo.unit_lo(u);
+      hi = geo.unit_lo(u + 1);
+    }
+  };
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (warp == 0 && lane == 0) {
@@ -323,47 +365,50 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
     {   // whole warp walks the loop; one elected lane issues
       long long g = t1;
       int gi = 0, sg = 0;   // local tile counter, segment counter
-      while (g > t0) {
-        const Seg s = seg_before(g);
-        const int col = s.h * HD;
-        const int kv_row = a.kv_row0 + (a.cross ? (td->e[s.e].pver & 1) : s.e) * a.kv_lane_rows;
-        if (sg > 0) tc::mbar_wait(q_empty, (sg - 1) & 1);
-        if (tc::elect_one()) {
-          if (CL > 1) {   // both CTAs' Q land on the even CTA's barrier
-            if (cr == 0) tc::mbar_expect_tx(q_full, 2 * SM::Q);
-            for (int ch = 0; ch < NCH; ++ch)
-              tc::tma_load_2d_cg2(sQ + ch * (kAttnBQ * 128), &tmQ, tc::mapa_shared(q_full, 0), col + ch * 64,
-                                  s.e * a.L + s.q0);
-          } else {
-            tc::mbar_expect_tx(q_full, SM::Q);
-            for (int ch = 0; ch < NCH; ++ch)
-              tc::tma_load_2d(sQ + ch * (kAttnBQ * 128), &tmQ, q_full, col + ch * 64, s.e * a.L + s.q0);
-          }
-        }
-        __syncwarp();
-        for (int j = s.jb; j < s.je; ++j, ++gi) {
-          const int st = gi % KS;
-          tc::mbar_wait(k_empty + st, ((gi / KS) & 1) ^ 1);
-          ATTN_TRACE(8, gi);
+      for (int rg = 0; rg < nrg; ++rg) {
+        range_of(rg, t0, g);
+        while (g > t0) {
+          const Seg s = seg_before(g);
+          const int col = s.h * HD;
+          const int kv_row = a.kv_row0 + (a.cross ? (td->e[s.e].pver & 1) : s.e) * a.kv_lane_rows;
+          if (sg > 0) tc::mbar_wait(q_empty, (sg - 1) & 1);
           if (tc::elect_one()) {
-            if (a.dbg & 4) {
-              tc::mbar_arrive(k_full + st);
-            } else if (CL > 1) {   // this CTA's 64 keys x 128 dims, counted on the even CTA
-              if (cr == 0) tc::mbar_expect_tx(k_full + st, 2 * SM::KV);
+            if (CL > 1) {   // both CTAs' Q land on the even CTA's barrier
+              if (cr == 0) tc::mbar_expect_tx(q_full, 2 * SM::Q);
               for (int ch = 0; ch < NCH; ++ch)
-                tc::tma_load_2d_cg2(sK + st * SM::KV + ch * (kAttnBKV / 2 * 128), &tmK, tc::mapa_shared(k_full + st, 0),
-                                    col + ch * 64, kv_row + j * kAttnBKV + cr * (kAttnBKV / 2));
+                tc::tma_load_2d_cg2(sQ + ch * (kAttnBQ * 128), &tmQ, tc::mapa_shared(q_full, 0), col + ch * 64,
+                                    s.e * a.L + s.q0);
             } else {
-              tc::mbar_expect_tx(k_full + st, SM::KV);
+              tc::mbar_expect_tx(q_full, SM::Q);
               for (int ch = 0; ch < NCH; ++ch)
-                tc::tma_load_2d(sK + st * SM::KV + ch * (kAttnBKV * 128), &tmK, k_full + st, col + ch * 64,
-                                kv_row + j * kAttnBKV);
+                tc::tma_load_2d(sQ + ch * (kAttnBQ * 128), &tmQ, q_full, col + ch * 64, s.e * a.L + s.q0);
             }
           }
           __syncwarp();
+          for (int j = s.jb; j < s.je; ++j, ++gi) {
+            const int st = gi % KS;
+            tc::mbar_wait(k_empty + st, ((gi / KS) & 1) ^ 1);
+            ATTN_TRACE(8, gi);
+            if (tc::elect_one()) {
+              if (a.dbg & 4) {
+                tc::mbar_arrive(k_full + st);
+              } else if (CL > 1) {   // this CTA's 64 keys x 128 dims, counted on the even CTA
+                if (cr == 0) tc::mbar_expect_tx(k_full + st, 2 * SM::KV);
+                for (int ch = 0; ch < NCH; ++ch)
+                  tc::tma_load_2d_cg2(sK + st * SM::KV + ch * (kAttnBKV / 2 * 128), &tmK, tc::mapa_shared(k_full + st, 0),
+                                      col + ch * 64, kv_row + j * kAttnBKV + cr * (kAttnBKV / 2));
+              } else {
+                tc::mbar_expect_tx(k_full + st, SM::KV);
+                for (int ch = 0; ch < NCH; ++ch)
+                  tc::tma_load_2d(sK + st * SM::KV + ch * (kAttnBKV * 128), &tmK, k_full + st, col + ch * 64,
+                                  kv_row + j * kAttnBKV);
+              }
+            }
+            __syncwarp();
+          }
+          g = s.gs;
+          ++sg;
         }
-        g = s.gs;
-        ++sg;
       }
     }
   } else if (warp == 10) {
@@ -373,31 +418,34 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
     {
       long long g = t1;
       int gi = 0;
-      while (g > t0) {
-        const Seg s = seg_before(g);
-        const int col = s.h * HD;
-        const int kv_row = a.kv_row0 + (a.cross ? (td->e[s.e].pver & 1) : s.e) * a.kv_lane_rows;
-        for (int j = s.jb; j < s.je; ++j, ++gi) {
-          const int st = gi % VS;
-          tc::mbar_wait(v_empty + st, ((gi / VS) & 1) ^ 1);
-          ATTN_TRACE(9, gi);
-          if (tc::elect_one()) {
-            if (a.dbg & 4) {
-              tc::mbar_arrive(v_full + st);
-            } else if (CL > 1) {   // 128 keys x this CTA's 64 head-dim columns
-              if (cr == 0) tc::mbar_expect_tx(v_full + st, 2 * SM::KV);
-              tc::tma_load_2d_cg2(sV + st * SM::KV, &tmV, tc::mapa_shared(v_full + st, 0), col + cr * 64,
+      for (int rg = 0; rg < nrg; ++rg) {
+        range_of(rg, t0, g);
+        while (g > t0) {
+          const Seg s = seg_before(g);
+          const int col = s.h * HD;
+          const int kv_row = a.kv_row0 + (a.cross ? (td->e[s.e].pver & 1) : s.e) * a.kv_lane_rows;
+          for (int j = s.jb; j < s.je; ++j, ++gi) {
+            const int st = gi % VS;
+            tc::mbar_wait(v_empty + st, ((gi / VS) & 1) ^ 1);
+            ATTN_TRACE(9, gi);
+            if (tc::elect_one()) {
+              if (a.dbg & 4) {
+                tc::mbar_arrive(v_full + st);
+              } else if (CL > 1) {   // 128 keys x this CTA's 64 head-dim columns
+                if (cr == 0) tc::mbar_expect_tx(v_full + st, 2 * SM::KV);
+                tc::tma_load_2d_cg2(sV + st * SM::KV, &tmV, tc::mapa_shared(v_full + st, 0), col + cr * 64,
+                                    kv_row + j * kAttnBKV);
+              } else {
+                tc::mbar_expect_tx(v_full + st, SM::KV);
+                for (int ch = 0; ch < NCH; ++ch)
+                  tc::tma_load_2d(sV + st * SM::KV + ch * (kAttnBKV * 128), &tmV, v_full + st, col + ch * 64,
                                   kv_row + j * kAttnBKV);
-            } else {
-              tc::mbar_expect_tx(v_full + st, SM::KV);
-              for (int ch = 0; ch < NCH; ++ch)
-                tc::tma_load_2d(sV + st * SM::KV + ch * (kAttnBKV * 128), &tmV, v_full + st, col + ch * 64,
-                                kv_row + j * kAttnBKV);
+              }
             }
+            __syncwarp();
           }
-          __syncwarp();
+          g = s.gs;
         }
-        g = s.gs;
       }
     }
   } else if (warp == 1) {
@@ -437,51 +485,54 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
       };
       long long g = t1;
       int gi = 0, sg = 0;
-      while (g > t0) {
-        const Seg s = seg_before(g);
-        const int nt = s.je - s.jb;
-        tc::mbar_wait(q_full, sg & 1);
-        auto release_q = [&]() {   // last S of the segment issued: Q smem reusable once it lands
-          if (tc::elect_one()) commit(q_empty);
-          __syncwarp();
-        };
-        issue_S(gi);
-        if (nt > 1) issue_S(gi + 1);
-        if (nt <= 2) release_q();
-        for (int t = 0; t < nt; ++t) {
-          const int gt = gi + t;
-          if (t + 2 < nt) {
-            issue_S(gt + 2);
-            if (t + 3 == nt) release_q();
-          }
-          tc::mbar_wait(v_full + (gt % VS), (gt / VS) & 1);
-          ATTN_TRACE(0, gt);
-          if (t == 0 && sg > 0) tc::mbar_wait(o_empty, (sg - 1) & 1);
-          tc::mbar_wait(p_full + gt % 3, (gt / 3) & 1);
-          ATTN_TRACE(1, gt);
-          tc::tc_fence_after();
-          const uint32_t va = tc::smem_u32(sV + (gt % VS) * SM::KV);
-          if (tc::elect_one()) {
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {   // O += P V; A = P from TMEM (bf16 pairs, 8 columns per K=16):
-                                            // keys 64h..64h+63 sit in slot columns [64h, 64h+32)
-              if (!(a.dbg & 10)) {
-                if (CL > 1)   // B = this CTA's 64 head-dim columns of V (one 64-wide block)
-                  tc::mma_bf16_ts_cg2(tO, tS(gt % 3) + (k >> 2) * 64 + (k & 3) * 8,
-                                      tc::sw128_mnmajor_desc(va + k * 2048, kAttnBKV * 128), idO, (t | k) != 0);
-                else
-                  tc::mma_bf16_ts(tO, tS(gt % 3) + (k >> 2) * 64 + (k & 3) * 8,
-                                  tc::sw128_mnmajor_desc(va + k * 2048, kAttnBKV * 128), idO, (t | k) != 0);
-              }
+      for (int rg = 0; rg < nrg; ++rg) {
+        range_of(rg, t0, g);
+        while (g > t0) {
+          const Seg s = seg_before(g);
+          const int nt = s.je - s.jb;
+          tc::mbar_wait(q_full, sg & 1);
+          auto release_q = [&]() {   // last S of the segment issued: Q smem reusable once it lands
+            if (tc::elect_one()) commit(q_empty);
+            __syncwarp();
+          };
+          issue_S(gi);
+          if (nt > 1) issue_S(gi + 1);
+          if (nt <= 2) release_q();
+          for (int t = 0; t < nt; ++t) {
+            const int gt = gi + t;
+            if (t + 2 < nt) {
+              issue_S(gt + 2);
+              if (t + 3 == nt) release_q();
             }
-            commit(v_empty + (gt % VS));
-            commit(pv_done + gt % 3);
+            tc::mbar_wait(v_full + (gt % VS), (gt / VS) & 1);
+            ATTN_TRACE(0, gt);
+            if (t == 0 && sg > 0) tc::mbar_wait(o_empty, (sg - 1) & 1);
+            tc::mbar_wait(p_full + gt % 3, (gt / 3) & 1);
+            ATTN_TRACE(1, gt);
+            tc::tc_fence_after();
+            const uint32_t va = tc::smem_u32(sV + (gt % VS) * SM::KV);
+            if (tc::elect_one()) {
+  #pragma unroll
+              for (int k = 0; k < 8; ++k) {   // O += P V; A = P from TMEM (bf16 pairs, 8 columns per K=16):
+                                              // keys 64h..64h+63 sit in slot columns [64h, 64h+32)
+                if (!(a.dbg & 10)) {
+                  if (CL > 1)   // B = this CTA's 64 head-dim columns of V (one 64-wide block)
+                    tc::mma_bf16_ts_cg2(tO, tS(gt % 3) + (k >> 2) * 64 + (k & 3) * 8,
+                                        tc::sw128_mnmajor_desc(va + k * 2048, kAttnBKV * 128), idO, (t | k) != 0);
+                  else
+                    tc::mma_bf16_ts(tO, tS(gt % 3) + (k >> 2) * 64 + (k & 3) * 8,
+                                    tc::sw128_mnmajor_desc(va + k * 2048, kAttnBKV * 128), idO, (t | k) != 0);
+                }
+              }
+              commit(v_empty + (gt % VS));
+              commit(pv_done + gt % 3);
+            }
+            __syncwarp();
           }
-          __syncwarp();
+          gi += nt;
+          g = s.gs;
+          ++sg;
         }
-        gi += nt;
-        g = s.gs;
-        ++sg;
       }
     }
   } else if (warp <= 9) {
@@ -501,205 +552,208 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
     };
     long long g = t1;
     int gi = 0, sg = 0;
-    while (g > t0) {
-      const Seg s = seg_before(g);
-      const int nt = s.je - s.jb;
-      const int Lk = a.cross ? a.Lk_cross : td->e[s.e].nvalid * a.L;
-      float m_used = -INFINITY;   // row max the current P / O are relative to (log2 domain)
-      float l = 0.f;              // this half's share of the row sum
-      for (int t = 0; t < nt; ++t) {
-        const int gt = gi + t;
-        const int b = gt % 3;
-        tc::mbar_wait(s_full + b, (gt / 3) & 1);
-        if (quarter == 0) ATTN_TRACE(4 + 2 * half, gt);
-        tc::tc_fence_after();
-        if (a.dbg & 1) {   // timing experiment: no softmax work, P = 0
-          uint32_t z[32];
-#pragma unroll
-          for (int i = 0; i < 32; ++i) z[i] = 0u;
-          tc::tmem_st32(tS(b) + lane_off + half * HC, z);
+    for (int rg = 0; rg < nrg; ++rg) {
+      range_of(rg, t0, g);
+      while (g > t0) {
+        const Seg s = seg_before(g);
+        const int nt = s.je - s.jb;
+        const int Lk = a.cross ? a.Lk_cross : td->e[s.e].nvalid * a.L;
+        float m_used = -INFINITY;   // row max the current P / O are relative to (log2 domain)
+        float l = 0.f;              // this half's share of the row sum
+        for (int t = 0; t < nt; ++t) {
+          const int gt = gi + t;
+          const int b = gt % 3;
+          tc::mbar_wait(s_full + b, (gt / 3) & 1);
+          if (quarter == 0) ATTN_TRACE(4 + 2 * half, gt);
+          tc::tc_fence_after();
+          if (a.dbg & 1) {   // timing experiment: no softmax work, P = 0
+            uint32_t z[32];
+  #pragma unroll
+            for (int i = 0; i < 32; ++i) z[i] = 0u;
+            tc::tmem_st32(tS(b) + lane_off + half * HC, z);
+            tc::tmem_st_wait();
+            l = 1.f;
+            m_used = 0.f;
+            tc::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) arrive_lead(p_full + b);
+            if (quarter == 0) ATTN_TRACE(5 + 2 * half, gt);
+            continue;
+          }
+          float sv[HC];
+          {
+            uint32_t r[HC];
+  #pragma unroll
+            for (int cc = 0; cc < HC / 32; ++cc)
+              tc::tmem_ld32(tS(b) + lane_off + half * HC + cc * 32, *reinterpret_cast<uint32_t(*)[32]>(r + cc * 32));
+            tc::tmem_ld_wait();
+  #pragma unroll
+            for (int i = 0; i < HC; ++i) sv[i] = __uint_as_float(r[i]);
+          }
+          if (quarter == 0) ATTN_TRACE(10 + 2 * half, gt);
+          const int kvalid = Lk - (s.jb + t) * kAttnBKV - half * HC;
+          const bool full_tile = kvalid >= HC;
+          if (!full_tile) {
+  #pragma unroll
+            for (int i = 0; i < HC; ++i) sv[i] = (i < kvalid) ? sv[i] : -INFINITY;
+          }
+          float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};   // 4 independent chains
+  #pragma unroll
+          for (int i = 0; i < HC; i += 8) {
+  #pragma unroll
+            for (int k = 0; k < 4; ++k) mq[k] = fmaxf(mq[k], fmaxf(sv[i + 2 * k], sv[i + 2 * k + 1]));
+          }
+          float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3])) * a.scale_log2;
+          // row max over both key halves (both warps then take the same rescale decision)
+          xm[((gt & 1) * 2 + half) * 128 + row] = mx;
+          pair_sync();
+          mx = fmaxf(mx, xm[((gt & 1) * 2 + (half ^ 1)) * 128 + row]);
+          if (quarter == 0) ATTN_TRACE(11 + 2 * half, gt);
+          // lazy rescale: P / O stay relative to m_used until the max grows by > 2^8
+          if (mx > m_used + 8.f) {
+            if (t > 0) {     // O row (this half's HD/2 columns) *= 2^(m_used - m_new) once PV_{t-1} landed
+              tc::mbar_wait(pv_done + (gt - 1) % 3, ((gt - 1) / 3) & 1);
+              tc::tc_fence_after();
+              const float alpha = ex2(m_used - mx);
+              l *= alpha;
+  #pragma unroll
+              for (int cc = 0; cc < HO / 16; ++cc) {
+                uint32_t r[16];
+                const uint32_t ta = tO + lane_off + half * HO + cc * 16;
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
+                    "[%16];"
+                    : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                      "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                      "=r"(r[15])
+                    : "r"(ta));
+                tc::tmem_ld_wait();
+  #pragma unroll
+                for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
+                tc::tmem_st16(ta, r);
+              }
+              tc::tmem_st_wait();
+            }
+            m_used = mx;
+          }
+          // P = exp2(s * scale - m_used) -> bf16 pairs over this half's own S columns (A
+          // operand of the PV MMA); a row with no valid key yet writes P = 0
+          const float msub = m_used == -INFINITY ? 0.f : m_used;
+          const uint64_t sc2 = f2pack(a.scale_log2, a.scale_log2), nm2 = f2pack(-msub, -msub);
+          uint32_t pk[HC / 2];
+          // full tiles move a share of the exponentials to the FMA pipe (the MUFU alone would
+          // need 8 cycles per warp instruction x 64 per half-row: the MMA time of a tile)
+          const float rs = full_tile ? p_row<HC, true>(sv, pk, sc2, nm2) : p_row<HC, false>(sv, pk, sc2, nm2);
+          tc::tmem_st32(tS(b) + lane_off + half * HC, pk);
           tc::tmem_st_wait();
-          l = 1.f;
-          m_used = 0.f;
+          l += rs;
           tc::tc_fence_before();
           __syncwarp();
           if (lane == 0) arrive_lead(p_full + b);
           if (quarter == 0) ATTN_TRACE(5 + 2 * half, gt);
-          continue;
         }
-        float sv[HC];
-        {
-          uint32_t r[HC];
-#pragma unroll
-          for (int cc = 0; cc < HC / 32; ++cc)
-            tc::tmem_ld32(tS(b) + lane_off + half * HC + cc * 32, *reinterpret_cast<uint32_t(*)[32]>(r + cc * 32));
-          tc::tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < HC; ++i) sv[i] = __uint_as_float(r[i]);
-        }
-        if (quarter == 0) ATTN_TRACE(10 + 2 * half, gt);
-        const int kvalid = Lk - (s.jb + t) * kAttnBKV - half * HC;
-        const bool full_tile = kvalid >= HC;
-        if (!full_tile) {
-#pragma unroll
-          for (int i = 0; i < HC; ++i) sv[i] = (i < kvalid) ? sv[i] : -INFINITY;
-        }
-        float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};   // 4 independent chains
-#pragma unroll
-        for (int i = 0; i < HC; i += 8) {
-#pragma unroll
-          for (int k = 0; k < 4; ++k) mq[k] = fmaxf(mq[k], fmaxf(sv[i + 2 * k], sv[i + 2 * k + 1]));
-        }
-        float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3])) * a.scale_log2;
-        // row max over both key halves (both warps then take the same rescale decision)
-        xm[((gt & 1) * 2 + half) * 128 + row] = mx;
+        // end of segment: last PV landed -> O / (l_half0 + l_half1), this half's columns
+        const int gl = gi + nt - 1;   // last tile of the segment
+        xl[half * 128 + row] = l;
+        tc::mbar_wait(pv_done + gl % 3, (gl / 3) & 1);
+        tc::tc_fence_after();
         pair_sync();
-        mx = fmaxf(mx, xm[((gt & 1) * 2 + (half ^ 1)) * 128 + row]);
-        if (quarter == 0) ATTN_TRACE(11 + 2 * half, gt);
-        // lazy rescale: P / O stay relative to m_used until the max grows by > 2^8
-        if (mx > m_used + 8.f) {
-          if (t > 0) {     // O row (this half's HD/2 columns) *= 2^(m_used - m_new) once PV_{t-1} landed
-            tc::mbar_wait(pv_done + (gt - 1) % 3, ((gt - 1) / 3) & 1);
-            tc::tc_fence_after();
-            const float alpha = ex2(m_used - mx);
-            l *= alpha;
-#pragma unroll
-            for (int cc = 0; cc < HO / 16; ++cc) {
-              uint32_t r[16];
-              const uint32_t ta = tO + lane_off + half * HO + cc * 16;
-              asm volatile(
-                  "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
-                  "[%16];"
-                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-                    "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
-                    "=r"(r[15])
-                  : "r"(ta));
-              tc::tmem_ld_wait();
-#pragma unroll
-              for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-              tc::tmem_st16(ta, r);
+        const float lt = l + xl[(half ^ 1) * 128 + row];
+        const bool partial = s.je < s.J;               // head / middle piece of a unit: hand on
+        const bool finisher = !partial && s.jb > 0;    // tail piece: merge the earlier pieces
+        const int slot = c * CL + cr;
+        const int qr = s.q0 + row;
+        // partial layout [slot][half][granule j][row][4]: a warp moves 32 rows x 16 B at once
+        auto part_at = [&](int sl, int j) {
+          return reinterpret_cast<float4*>(a.part_o) + (size_t(sl * 2 + half) * (HO / 4) + j) * kAttnBQ + row;
+        };
+        int c_first = c;
+        float wown = 1.f, den = lt, Mfin = m_used;
+        if (finisher) {   // pieces of this unit from CTAs c_first .. c-1 (their first-visited segment)
+          c_first = geo.cta_of(s.ustart, G);
+          if (warp == 2 && lane == 0) {
+            for (int cc = c_first; cc < c; ++cc) {
+              const int* f = a.flags + cc * CL + cr;
+              int v = 0;
+              do {
+                asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+              } while (v == 0);
             }
-            tc::tmem_st_wait();
           }
-          m_used = mx;
-        }
-        // P = exp2(s * scale - m_used) -> bf16 pairs over this half's own S columns (A
-        // operand of the PV MMA); a row with no valid key yet writes P = 0
-        const float msub = m_used == -INFINITY ? 0.f : m_used;
-        const uint64_t sc2 = f2pack(a.scale_log2, a.scale_log2), nm2 = f2pack(-msub, -msub);
-        uint32_t pk[HC / 2];
-        // full tiles move a share of the exponentials to the FMA pipe (the MUFU alone would
-        // need 8 cycles per warp instruction x 64 per half-row: the MMA time of a tile)
-        const float rs = full_tile ? p_row<HC, true>(sv, pk, sc2, nm2) : p_row<HC, false>(sv, pk, sc2, nm2);
-        tc::tmem_st32(tS(b) + lane_off + half * HC, pk);
-        tc::tmem_st_wait();
-        l += rs;
-        tc::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) arrive_lead(p_full + b);
-        if (quarter == 0) ATTN_TRACE(5 + 2 * half, gt);
-      }
-      // end of segment: last PV landed -> O / (l_half0 + l_half1), this half's columns
-      const int gl = gi + nt - 1;   // last tile of the segment
-      xl[half * 128 + row] = l;
-      tc::mbar_wait(pv_done + gl % 3, (gl / 3) & 1);
-      tc::tc_fence_after();
-      pair_sync();
-      const float lt = l + xl[(half ^ 1) * 128 + row];
-      const bool partial = s.je < s.J;               // head / middle piece of a unit: hand on
-      const bool finisher = !partial && s.jb > 0;    // tail piece: merge the earlier pieces
-      const int slot = c * CL + cr;
-      const int qr = s.q0 + row;
-      // partial layout [slot][half][granule j][row][4]: a warp moves 32 rows x 16 B at once
-      auto part_at = [&](int sl, int j) {
-        return reinterpret_cast<float4*>(a.part_o) + (size_t(sl * 2 + half) * (HO / 4) + j) * kAttnBQ + row;
-      };
-      int c_first = c;
-      float wown = 1.f, den = lt, Mfin = m_used;
-      if (finisher) {   // pieces of this unit from CTAs c_first .. c-1 (their first-visited segment)
-        c_first = geo.cta_of(s.ustart, G);
-        if (warp == 2 && lane == 0) {
+          asm volatile("bar.sync 1, 256;" ::: "memory");
+          float M = m_used;
+          for (int cc = c_first; cc < c; ++cc) M = fmaxf(M, __ldcg(a.part_ml + (size_t(cc * CL + cr) * kAttnBQ + row) * 2));
+          Mfin = M;
+          wown = m_used == -INFINITY ? 0.f : ex2(m_used - M);
+          den = lt * wown;
           for (int cc = c_first; cc < c; ++cc) {
-            const int* f = a.flags + cc * CL + cr;
-            int v = 0;
-            do {
-              asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-            } while (v == 0);
+            const float2 ml = __ldcg(reinterpret_cast<const float2*>(a.part_ml) + size_t(cc * CL + cr) * kAttnBQ + row);
+            den += (ml.x == -INFINITY ? 0.f : ex2(ml.x - M)) * ml.y;
           }
         }
-        asm volatile("bar.sync 1, 256;" ::: "memory");
-        float M = m_used;
-        for (int cc = c_first; cc < c; ++cc) M = fmaxf(M, __ldcg(a.part_ml + (size_t(cc * CL + cr) * kAttnBQ + row) * 2));
-        Mfin = M;
-        wown = m_used == -INFINITY ? 0.f : ex2(m_used - M);
-        den = lt * wown;
-        for (int cc = c_first; cc < c; ++cc) {
-          const float2 ml = __ldcg(reinterpret_cast<const float2*>(a.part_ml) + size_t(cc * CL + cr) * kAttnBQ + row);
-          den += (ml.x == -INFINITY ? 0.f : ex2(ml.x - M)) * ml.y;
-        }
-      }
-      const float inv = partial ? 1.f : 1.f / den;
-      bf16* orow = reinterpret_cast<bf16*>(a.o) + size_t(s.e * a.L + qr) * a.ldo + s.h * HD + half * HO;
-#pragma unroll
-      for (int cc = 0; cc < HO / 32; ++cc) {
-        uint32_t r0[32];
-        tc::tmem_ld32(tO + lane_off + half * HO + cc * 32, r0);
-        tc::tmem_ld_wait();
-        float o[32];
-        if (partial) {
-#pragma unroll
-          for (int jj = 0; jj < 8; ++jj)
-            __stcg(part_at(slot, cc * 8 + jj), make_float4(__uint_as_float(r0[4 * jj]), __uint_as_float(r0[4 * jj + 1]),
-                                                          __uint_as_float(r0[4 * jj + 2]),
-                                                          __uint_as_float(r0[4 * jj + 3])));
-          continue;
-        }
-#pragma unroll
-        for (int i = 0; i < 32; ++i) o[i] = __uint_as_float(r0[i]) * wown;
-        if (finisher) {
-          const float M = Mfin;
-          for (int k = c_first; k < c; ++k) {
-            const float mk = __ldcg(a.part_ml + (size_t(k * CL + cr) * kAttnBQ + row) * 2);
-            const float wk = mk == -INFINITY ? 0.f : ex2(mk - M);
-#pragma unroll
-            for (int jj = 0; jj < 8; ++jj) {
-              const float4 p4 = __ldcg(part_at(k * CL + cr, cc * 8 + jj));
-              o[4 * jj] += wk * p4.x;
-              o[4 * jj + 1] += wk * p4.y;
-              o[4 * jj + 2] += wk * p4.z;
-              o[4 * jj + 3] += wk * p4.w;
+        const float inv = partial ? 1.f : 1.f / den;
+        bf16* orow = reinterpret_cast<bf16*>(a.o) + size_t(s.e * a.L + qr) * a.ldo + s.h * HD + half * HO;
+  #pragma unroll
+        for (int cc = 0; cc < HO / 32; ++cc) {
+          uint32_t r0[32];
+          tc::tmem_ld32(tO + lane_off + half * HO + cc * 32, r0);
+          tc::tmem_ld_wait();
+          float o[32];
+          if (partial) {
+  #pragma unroll
+            for (int jj = 0; jj < 8; ++jj)
+              __stcg(part_at(slot, cc * 8 + jj), make_float4(__uint_as_float(r0[4 * jj]), __uint_as_float(r0[4 * jj + 1]),
+                                                            __uint_as_float(r0[4 * jj + 2]),
+                                                            __uint_as_float(r0[4 * jj + 3])));
+            continue;
+          }
+  #pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = __uint_as_float(r0[i]) * wown;
+          if (finisher) {
+            const float M = Mfin;
+            for (int k = c_first; k < c; ++k) {
+              const float mk = __ldcg(a.part_ml + (size_t(k * CL + cr) * kAttnBQ + row) * 2);
+              const float wk = mk == -INFINITY ? 0.f : ex2(mk - M);
+  #pragma unroll
+              for (int jj = 0; jj < 8; ++jj) {
+                const float4 p4 = __ldcg(part_at(k * CL + cr, cc * 8 + jj));
+                o[4 * jj] += wk * p4.x;
+                o[4 * jj + 1] += wk * p4.y;
+                o[4 * jj + 2] += wk * p4.z;
+                o[4 * jj + 3] += wk * p4.w;
+              }
             }
           }
-        }
-        if (qr < a.L) {
-          uint32_t pk[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            __nv_bfloat162 b2 = __floats2bfloat162_rn(o[2 * i] * inv, o[2 * i + 1] * inv);
-            pk[i] = *reinterpret_cast<uint32_t*>(&b2);
+          if (qr < a.L) {
+            uint32_t pk[16];
+  #pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              __nv_bfloat162 b2 = __floats2bfloat162_rn(o[2 * i] * inv, o[2 * i + 1] * inv);
+              pk[i] = *reinterpret_cast<uint32_t*>(&b2);
+            }
+  #pragma unroll
+            for (int i = 0; i < 4; ++i)
+              reinterpret_cast<uint4*>(orow + cc * 32)[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
           }
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-            reinterpret_cast<uint4*>(orow + cc * 32)[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
         }
+        if (partial) {   // publish the piece: (m, l) of the row, then one release of the flag
+          if (half == 0) __stcg(reinterpret_cast<float2*>(a.part_ml) + size_t(slot) * kAttnBQ + row, make_float2(m_used, lt));
+          __threadfence();
+          asm volatile("bar.sync 1, 256;" ::: "memory");
+          if (warp == 2 && lane == 0) asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(a.flags + slot), "r"(1) : "memory");
+        }
+        if (finisher) {   // merged: re-arm the contributors' flags for the next launch
+          asm volatile("bar.sync 1, 256;" ::: "memory");
+          if (warp == 2 && lane == 0)
+            for (int cc = c_first; cc < c; ++cc) a.flags[cc * CL + cr] = 0;
+        }
+        tc::tc_fence_before();
+        pair_sync();   // xl reusable
+        if (lane == 0) arrive_lead(o_empty);
+        gi += nt;
+        g = s.gs;
+        ++sg;
       }
-      if (partial) {   // publish the piece: (m, l) of the row, then one release of the flag
-        if (half == 0) __stcg(reinterpret_cast<float2*>(a.part_ml) + size_t(slot) * kAttnBQ + row, make_float2(m_used, lt));
-        __threadfence();
-        asm volatile("bar.sync 1, 256;" ::: "memory");
-        if (warp == 2 && lane == 0) asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(a.flags + slot), "r"(1) : "memory");
-      }
-      if (finisher) {   // merged: re-arm the contributors' flags for the next launch
-        asm volatile("bar.sync 1, 256;" ::: "memory");
-        if (warp == 2 && lane == 0)
-          for (int cc = c_first; cc < c; ++cc) a.flags[cc * CL + cr] = 0;
-      }
-      tc::tc_fence_before();
-      pair_sync();   // xl reusable
-      if (lane == 0) arrive_lead(o_empty);
-      gi += nt;
-      g = s.gs;
-      ++sg;
     }
   }
   tc::tc_fence_before();
@@ -731,6 +785,13 @@ inline bool tc_attn_enabled() { return true; }
 inline int attn_pick_per_unit(long long units, long long tiles, int num_sms) {
   (void)tiles;
   return units <= num_sms ? 1 : 0;
+}
+
+// Hybrid stream-K (whole units round-robin, then an even split of the last partial
+// round); SDV2_ATTN_RR=0 gives the plain even split of all tiles.
+inline int attn_rr() {
+  static const int v = getenv("SDV2_ATTN_RR") ? atoi(getenv("SDV2_ATTN_RR")) : 1;
+  return v;
 }
 
 inline int attn_cluster() {

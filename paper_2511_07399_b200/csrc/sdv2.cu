@@ -434,6 +434,7 @@ sdv2_status attention(sdv2_handle* h, const AttnArgs& aa, int Mrows_entries, dou
         const int CL = h->hd == 128 ? attn_cluster() : 1, QP = (ta.QT + CL - 1) / CL;   // decide on query-tile groups
         ta.per_unit = attn_pick_per_unit((long long)Mrows_entries * ta.H * QP, tiles * QP / ta.QT,
                                          h->aplan.num_sms / CL);
+        ta.rr = attn_rr();
       }
       const void *Kb, *Vb;
       long long kv_rows;
@@ -1232,17 +1233,17 @@ extern "C" sdv2_status sdv2_debug_attention(const void* q, const void* K, const 
     ready = true;
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  // one active entry; written once per scratch buffer (a pageable copy per call would
-  // serialise the stream and pollute kernel timings)
-  static void* last_scratch = nullptr;
-  if (scratch != last_scratch) {
-    TickDesc tdh;
-    std::memset(&tdh, 0, sizeof(tdh));
-    tdh.n_active = 1;
-    tdh.e[0].active = 1;
-    if (cudaMemcpy(scratch, &tdh, sizeof(tdh), cudaMemcpyHostToDevice) != cudaSuccess) return SDV2_E_CUDA;
-    last_scratch = scratch;
+  // one active entry, written on every call from a pinned host copy (asynchronous: no
+  // stream serialisation; a caller's new scratch tensor may reuse a freed address, so
+  // "written once per buffer" is not safe)
+  static TickDesc* tdh = nullptr;
+  if (!tdh) {
+    if (cudaMallocHost(&tdh, sizeof(TickDesc)) != cudaSuccess) return SDV2_E_CUDA;
+    std::memset(tdh, 0, sizeof(TickDesc));
+    tdh->n_active = 1;
+    tdh->e[0].active = 1;
   }
+  if (cudaMemcpyAsync(scratch, tdh, sizeof(TickDesc), cudaMemcpyHostToDevice, s) != cudaSuccess) return SDV2_E_CUDA;
   static float* part = nullptr;
   if (!part && cudaMalloc(&part, attn_scratch_floats(kMaxSMs, 128) * 4) != cudaSuccess) return SDV2_E_CUDA;
   AttnTcArgs ta{};
@@ -1261,6 +1262,7 @@ extern "C" sdv2_status sdv2_debug_attention(const void* q, const void* K, const 
   ta.kv_lane_rows = 0;
   const long long tiles = (long long)H * ta.QT * ((Lk + kAttnBKV - 1) / kAttnBKV);
   ta.per_unit = getenv("SDV2_ATTN_PER_UNIT") ? atoi(getenv("SDV2_ATTN_PER_UNIT")) : 0;
+  ta.rr = attn_rr();
   ta.dbg = getenv("SDV2_ATTN_DBG") ? atoi(getenv("SDV2_ATTN_DBG")) : 0;
   // SDV2_ATTN_TRACE=<file>: per-tile clock64 stamps of CTA 0 (pipeline analysis)
   const char* trace_path = getenv("SDV2_ATTN_TRACE");

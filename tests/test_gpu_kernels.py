@@ -63,7 +63,10 @@ def test_tc_gemm(M, N, K, epi):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("Lq,Lk,H,hd", [(16, 48, 2, 64), (1560, 7800, 2, 128), (1560, 512, 3, 128), (128, 128, 1, 128), (1560, 7800, 12, 128), (300, 1000, 5, 64),
-                                        (200, 300, 2, 64), (1024, 5120, 2, 128)])
+                                        (200, 300, 2, 64), (1024, 5120, 2, 128),
+                                        # hybrid schedule: 384 units = one whole-unit round + a split
+                                        # of the remaining 236; 148 units (split only)
+                                        (4096, 1024, 12, 128), (4736, 256, 4, 128)])
 def test_tc_attention(Lq, Lk, H, hd):
     import torch
     L_ = lib()
