@@ -66,7 +66,9 @@ def test_tc_gemm(M, N, K, epi):
                                         (200, 300, 2, 64), (1024, 5120, 2, 128),
                                         # hybrid schedule: 384 units = one whole-unit round + a split
                                         # of the remaining 236; 148 units (split only)
-                                        (4096, 1024, 12, 128), (4736, 256, 4, 128)])
+                                        (4096, 1024, 12, 128), (4736, 256, 4, 128),
+                                        # cross-attention shape at n = 1 (156 units of 4 key tiles)
+                                        (1560, 512, 12, 128)])
 def test_tc_attention(Lq, Lk, H, hd):
     import torch
     L_ = lib()
