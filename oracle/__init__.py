@@ -22,16 +22,25 @@ It shares no code with the CUDA path.  Floating point runs in a caller-chosen
 dtype (float64 for the parity pins, float32 = the north-star "fp32 oracle");
 sinusoid / RoPE tables / Box–Muller / cosines / motion statistics are fp64.
 
-Parity status per function:
+Parity status per function (DESIGN.md §3 names the pin of every function):
   pinned:   philox (Random123 KAT), motion controller (SPEC worked examples and
             closed forms), sink refresh, rope_position, ring/sink metadata
             (Appendix A trace), partition (brute force + SPEC examples), norms /
             activations / attention (torch library routines + closed forms),
             patchify/unpatchify (torch conv3d / einsum), RoPE (relative
-            invariance, identity at 0), sampler (perfect-denoiser closed form),
-            time embedding (t=0 closed form), residual wiring (identity block),
-            streaming cache == brute-force full attention, pipelined ==
-            sequential (order independence), causality.
+            invariance, identity at 0, the per-group frequency law at hand-computed
+            angles, interleaved pair rotation), token positions (height/width on a
+            non-square latent, tied to patchify), rms_g over the full dim,
+            time embedding (closed form with one-hot weights: t = 1000 sigma, SiLU
+            placement, cos-first sinusoid, [6, d] view), text embedding / prompt K,V
+            (closed form), block wiring (modulation row order, gates, ungated cross
+            residual, norm3 affine, cross q RMS: closed forms), head (shift/scale
+            rows), sampler (perfect-denoiser closed form), residual wiring
+            (identity block), streaming cache == brute-force full attention,
+            stream-level RoPE-reset invariance with m = 0 (P2(iii)), pipelined ==
+            sequential (order independence), causality.  tests/test_oracle_mutations.py
+            shows every closed-form pin fails under its plausible misreadings.
   parity unpinned: the full random-init model output as a whole (no trained
-            weights or published tensors exist; only oracle <-> GPU).
+            weights or published tensors exist); it is the composition of the
+            pinned functions, checked only oracle <-> GPU.
 """
