@@ -378,8 +378,14 @@ def main():
     ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(sg.CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--pp-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="stage transport for --gpus > 1 (gloo: host staging, several ranks on one GPU)")
+    ap.add_argument("--lib", default=None, help="alternative libsdv2.so build (A/B timing)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.lib:
+        from paper_2511_07399_b200.sdv2 import load_library
+        load_library(os.path.abspath(args.lib))
     cfg = sg.CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg)

@@ -20,9 +20,13 @@
  *  - Every call returns sdv2_status; nothing throws across the ABI.
  *  - All device work is enqueued on the stream given to sdv2_create; calls return
  *    before completion.  A handle is single-owner and not thread-safe.
- *  - The library never calls cudaMalloc: all device memory is the caller-owned
- *    workspace (sdv2_workspace_bytes), carved at create.  The small pinned host
- *    staging area for per-tick descriptors is allocated with cudaHostAlloc.
+ *  - The library never calls cudaMalloc on the product path: all device memory is the
+ *    caller-owned workspace (sdv2_workspace_bytes), carved at create (weights, KV lanes,
+ *    activations, attention split partials and hand-off flags).  The small pinned host
+ *    staging area for per-tick descriptors is allocated with cudaHostAlloc; sdv2_destroy
+ *    frees it.  (The kernel-level test hooks at the end own a private scratch.)
+ *  - No environment variable changes what the product path computes or how fast:
+ *    execution choices are the explicit sdv2_exec_options given to sdv2_create.
  *  - Tensors are row-major, fp32 unless stated.
  */
 #ifndef SDV2_H
@@ -94,7 +98,7 @@ typedef struct {
   const float* timesteps;
   int32_t num_timesteps;
   int32_t rope_reset_frames;    /* T_reset >= max(m, W) * T', T_reset + T' <= 4096 */
-  int32_t motion_k;             /* window of k+1 motion values, 0 <= k < 64 */
+  int32_t motion_k;             /* window of k+1 motion values, 0 <= k <= 62 */
   float motion_sigma;           /* > 0 */
   float s_min, s_max;           /* 0 <= s_min < s_max <= 1 */
   float ema_lambda;             /* in (0, 1] */
@@ -151,23 +155,45 @@ typedef struct {
 
 typedef struct sdv2_handle sdv2_handle;
 
+/* Execution options (NULL = the defaults in brackets).  None changes the numerics:
+ * every GEMM configuration the tuner may pick reduces each output element over K in
+ * the same order (no split-K), so results are bit-identical across tunings.
+ *   tune_gemms   [1] time every candidate tile configuration of each projection GEMM
+ *                    shape at create (CUDA-graph replay on the real buffers) and keep
+ *                    the fastest; 0 = the tile-balance model's pick, no timing.
+ *   pdl          [1] programmatic dependent launch between the call's kernels.
+ *   graphs       [1] replay the per-call device work from CUDA graphs. */
+typedef struct {
+  int32_t tune_gemms;
+  int32_t pdl;
+  int32_t graphs;
+} sdv2_exec_options;
+
 /* Bytes of device workspace a handle needs (0 on invalid descriptors). */
 size_t sdv2_workspace_bytes(const sdv2_model_desc* md, const sdv2_geometry* g,
                             const sdv2_pipeline_desc* pp, sdv2_precision prec);
 
 /* Validate, carve the workspace, pack this rank's weights (fp32 -> bf16 K-major for
- * SDV2_BF16), build TMA descriptors.  `stream` is a cudaStream_t (NULL = legacy). */
+ * SDV2_BF16), build TMA descriptors.  `stream` is a cudaStream_t (NULL = legacy);
+ * `opts` may be NULL (defaults).  Errors: SDV2_E_SHAPE / SDV2_E_UNSUPPORTED for shapes,
+ * SDV2_E_INVALID for a bad pipeline descriptor or (steps - 1) * world + 1 > 128 (the
+ * chunk-record ring), SDV2_E_WORKSPACE, SDV2_E_CUDA (text in sdv2_last_error; the handle
+ * is then returned in *out so the caller can read the text and destroy it). */
 sdv2_status sdv2_create(const sdv2_model_desc* md, const sdv2_geometry* g,
                         const sdv2_pipeline_desc* pp, sdv2_precision prec,
                         const sdv2_weights* w, void* workspace, size_t workspace_bytes,
-                        int device, void* stream, sdv2_handle** out);
+                        int device, void* stream, const sdv2_exec_options* opts, sdv2_handle** out);
 
 /* Start a new stream: zero KV lanes, metadata and controller state; embed the prompt
  * (host [text_len, text_dim] fp32) and compute every local block's cross K/V. */
 sdv2_status sdv2_reset_stream(sdv2_handle* h, const sdv2_stream_desc* sd, const float* prompt_host);
 
-/* Switch prompt: takes effect from the next chunk admitted (the next call); in-flight
- * entries keep the prompt they were admitted with (two prompt versions resident). */
+/* Switch prompt: takes effect from the next chunk admitted (the next
+ * call); in-flight entries keep the prompt they were admitted with.  Two prompt versions
+ * are resident, so a switch must come at least (steps - 1) * world calls after the
+ * previous one (the oldest chunk admitted under the version being overwritten has then
+ * left the pipeline); an earlier switch returns SDV2_E_STATE and changes nothing.
+ * SDV2_E_INVALID for a zero-norm prompt mean. */
 sdv2_status sdv2_set_prompt(sdv2_handle* h, const float* prompt_host);
 
 /* One stage-tick.  Rank 0: chunk_latent [C, T', h, w] fp32 (host or device pointer)
@@ -210,6 +236,15 @@ sdv2_status sdv2_profile_read(sdv2_handle* h, sdv2_profile* out);
 sdv2_status sdv2_debug_gemm(const void* A, const void* W, const float* bias, void* out, int32_t M, int32_t N,
                             int32_t K, int32_t epi, const float* mod, const float* e0, int32_t gate_row, int32_t L,
                             void* stream);
+
+/* Kernel-level test hooks: the configurations the create-time GEMM tuner chooses from
+ * for shape (M, N, K, epi) as (cluster size MC, tile width BN, stream-K SK, early residual
+ * fetch XE) quadruples, and one GEMM launched with an explicit configuration. */
+sdv2_status sdv2_debug_gemm_candidates(int32_t M, int32_t N, int32_t K, int32_t epi, int32_t* cfg4,
+                                       int32_t max_cfgs, int32_t* count);
+sdv2_status sdv2_debug_gemm_cfg(const void* A, const void* W, const float* bias, void* out, int32_t M, int32_t N,
+                                int32_t K, int32_t epi, const float* mod, const float* e0, int32_t gate_row,
+                                int32_t L, const int32_t* cfg4, void* stream);
 
 /* Kernel-level test hook: tensor-core attention softmax(q K^T / sqrt(hd)) V for one
  * query block q [Lq, H*hd] over keys K/V [Lk, H*hd] (bf16, device) -> o [Lq, H*hd]

@@ -788,28 +788,27 @@ inline int attn_pick_per_unit(long long units, long long tiles, int num_sms) {
 }
 
 // Hybrid stream-K (whole units round-robin, then an even split of the last partial
-// round); SDV2_ATTN_RR=0 gives the plain even split of all tiles.
-inline int attn_rr() {
-  static const int v = getenv("SDV2_ATTN_RR") ? atoi(getenv("SDV2_ATTN_RR")) : 1;
-  return v;
-}
+// round) is the schedule; rr = 0 (the plain even split of all tiles) stays reachable
+// through the kernel-level test hook only.
+constexpr int kAttnRR = 1;
+inline int attn_rr() { return kAttnRR; }
 
-inline int attn_cluster() {
-  const char* e = getenv("SDV2_ATTN_CL");
-  return e ? (atoi(e) == 2 ? 2 : 1) : 1;   // measured neutral at the 1.3B shapes: off by default
-}
+// CTA-pair attention (cluster 2) was measured neutral at the 1.3B shapes and slower at
+// 14B (84 vs 57 ms/step): single-CTA units.
+constexpr int kAttnCluster = 1;
+inline int attn_cluster() { return kAttnCluster; }
 
-inline bool attn_plan_init(AttnPlan& p, PFN_encodeTiled enc, int num_sms) {
+// flags: [num_sms] ints of caller-owned device memory (the handle carves them from
+// its workspace and zeroes them once; the kernel leaves them zero after every launch).
+inline bool attn_plan_init(AttnPlan& p, PFN_encodeTiled enc, int num_sms, int* flags) {
   p.encode = enc;
   p.num_sms = num_sms;
-  cudaFuncSetAttribute(attn_tc_kernel<128, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, AttnSmem<128>::total);
-  cudaFuncSetAttribute(attn_tc_kernel<64, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, AttnSmem<64>::total);
-  cudaFuncSetAttribute(attn_tc_kernel<128, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, AttnSmem<128, 2>::total);
-  if (!p.flags) {
-    if (cudaMalloc(&p.flags, size_t(num_sms) * sizeof(int)) != cudaSuccess ||
-        cudaMemset(p.flags, 0, size_t(num_sms) * sizeof(int)) != cudaSuccess)
-      return false;
-  }
+  if (!flags) return false;
+  if (cudaFuncSetAttribute(attn_tc_kernel<128, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, AttnSmem<128>::total) != cudaSuccess ||
+      cudaFuncSetAttribute(attn_tc_kernel<64, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, AttnSmem<64>::total) != cudaSuccess ||
+      cudaFuncSetAttribute(attn_tc_kernel<128, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, AttnSmem<128, 2>::total) != cudaSuccess)
+    return false;
+  p.flags = flags;
   p.ready = true;
   return true;
 }

@@ -660,14 +660,6 @@ inline bool tc_gemm_plan(TmaGemmPlan& p, std::string* err) {
   gemm_set_attr<EPI_RES_GATE, bf16, 1>(); gemm_set_attr<EPI_RES_GATE, bf16, 2>();
   gemm_set_attr<EPI_RES, bf16, 1>(); gemm_set_attr<EPI_RES, bf16, 2>();
   gemm_set_attr<EPI_STORE, float, 1>(); gemm_set_attr<EPI_STORE, float, 2>();
-  if (!p.sk_ws) {
-    if (cudaMalloc(&p.sk_ws, size_t(p.num_sms) * kGemmSkSlotFloats * sizeof(float)) != cudaSuccess ||
-        cudaMalloc(&p.sk_flags, size_t(p.num_sms) * sizeof(int)) != cudaSuccess ||
-        cudaMemset(p.sk_flags, 0, size_t(p.num_sms) * sizeof(int)) != cudaSuccess) {
-      *err = "stream-K workspace allocation failed";
-      return false;
-    }
-  }
   return true;
 }
 
@@ -782,15 +774,6 @@ inline cudaError_t gemm_dispatch(cudaStream_t s, int grid, const CUtensorMap& ma
   }
 }
 
-inline int tc_gemm_default_mc() {
-  const char* e = getenv("SDV2_GEMM_MC");
-  return e ? atoi(e) : 1;
-}
-inline int tc_gemm_default_sk() {
-  const char* e = getenv("SDV2_GEMM_SK");
-  return e ? atoi(e) : 0;
-}
-
 inline std::string gemm_key(int M, int N, int K, int epi) {
   return std::to_string(M) + ":" + std::to_string(N) + ":" + std::to_string(K) + ":" + std::to_string(epi);
 }
@@ -811,6 +794,10 @@ inline bool tc_gemm_cfg(cudaStream_t s, TmaGemmPlan& p, const void* A, const voi
   const int slots = p.num_sms / MC;
   const int grid = MC * int(work < slots ? work : slots);
   // residual x tile staged in the operand ring when no cluster gets a second tile
+  if (gc.SK && (!p.sk_ws || !p.sk_flags)) {
+    *err = "tc_gemm: stream-K needs the (test-hook) partial workspace";
+    return false;
+  }
   const GemmSk sk{gc.SK, (!gc.SK && !gc.XE && tiles <= slots) ? 1 : 0, p.sk_ws, p.sk_flags};
   cudaError_t e = MC == 2 ? gemm_dispatch<2>(s, grid, *ma, *mb, *mx, M, N, K, BN, epi, ep, sk)
                           : gemm_dispatch<1>(s, grid, *ma, *mb, *mx, M, N, K, BN, epi, ep, sk);
@@ -838,8 +825,9 @@ inline bool tc_gemm_check(int N, int K, int epi, std::string* err) {
 inline GemmCfg tc_gemm_default_cfg(const TmaGemmPlan& p, int M, int N, int epi) {
   const int num_m = (M + kGemmBM - 1) / kGemmBM;
   GemmCfg c;
-  c.MC = (num_m >= 2 && tc_gemm_default_mc() == 2) ? 2 : 1;
-  c.SK = tc_gemm_default_sk();
+  (void)num_m;
+  c.MC = 1;
+  c.SK = 0;
   const bool res = (epi == EPI_RES_GATE || epi == EPI_RES);
   const int max_bn = res ? kResMaxBN : 256;
   c.BN = c.SK ? std::min(max_bn, (N + 31) / 32 * 32) : tc_pick_bn(M, N, p.num_sms, c.MC, max_bn);
@@ -856,33 +844,36 @@ inline bool tc_gemm(cudaStream_t s, TmaGemmPlan& p, const void* A, const void* W
 }
 
 // Create-time autotuning of one GEMM shape on the real buffers: every (MC = 1, 2) x
-// tile width, plus stream-K at the three best tile widths of the balance model, by
-// CUDA-event time.  The timed launches cycle through the weights of the different
+// tile width (x early residual fetch), by CUDA-event time.  Every candidate reduces
+// each output element over K in the same order (one CTA / CTA pair walks all k-blocks
+// of its tile in order; no split-K), so the choice changes speed, never bits:
+// tests/test_gpu_kernels.py::test_gemm_configs_bitwise_identical runs every candidate.
+// Stream-K (ordered partial fix-up) changes the reduction order and is kept out of the
+// product path (it was never the fastest at the DiT shapes).  The timed launches cycle through the weights of the different
 // local blocks (Ws[0..nW)) so, as in a real step, the weights stream from HBM instead
 // of sitting in L2 after the first launch.
-inline bool tc_gemm_tune(cudaStream_t s, TmaGemmPlan& p, const void* A, const void* const* Ws, int nW, int M, int N,
-                         int K, int epi, const EpiArgs& ep, std::string* err) {
-  if (!tc_gemm_check(N, K, epi, err)) return false;
-  const std::string key = gemm_key(M, N, K, epi);
-  if (p.tuned.count(key)) return true;
+// The configurations the tuner chooses from (also listed by the test hook).
+inline std::vector<GemmCfg> tc_gemm_candidates(const TmaGemmPlan& p, int M, int N, int epi) {
   const int num_m = (M + kGemmBM - 1) / kGemmBM;
   const bool res = (epi == EPI_RES_GATE || epi == EPI_RES);
   std::vector<GemmCfg> cands;
   const int max_bn = std::min(res ? kResMaxBN : 256, (N + 31) / 32 * 32);
   for (int MC = 1; MC <= (num_m >= 2 ? 2 : 1); ++MC) {
-    std::vector<std::pair<double, int>> ranked;
-    const int num_mg = (num_m + MC - 1) / MC, slots = p.num_sms / MC;
+    const int slots = p.num_sms / MC;
     for (int bn = max_bn; bn >= std::min(64, max_bn); bn -= 32) {   // narrow N (head): BN = 32
       cands.push_back({MC, bn, 0});
       if (res && ((num_m + MC - 1) / MC) * ((N + bn - 1) / bn) <= slots) cands.push_back({MC, bn, 0, 1});
-      const int num_n = (N + bn - 1) / bn, tiles = num_mg * num_n, waves = (tiles + slots - 1) / slots;
-      const double eff = double(N) / double(num_n * bn) * double(num_m) / double(num_mg * MC) * double(tiles) /
-                         double(waves * slots);
-      ranked.push_back({-eff, -bn});
     }
-    std::sort(ranked.begin(), ranked.end());
-    for (size_t i = 0; i < ranked.size() && i < 2; ++i) cands.push_back({MC, -ranked[i].second, 1});
   }
+  return cands;
+}
+
+inline bool tc_gemm_tune(cudaStream_t s, TmaGemmPlan& p, const void* A, const void* const* Ws, int nW, int M, int N,
+                         int K, int epi, const EpiArgs& ep, std::string* err) {
+  if (!tc_gemm_check(N, K, epi, err)) return false;
+  const std::string key = gemm_key(M, N, K, epi);
+  if (p.tuned.count(key)) return true;
+  const std::vector<GemmCfg> cands = tc_gemm_candidates(p, M, N, epi);
   if (cands.empty()) {
     *err = "gemm tune: no candidate configuration";
     return false;

@@ -108,6 +108,7 @@ struct sdv2_handle {
   float* u;                   // patchified tokens [Mmax, 4C] fp32
   float* yh;                  // head output [Mmax, 4C] fp32
   float* attn_part;           // stream-K attention partials
+  int* attn_flags;            // [kMaxSMs] split-unit hand-off flags (zero between launches)
   void* head_w_tw;            // head weight [4C, d] TW
   float* t1;                  // [n, d]
   void* a;                    // [Mmax, d] TA
@@ -145,7 +146,9 @@ struct sdv2_handle {
   TickDesc* td_host_cur = nullptr;
   // CUDA graphs of the call body, keyed by (active entries, call parity)
   bool graphs = true;
-  bool pdl = true;        // programmatic dependent launch (SDV2_PDL=0 disables): +2 % fps measured
+  bool pdl = true;        // programmatic dependent launch (sdv2_exec_options.pdl): +2 % fps measured
+  bool tune = true;       // create-time GEMM tile tuning (sdv2_exec_options.tune_gemms)
+  int64_t last_switch_call = -1;   // call index of the last sdv2_set_prompt (-1: none since reset)
   cudaGraphExec_t graph_exec[2 * (kMaxSteps + 1)] = {};
   int64_t graph_launches[2 * (kMaxSteps + 1)] = {};
   // profiling (sdv2_profile_enable): event pairs around each launch, per class
@@ -252,6 +255,7 @@ size_t carve(sdv2_handle* h, void* base) {
   h->u = cv.take<float>(size_t(h->Mmax) * h->P);
   h->yh = cv.take<float>(size_t(h->Mmax) * h->P);
   h->attn_part = cv.take<float>(attn_scratch_floats(kMaxSMs, h->hd));
+  h->attn_flags = cv.take<int>(kMaxSMs);
   h->t1 = cv.take<float>(size_t(h->n) * d);
   // activation scratch, aliased by the weight staging buffer during create
   {
@@ -329,6 +333,9 @@ sdv2_status fill_dims(sdv2_handle* h, const sdv2_model_desc* md, const sdv2_geom
   } else {
     h->K = 1; h->rank = 0; h->b0 = 0; h->b1 = md->num_blocks;
   }
+  // the control plane keeps the records of the last kRecRing admitted chunks; the oldest
+  // in-flight entry is (n-1) K calls old
+  if (int64_t(h->n - 1) * h->K + 1 > kRecRing) { *why = "(steps - 1) * world + 1 exceeds the chunk-record ring"; return SDV2_E_INVALID; }
   h->nb = h->b1 - h->b0;
   return SDV2_OK;
 }
@@ -799,7 +806,7 @@ size_t sdv2_workspace_bytes(const sdv2_model_desc* md, const sdv2_geometry* g, c
 
 sdv2_status sdv2_create(const sdv2_model_desc* md, const sdv2_geometry* g, const sdv2_pipeline_desc* pp,
                         sdv2_precision prec, const sdv2_weights* w, void* workspace, size_t workspace_bytes,
-                        int device, void* stream, sdv2_handle** out) {
+                        int device, void* stream, const sdv2_exec_options* opts, sdv2_handle** out) {
   if (!out) return SDV2_E_INVALID;
   *out = nullptr;
   auto* h = new sdv2_handle();
@@ -820,7 +827,11 @@ sdv2_status sdv2_create(const sdv2_model_desc* md, const sdv2_geometry* g, const
   }
   h->device = device;
   h->stream = static_cast<cudaStream_t>(stream);
-  if (const char* e = getenv("SDV2_PDL")) h->pdl = atoi(e) != 0;
+  if (opts) {
+    h->tune = opts->tune_gemms != 0;
+    h->pdl = opts->pdl != 0;
+    h->graphs = opts->graphs != 0;
+  }
   h->ws_bytes = workspace_bytes;
   if (cudaSetDevice(device) != cudaSuccess) {
     delete h;
@@ -886,9 +897,13 @@ sdv2_status sdv2_create(const sdv2_model_desc* md, const sdv2_geometry* g, const
   }
   if (h->prec == SDV2_BF16) {
     if (!tc_gemm_plan(h->gplan, &h->err)) return fail(SDV2_E_CUDA);
-    attn_plan_init(h->aplan, h->gplan.encode, std::min(h->gplan.num_sms, kMaxSMs));
+    if (cudaMemsetAsync(h->attn_flags, 0, kMaxSMs * sizeof(int), h->stream) != cudaSuccess ||
+        !attn_plan_init(h->aplan, h->gplan.encode, std::min(h->gplan.num_sms, kMaxSMs), h->attn_flags)) {
+      h->err = "attention plan initialisation failed";
+      return fail(SDV2_E_CUDA);
+    }
   }
-  if (h->prec == SDV2_BF16 && !(getenv("SDV2_TUNE") && atoi(getenv("SDV2_TUNE")) == 0)) {
+  if (h->prec == SDV2_BF16 && h->tune) {
     // Autotune the projection GEMMs of every tick shape (M = active entries x L) on the
     // real buffers (their contents are scratch until reset_stream).
     const BlockW& B = h->bw[0];
@@ -1019,6 +1034,7 @@ sdv2_status sdv2_reset_stream(sdv2_handle* h, const sdv2_stream_desc* sd, const 
     CK(cudaStreamSynchronize(h->stream));
   }
   h->pver = 0;
+  h->last_switch_call = -1;
   sdv2_status s = set_prompt_common(h, prompt_host, 0);
   if (s != SDV2_OK) return s;
   h->stream_ready = true;
@@ -1028,11 +1044,21 @@ sdv2_status sdv2_reset_stream(sdv2_handle* h, const sdv2_stream_desc* sd, const 
 sdv2_status sdv2_set_prompt(sdv2_handle* h, const float* prompt_host) {
   if (!h || !prompt_host) return SDV2_E_INVALID;
   if (!h->stream_ready) return SDV2_E_STATE;
-  // the version slot being overwritten must not be used by an in-flight entry: the
-  // oldest in-flight chunk is call - (n-1) K; versions alternate, so require that the
-  // previous switch happened at least (n-1) K + 1 calls ago.
+  // Versions alternate between two resident slots: the switch to version v overwrites
+  // the slot of version v-2, whose last chunk was admitted at call c_{v-1} - 1 and is
+  // processed (entry j = n-1) at call c_{v-1} - 1 + (n-1) K.  The overwrite is ordered
+  // before call c_v, so it is safe iff c_v - c_{v-1} >= (n-1) K.
+  const int64_t now = h->ctl.calls();
+  if (h->last_switch_call >= 0 && now - h->last_switch_call < int64_t(h->n - 1) * h->K) {
+    h->err = "prompt switch too soon: " + std::to_string(now - h->last_switch_call) + " calls after the previous one, " +
+             std::to_string(int64_t(h->n - 1) * h->K) + " needed (two prompt versions are resident)";
+    return SDV2_E_STATE;
+  }
   sdv2_status s = set_prompt_common(h, prompt_host, h->pver + 1);
-  if (s == SDV2_OK) h->pver += 1;
+  if (s == SDV2_OK) {
+    h->pver += 1;
+    h->last_switch_call = now;
+  }
   return s;
 }
 
@@ -1160,16 +1186,72 @@ sdv2_status sdv2_destroy(sdv2_handle* h) {
 
 }  // extern "C"
 
+namespace {
+// Test-hook GEMM plan with a private stream-K partial workspace (the product path never
+// runs stream-K; the hook keeps it reachable for kernel tests).
+bool debug_gemm_plan(TmaGemmPlan*& out, std::string* err) {
+  static TmaGemmPlan plan;
+  static bool ready = false;
+  if (!ready) {
+    if (!tc_gemm_plan(plan, err)) return false;
+    if (cudaMalloc(&plan.sk_ws, size_t(plan.num_sms) * kGemmSkSlotFloats * sizeof(float)) != cudaSuccess ||
+        cudaMalloc(&plan.sk_flags, size_t(plan.num_sms) * sizeof(int)) != cudaSuccess ||
+        cudaMemset(plan.sk_flags, 0, size_t(plan.num_sms) * sizeof(int)) != cudaSuccess) {
+      *err = "test-hook stream-K workspace allocation failed";
+      return false;
+    }
+    ready = true;
+  }
+  out = &plan;
+  return true;
+}
+}  // namespace
+
+extern "C" sdv2_status sdv2_debug_gemm_candidates(int32_t M, int32_t N, int32_t K, int32_t epi, int32_t* cfg4,
+                                                  int32_t max_cfgs, int32_t* count) {
+  TmaGemmPlan* pl = nullptr;
+  std::string err;
+  if (!cfg4 || !count || !debug_gemm_plan(pl, &err)) return SDV2_E_INVALID;
+  if (!tc_gemm_check(N, K, epi, &err)) return SDV2_E_SHAPE;
+  const std::vector<GemmCfg> c = tc_gemm_candidates(*pl, M, N, epi);
+  *count = int32_t(c.size());
+  for (int i = 0; i < int(c.size()) && i < max_cfgs; ++i) {
+    cfg4[4 * i] = c[i].MC; cfg4[4 * i + 1] = c[i].BN; cfg4[4 * i + 2] = c[i].SK; cfg4[4 * i + 3] = c[i].XE;
+  }
+  return SDV2_OK;
+}
+
+extern "C" sdv2_status sdv2_debug_gemm_cfg(const void* A, const void* W, const float* bias, void* out, int32_t M,
+                                           int32_t N, int32_t K, int32_t epi, const float* mod, const float* e0,
+                                           int32_t gate_row, int32_t L, const int32_t* cfg4, void* stream) {
+  TmaGemmPlan* pl = nullptr;
+  std::string err;
+  if (!cfg4 || !debug_gemm_plan(pl, &err)) return SDV2_E_INVALID;
+  EpiArgs ep{};
+  ep.out = out;
+  ep.ldo = N;
+  ep.bias = bias;
+  ep.mod = mod;
+  ep.e0 = e0;
+  ep.gate_row = gate_row;
+  ep.L = L > 0 ? L : 1;
+  GemmCfg gc{cfg4[0], cfg4[1], cfg4[2]};
+  gc.XE = cfg4[3];
+  if (!tc_gemm_check(N, K, epi, &err) ||
+      !tc_gemm_cfg(static_cast<cudaStream_t>(stream), *pl, A, W, M, N, K, epi, ep, gc, &err)) {
+    fprintf(stderr, "sdv2_debug_gemm_cfg: %s\n", err.c_str());
+    return SDV2_E_CUDA;
+  }
+  return SDV2_OK;
+}
+
 extern "C" sdv2_status sdv2_debug_gemm(const void* A, const void* W, const float* bias, void* out, int32_t M, int32_t N,
                                        int32_t K, int32_t epi, const float* mod, const float* e0, int32_t gate_row,
                                        int32_t L, void* stream) {
-  static TmaGemmPlan plan;
-  static bool ready = false;
+  TmaGemmPlan* pl = nullptr;
   std::string err;
-  if (!ready) {
-    if (!tc_gemm_plan(plan, &err)) return SDV2_E_CUDA;
-    ready = true;
-  }
+  if (!debug_gemm_plan(pl, &err)) return SDV2_E_CUDA;
+  TmaGemmPlan& plan = *pl;
   EpiArgs ep{};
   ep.out = out;
   ep.ldo = N;
@@ -1226,10 +1308,14 @@ extern "C" sdv2_status sdv2_debug_attention(const void* q, const void* K, const 
   static TmaGemmPlan gp;
   static AttnPlan ap;
   static bool ready = false;
+  static int* flags = nullptr;
   std::string err;
   if (!ready) {
     if (!tc_gemm_plan(gp, &err)) return SDV2_E_CUDA;
-    attn_plan_init(ap, gp.encode, std::min(gp.num_sms, kMaxSMs));
+    if (cudaMalloc(&flags, kMaxSMs * sizeof(int)) != cudaSuccess ||
+        cudaMemset(flags, 0, kMaxSMs * sizeof(int)) != cudaSuccess ||
+        !attn_plan_init(ap, gp.encode, std::min(gp.num_sms, kMaxSMs), flags))
+      return SDV2_E_CUDA;
     ready = true;
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);

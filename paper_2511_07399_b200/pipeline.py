@@ -98,10 +98,34 @@ class StageTransport:
         if self.host and self.device is not None:
             self.torch.cuda.synchronize(self.device)   # device outputs complete before host copy
         works = self.dist.batch_isend_irecv(ops) if ops else []
-        self.pending.append((works, post))
+        kinds = ["recv" if o.op is self.dist.irecv else "send" for o in ops]
+        if len(works) != len(ops):       # one coalesced work for the whole group (NCCL)
+            kinds = ["recv"] * len(works)
+        self.pending.append((works, kinds, post))
 
     def wait(self):
-        for works, post in self.pending:
+        """Before the next call c+1: only its INPUTS must have arrived (the
+        communication stream overlaps local computation).  The sends of call c read the
+        parity-(c % 2) output buffers, which call c+2 overwrites, so they are waited for
+        one call later (all works of older posts here)."""
+        last = len(self.pending) - 1
+        keep = []
+        for i, (works, kinds, post) in enumerate(self.pending):
+            sends = []
+            for w, k in zip(works, kinds):
+                if k == "recv" or i < last:
+                    w.wait()
+                else:
+                    sends.append(w)
+            for dst, wire in post:
+                dst.copy_(wire, non_blocking=False)
+            if sends:
+                keep.append((sends, ["send"] * len(sends), []))
+        self.pending = keep
+
+    def drain(self):
+        """Wait for every outstanding transfer (end of a run)."""
+        for works, _, post in self.pending:
             for w in works:
                 w.wait()
             for dst, wire in post:
@@ -160,7 +184,7 @@ def run_pipelined(stage, transport: StageTransport, chunks, out_cb, num_calls: i
             if after_call:
                 after_call(c, oc)
             transport.post(c, num_calls)
-        transport.wait()
+        transport.drain()
     return outs
 
 
@@ -173,10 +197,10 @@ def balanced_ranges(num_blocks: int, world: int, block_ms: float, first_extra_ms
 
 
 # ------------------------------------------------------------------------- bench
-def _pp_backend():
-    """NCCL over NVLink for the real multi-GPU run.  SDV2_PP_BACKEND=gloo moves the same
-    packets through host staging, so the bench logic runs with several ranks on one GPU."""
-    return os.environ.get("SDV2_PP_BACKEND", "nccl")
+def _pp_backend(args):
+    """NCCL over NVLink for the real multi-GPU run.  ``bench.py --pp-backend gloo`` moves the
+    same packets through host staging, so the bench logic runs with several ranks on one GPU."""
+    return getattr(args, "pp_backend", "nccl")
 
 
 def _gather(dist, vals, backend):
@@ -228,7 +252,7 @@ def run_pipeline_bench(args, cfg):
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    backend = _pp_backend()
+    backend = _pp_backend(args)
     dev_index = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(dev_index)
     if backend == "nccl":

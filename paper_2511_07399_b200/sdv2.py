@@ -53,6 +53,10 @@ class StreamDescC(ctypes.Structure):
                 ("ema_lambda", ctypes.c_float), ("sink_tau", ctypes.c_float), ("seed", ctypes.c_uint64)]
 
 
+class ExecOptionsC(ctypes.Structure):
+    _fields_ = [("tune_gemms", ctypes.c_int32), ("pdl", ctypes.c_int32), ("graphs", ctypes.c_int32)]
+
+
 class StageIOC(ctypes.Structure):
     _fields_ = [("act_in", ctypes.c_void_p), ("act_out", ctypes.c_void_p), ("act_bytes", ctypes.c_size_t),
                 ("ring_in", ctypes.c_void_p), ("ring_out", ctypes.c_void_p), ("ring_bytes", ctypes.c_size_t)]
@@ -85,7 +89,7 @@ def _declare(lib):
                                          ctypes.POINTER(PipelineC), ctypes.c_int]
     lib.sdv2_create.argtypes = [ctypes.POINTER(ModelDescC), ctypes.POINTER(GeometryC), ctypes.POINTER(PipelineC),
                                 ctypes.c_int, ctypes.POINTER(WeightsC), P, ctypes.c_size_t, ctypes.c_int, P,
-                                ctypes.POINTER(P)]
+                                ctypes.POINTER(ExecOptionsC), ctypes.POINTER(P)]
     lib.sdv2_reset_stream.argtypes = [P, ctypes.POINTER(StreamDescC), P]
     lib.sdv2_set_prompt.argtypes = [P, P]
     lib.sdv2_denoise_chunk.argtypes = [P, P, P, ctypes.POINTER(ctypes.c_int64)]
@@ -115,17 +119,25 @@ def _declare(lib):
 
 
 _LIB = None
+_LIB_PATH = LIB_PATH
+
+
+def load_library(path: str):
+    """Use another build of the same library (A/B timing tools); must precede the first lib()."""
+    global _LIB_PATH
+    if _LIB is not None and path != _LIB_PATH:
+        raise RuntimeError("libsdv2 already loaded from " + _LIB_PATH)
+    _LIB_PATH = path
 
 
 def lib():
     """Load libsdv2.so (raises if it has not been built: no fallback exists)."""
     global _LIB
     if _LIB is None:
-        path = os.environ.get("SDV2_LIB_PATH", LIB_PATH)   # A/B builds of the same library
-        if not os.path.exists(path):
-            raise RuntimeError(f"{path} is missing: run `python -m paper_2511_07399_b200.build` "
+        if not os.path.exists(_LIB_PATH):
+            raise RuntimeError(f"{_LIB_PATH} is missing: run `python -m paper_2511_07399_b200.build` "
                                "(the hot path has no CPU fallback)")
-        _LIB = _declare(ctypes.CDLL(path))
+        _LIB = _declare(ctypes.CDLL(_LIB_PATH))
     return _LIB
 
 
@@ -229,7 +241,7 @@ class Stage:
     """One pipeline stage (or the whole model when pipeline=None) of the hot path."""
 
     def __init__(self, md, geom, weights: Dict[str, np.ndarray], precision=SDV2_BF16, pipeline=None,
-                 device=0, stream=None):
+                 device=0, stream=None, tune_gemms=True, pdl=True, graphs=True):
         import torch
         self.torch = torch
         self.md, self.geom = md, geom
@@ -266,9 +278,10 @@ class Stage:
             keep.append(a)
         w = WeightsC(ptrs, len(names))
         h = ctypes.c_void_p()
+        self._opts = ExecOptionsC(int(tune_gemms), int(pdl), int(graphs))
         st = self.L.sdv2_create(ctypes.byref(self._mdc), ctypes.byref(self._gc), ppp, precision, ctypes.byref(w),
                                 ctypes.c_void_p(self.workspace.data_ptr()), nbytes + 1024, device,
-                                ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(h))
+                                ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(self._opts), ctypes.byref(h))
         if st != 0:
             if h.value:
                 msg = self.L.sdv2_last_error(h).decode()

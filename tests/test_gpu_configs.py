@@ -1,0 +1,217 @@
+"""GPU parity at the configurations and cache states the base parity tests do not reach
+(VERDICT r1 "untested configs"): configs[3] at its own shape (14B, n = 4), the fp32 path
+on a 1.3B-shaped block, the device K/V slot contents after eviction / re-base / sink
+refresh ("sink tokens are retained"), m = 0, T' = 2, the prompt-switch guard, and
+tuned handles being bitwise reproducible.  Tolerances are the north star's: fp32 path
+rel-L2 <= 1e-4, bf16 path rel-L2 <= 2e-2 per block, metadata bit-exact."""
+import dataclasses
+
+import numpy as np
+import pytest
+
+import synthgen as sg
+from oracle import model as M
+from oracle.stream import StreamOracle, run_stream
+from paper_2511_07399_b200.sdv2 import SDV2_BF16, SDV2_FP32, SDV2Error, Stage
+
+from gpu_harness import rel_l2, run_gpu, tiny_inputs
+
+TOL = {SDV2_FP32: 1e-4, SDV2_BF16: 2e-2}
+
+
+def _cfg(name, nblocks=None, num_chunks=None, steps=None, **geom):
+    cfg = sg.CONFIGS[name]
+    md = cfg.model if nblocks is None else dataclasses.replace(cfg.model, num_blocks=nblocks)
+    g = dataclasses.replace(cfg.geom, **geom) if geom else cfg.geom
+    st = cfg.stream
+    if steps is not None:
+        g = dataclasses.replace(g, steps=steps)
+        st = dataclasses.replace(st, timesteps=sg.SCHEDULES[steps])
+    return dataclasses.replace(cfg, model=md, geom=g, stream=st,
+                               num_chunks=cfg.num_chunks if num_chunks is None else num_chunks)
+
+
+def _check_stream(cfg, prec, dtype=np.float64, reset=None, oracle_chunks=None):
+    if reset is not None:
+        cfg = dataclasses.replace(cfg, stream=dataclasses.replace(cfg.stream, rope_reset_frames=reset))
+    W, ch, prompts = tiny_inputs(cfg, extra=cfg.geom.steps - 1, segment=2)
+    recs = run_stream(cfg, W, ch[:oracle_chunks or len(ch)], prompts, dtype=dtype, tap=True)
+    outs, taps, meta = run_gpu(cfg, W, ch, prompts, prec)
+    worst = 0.0
+    for (X, j), tl in taps.items():
+        if X >= len(recs):
+            continue
+        for b in range(cfg.model.num_blocks):
+            err = rel_l2(tl[b], recs[X]["entries"][j]["taps"][b])
+            worst = max(worst, err)
+            assert err <= TOL[prec], (X, j, b, err)
+    for X in range(min(cfg.num_chunks, len(recs))):
+        assert rel_l2(outs[X], recs[X]["out"]) <= TOL[prec], X
+    for (X, j), (slots, _, _) in meta.items():
+        if X < len(recs):
+            assert slots == {s: (t, p[0]) for s, (t, p) in recs[X]["lane_state"][(0, j)].items()}, (X, j)
+    return worst
+
+
+@pytest.mark.gpu
+def test_configs3_own_shape_bf16():
+    """configs[3] at its own shape: 14B block (d 5120, 40 heads, F 13824), 480p, n = 4
+    stream batch (M = 6240 rows per tick once full), 1 block, 3 chunks (6 ticks)."""
+    cfg = _cfg("wan14_480p_4step", nblocks=1, num_chunks=3)
+    worst = _check_stream(cfg, SDV2_BF16, dtype=np.float32, reset=4, oracle_chunks=3)
+    print(f"14B n=4: worst block rel-L2 {worst:.3e}")
+
+
+@pytest.mark.gpu
+def test_fp32_path_13b_block():
+    """The fp32 path on one 1.3B-shaped block at 480p (L = 1560) vs the fp64 oracle."""
+    cfg = _cfg("wan13_480p_1step", nblocks=1, num_chunks=3)
+    worst = _check_stream(cfg, SDV2_FP32, reset=4)
+    print(f"fp32 1.3B block: worst rel-L2 {worst:.3e}")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("prec", [SDV2_FP32, SDV2_BF16])
+def test_no_sinks_m0(prec):
+    """m = 0: the window alone, with re-bases (T_reset = 4)."""
+    cfg = _cfg("tiny", sink_chunks=0, window_chunks=2, num_chunks=10)
+    _check_stream(cfg, prec)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("prec", [SDV2_FP32, SDV2_BF16])
+def test_multi_frame_chunks(prec):
+    """T' = 2 latent frames per chunk (P:42 B x T' x H x W): L = 2 (h/2)(w/2) tokens, two
+    temporal RoPE positions per chunk, re-base every 2 chunks (T_reset = 4 frames)."""
+    cfg = _cfg("tiny", chunk_frames=2, num_chunks=8)
+    _check_stream(cfg, prec)
+
+
+@pytest.mark.gpu
+def test_multi_frame_chunks_13b_bf16():
+    cfg = _cfg("wan13_512_4step", nblocks=1, num_chunks=3, steps=2, chunk_frames=2)
+    _check_stream(cfg, SDV2_BF16, dtype=np.float32, reset=8, oracle_chunks=3)
+
+
+# ------------------------------------------------------ device K/V slot contents
+def _expected_slots(o: StreamOracle, md, geom, b, j):
+    """Oracle lane (block b, lane j) as the device stores it: slot -> (K rotated by RoPE at
+    the entry's current positions, V)."""
+    hd = md.head_dim
+    out = {}
+    for e in o.lanes[(b, j)].attended():
+        pt, ph, pw = M.token_positions(md, geom, e.pos)
+        phi = M.rope_angles(hd, pt, ph, pw)
+        k = np.concatenate([M.rope_apply(e.k[:, h * hd:(h + 1) * hd], phi) for h in range(md.num_heads)], axis=1)
+        out[e.slot] = (k.copy(), e.v.copy(), e.tag)
+    return out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("prec", [SDV2_FP32, SDV2_BF16])
+def test_device_kv_slots(prec):
+    """After every call, each valid slot of every (block, lane) on the device holds exactly
+    the oracle's cache entry: sink keys keep their anchors across evictions,
+    ring keys re-based by R(-T_reset) on a reset, refreshed sinks hold the
+    refreshing chunk at the sink anchor.  K/V compared after RoPE, per slot."""
+    import torch
+    cfg = _cfg("tiny", num_chunks=12)
+    md, g = cfg.model, cfg.geom
+    n, L, d = g.steps, g.tokens_per_chunk(md), md.dim
+    W, chunks, prompts = tiny_inputs(cfg, extra=n - 1)
+    o = StreamOracle(md, g, cfg.stream, W, dtype=np.float64)
+    starts = [0, *cfg.prompt_switch]
+    snaps = {}
+    for X, v in enumerate(chunks):
+        P = prompts[starts.index(X)] if X in starts else None
+        o.step_chunk(X, v, P)
+        snaps[X] = {(b, j): _expected_slots(o, md, g, b, j) for b in range(md.num_blocks) for j in range(n)}
+    stage = Stage(md, g, W, precision=prec)
+    stage.reset_stream(cfg.stream, prompts[0])
+    out = torch.zeros(chunks[0].shape, dtype=torch.float32, device="cuda")
+    dt = torch.float32 if prec == SDV2_FP32 else torch.bfloat16
+    seen_refresh = seen_rebase = seen_evict = False
+    for c, v in enumerate(chunks):
+        if c in starts and c > 0:
+            stage.set_prompt(prompts[starts.index(c)])
+        stage.denoise_chunk(torch.from_numpy(v).cuda().data_ptr(), out.data_ptr())
+        torch.cuda.synchronize()
+        info = stage.tick_info()
+        for j in range(n):
+            X = info["chunk"][j]
+            if X < 0:
+                continue
+            for b in range(md.num_blocks):
+                st = stage.cache_state(b, j)
+                exp = snaps[X][(b, j)]
+                assert sorted(exp) == list(range(st.num_valid)), (X, j, b)
+                seen_evict |= st.evictions > 0
+                seen_rebase |= st.resets > 0
+                for which in (0, 1):
+                    ptr, elems = stage.kv_lane(b, j, which)
+                    off = ptr - stage.workspace.data_ptr()
+                    nbytes = elems * (4 if prec == SDV2_FP32 else 2)
+                    t = stage.workspace[off:off + nbytes].view(dt)
+                    dev = t.float().view(g.sink_chunks + g.window_chunks, L, d).cpu().numpy()
+                    for slot, (ek, ev, tag) in exp.items():
+                        ref = ek if which == 0 else ev
+                        err = rel_l2(dev[slot], ref)
+                        assert err <= TOL[prec], (X, j, b, slot, tag, which, err)
+                        if slot < g.sink_chunks and tag != slot:
+                            seen_refresh = True
+    stage.close()
+    assert seen_evict and seen_rebase and seen_refresh
+
+
+# ----------------------------------------------------------- prompt guard
+@pytest.mark.gpu
+def test_prompt_switch_guard():
+    """Two prompt versions are resident: a switch sooner than (n-1) K calls after the
+    previous one would overwrite K/V still read by in-flight entries -> SDV2_E_STATE, and
+    the handle keeps working with the prompt in effect."""
+    import torch
+    cfg = sg.CONFIGS["tiny"]          # n = 2, K = 1: one call between switches
+    W, chunks, prompts = tiny_inputs(cfg)
+    p2 = sg.gen_prompt(cfg.model, 7)
+    stage = Stage(cfg.model, cfg.geom, W, precision=SDV2_BF16)
+    stage.reset_stream(cfg.stream, prompts[0])
+    out = torch.zeros(chunks[0].shape, dtype=torch.float32, device="cuda")
+    stage.denoise_chunk(torch.from_numpy(chunks[0]).cuda().data_ptr(), out.data_ptr())
+    stage.set_prompt(prompts[1])                  # first switch: always allowed
+    with pytest.raises(SDV2Error, match="invalid state"):
+        stage.set_prompt(p2)                      # 0 calls later: refused
+    stage.denoise_chunk(torch.from_numpy(chunks[1]).cuda().data_ptr(), out.data_ptr())
+    stage.set_prompt(p2)                          # 1 call later: allowed
+    stage.close()
+    # the refused switch changed nothing: a stream with one switch at call 1 is reproduced
+    cfg1 = dataclasses.replace(cfg, prompt_switch=(1,))
+    ref, _, _ = run_gpu(cfg1, W, chunks, prompts, SDV2_BF16, tap=False)
+    stage = Stage(cfg.model, cfg.geom, W, precision=SDV2_BF16)
+    stage.reset_stream(cfg.stream, prompts[0])
+    got = {}
+    for c, v in enumerate(chunks):
+        if c == 1:
+            stage.set_prompt(prompts[1])
+            with pytest.raises(SDV2Error):
+                stage.set_prompt(p2)
+        oc = stage.denoise_chunk(torch.from_numpy(v).cuda().data_ptr(), out.data_ptr())
+        torch.cuda.synchronize()
+        if oc >= 0:
+            got[oc] = out.cpu().numpy().copy()
+    stage.close()
+    for X in ref:
+        assert np.array_equal(got[X], ref[X]), X
+
+
+# -------------------------------------------------- reproducible tuning
+@pytest.mark.gpu
+def test_tuned_handles_bitwise_equal_13b():
+    """Two independently tuned handles on a 1.3B-shaped 2-block 480p model give identical
+    bits (every tuner candidate reduces in the same order)."""
+    cfg = _cfg("wan13_480p_1step", nblocks=2, num_chunks=4)
+    W, ch, prompts = tiny_inputs(cfg)
+    a, _, _ = run_gpu(cfg, W, ch, prompts, SDV2_BF16, tap=False)
+    b, _, _ = run_gpu(cfg, W, ch, prompts, SDV2_BF16, tap=False)
+    assert sorted(a) == sorted(b) and a
+    for X in a:
+        assert np.array_equal(a[X], b[X]), X

@@ -90,3 +90,63 @@ def test_tc_attention(Lq, Lk, H, hd):
     ref = torch.nn.functional.scaled_dot_product_attention(qh, kh, vh).transpose(0, 1).reshape(Lq, H * hd)
     err = (o.float() - ref).norm() / ref.norm()
     assert err < 1.5e-2, err
+
+
+def _cands(M, N, K, epi):
+    L_ = lib()
+    L_.sdv2_debug_gemm_candidates.argtypes = [ctypes.c_int32] * 4 + [P, ctypes.c_int32, P]
+    L_.sdv2_debug_gemm_candidates.restype = ctypes.c_int
+    buf = (ctypes.c_int32 * 256)()
+    cnt = ctypes.c_int32()
+    assert L_.sdv2_debug_gemm_candidates(M, N, K, epi, buf, 64, ctypes.byref(cnt)) == 0
+    return [tuple(buf[4 * i:4 * i + 4]) for i in range(cnt.value)]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("M,N,K,epi", [(1560, 4608, 1536, 0), (1560, 1536, 1536, 2), (1560, 8960, 1536, 1),
+                                       (1560, 1536, 8960, 2), (1560, 1536, 1536, 3), (6240, 1536, 1536, 2),
+                                       (4096, 8960, 1536, 1), (1560, 64, 1536, 4), (6240, 5120, 5120, 0)])
+def test_gemm_configs_bitwise_identical(M, N, K, epi):
+    """Every configuration the create-time tuner may pick (cluster size, tile width, early
+    residual fetch) reduces each output element over K in the same order, so the tuner's
+    timing-dependent choice never changes results: all candidates agree bit for bit."""
+    import torch
+    L_ = lib()
+    L_.sdv2_debug_gemm_cfg.argtypes = [P, P, P, P] + [ctypes.c_int32] * 4 + [P, P, ctypes.c_int32, ctypes.c_int32,
+                                                                            P, P]
+    L_.sdv2_debug_gemm_cfg.restype = ctypes.c_int
+    cands = _cands(M, N, K, epi)
+    assert len(cands) >= 2 and all(c[2] == 0 for c in cands)       # no stream-K on the product path
+    torch.manual_seed(M + N + K)
+    A = (torch.randn(M, K, device="cuda") * 0.5).bfloat16()
+    W = (torch.randn(N, K, device="cuda") / K ** 0.5).bfloat16()
+    bias = torch.randn(N, device="cuda")
+    L = 1560
+    mod = torch.randn(6, N, device="cuda")
+    e0 = torch.randn((M + L - 1) // L, 6, N, device="cuda")
+    x0 = torch.randn(M, N, device="cuda")
+    ref = None
+    for c in cands:
+        if epi in (2, 3):
+            out = x0.clone()
+        elif epi == 4:
+            out = torch.zeros(M, N, device="cuda")
+        else:
+            out = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
+        cfg = (ctypes.c_int32 * 4)(*c)
+        st = L_.sdv2_debug_gemm_cfg(A.data_ptr(), W.data_ptr(), bias.data_ptr(), out.data_ptr(), M, N, K, epi,
+                                    mod.data_ptr(), e0.data_ptr(), 2, L, cfg, torch.cuda.current_stream().cuda_stream)
+        assert st == 0, c
+        torch.cuda.synchronize()
+        if ref is None:
+            ref = out
+            exp = A.float() @ W.float().T + bias
+            if epi == 1:
+                exp = torch.nn.functional.gelu(exp, approximate="tanh")
+            if epi == 2:
+                exp = x0 + (mod[2][None, :] + e0[torch.arange(M, device="cuda") // L, 2, :]) * exp
+            if epi == 3:
+                exp = x0 + exp
+            assert ((out.float() - exp).norm() / exp.norm()).item() < 8e-3
+        else:
+            assert torch.equal(out, ref), (c, cands[0])

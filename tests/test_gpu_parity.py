@@ -110,14 +110,14 @@ def test_graph_replay_equals_eager(tiny_ref, prec):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("prec", [SDV2_FP32, SDV2_BF16])
-def test_reset_with_new_stream_constants_drops_stale_graphs(prec, monkeypatch):
+def test_reset_with_new_stream_constants_drops_stale_graphs(prec):
     """Captured call graphs bake stream constants (timesteps, seed, T_reset) in as kernel
     arguments: re-using a handle with a different stream descriptor must give exactly
     the output of a fresh handle with that descriptor (no stale graph replay)."""
     import dataclasses
     import torch
     from paper_2511_07399_b200.sdv2 import Stage
-    monkeypatch.setenv("SDV2_TUNE", "0")   # same GEMM configuration in both handles
+    # both handles tune their GEMMs independently: every candidate gives the same bits
     cfg = sg.CONFIGS["tiny"]
     W, chunks, prompts = tiny_inputs(cfg)
     sd2 = dataclasses.replace(cfg.stream, seed=cfg.stream.seed + 17, rope_reset_frames=cfg.stream.rope_reset_frames + 2)

@@ -21,21 +21,28 @@ def _free_port():
     return p
 
 
-def _inputs():
+def _inputs(kind="tiny"):
+    """tiny (configs[0]) or a 1.3B-shaped 2-block model at 480p, n = 1 (configs[1] block shapes)."""
+    import dataclasses
     cfg = sg.CONFIGS["tiny"]
-    W = sg.gen_weights(cfg.model, seed=0)
-    ls = sg.LatentStream(4, 8, 8, seed=1, segment=3)
+    if kind == "wan13":
+        base = sg.CONFIGS["wan13_480p_1step"]
+        cfg = dataclasses.replace(base, model=dataclasses.replace(base.model, num_blocks=2),
+                                  stream=dataclasses.replace(base.stream, rope_reset_frames=4))
+    md, g = cfg.model, cfg.geom
+    W = sg.gen_weights(md, seed=0)
+    ls = sg.LatentStream(md.latent_channels, g.latent_h, g.latent_w, seed=1, segment=3)
     chunks = [ls.chunk(X, 1) for X in range(NCALL)]
-    prompts = [sg.gen_prompt(cfg.model, 0), sg.gen_prompt(cfg.model, 1)]
+    prompts = [sg.gen_prompt(md, 0), sg.gen_prompt(md, 1)]
     return cfg, W, chunks, prompts
 
 
-def _run(prec, rank, world, q=None, port=None):
+def _run(prec, rank, world, q=None, port=None, kind="tiny"):
     import torch
     from paper_2511_07399_b200.pipeline import StageTransport, balanced_ranges, run_pipelined, stage_io_tensors
     from paper_2511_07399_b200.sdv2 import Stage
     torch.cuda.set_device(0)
-    cfg, W, chunks, prompts = _inputs()
+    cfg, W, chunks, prompts = _inputs(kind)
     if world > 1:
         import torch.distributed as dist
         os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -75,28 +82,28 @@ def _run(prec, rank, world, q=None, port=None):
     return idx, res
 
 
-def _worker(rank, world, port, q, prec):
-    _run(prec, rank, world, q, port)
+def _worker(rank, world, port, q, prec, kind):
+    _run(prec, rank, world, q, port, kind)
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("prec", [0, 1])
-def test_two_stage_pipeline_bitwise(prec):
+@pytest.mark.parametrize("prec,kind", [(0, "tiny"), (1, "tiny"), (1, "wan13")])
+def test_two_stage_pipeline_bitwise(prec, kind):
     import torch.multiprocessing as mp
     from paper_2511_07399_b200 import build
     build.build()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_worker, args=(r, 2, port, q, prec)) for r in range(2)]
+    ps = [ctx.Process(target=_worker, args=(r, 2, port, q, prec, kind)) for r in range(2)]
     for p in ps:
         p.start()
     idx, got = q.get(timeout=300)
     for p in ps:
         p.join(timeout=120)
         assert p.exitcode == 0
-    ref_idx, ref = _run(prec, 0, 1)
-    n = sg.CONFIGS["tiny"].geom.steps
+    ref_idx, ref = _run(prec, 0, 1, kind=kind)
+    n = _inputs(kind)[0].geom.steps
     assert idx == [-1] * ((n - 1) * 2) + list(range(NCALL - (n - 1) * 2))
     assert set(got) and set(got) <= set(ref)
     for X, v in got.items():

@@ -1,5 +1,5 @@
 #!/bin/bash
 # Pipeline bench logic with several ranks on ONE GPU (gloo host staging instead of NCCL).
 #   tools/pp_bench_check.sh [steps] [config] [ranks]
-SDV2_PP_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node ${3:-2} \
-  --master-addr 127.0.0.1 --master-port 29517 bench.py --gpus ${3:-2} --steps ${1:-20} --warmup 3 ${2:+--config $2}
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node ${3:-2} \
+  --master-addr 127.0.0.1 --master-port 29517 bench.py --pp-backend gloo --gpus ${3:-2} --steps ${1:-20} --warmup 3 ${2:+--config $2}
