@@ -221,6 +221,11 @@ def run_ours(args, cfg):
     B.build()
     torch.cuda.set_device(local)
     md, g, sd = cfg.model, cfg.geom, cfg.stream
+    Bs = args.streams
+    if Bs > 1:     # SLO batch: Bs independent streams per call
+        import dataclasses
+        g = dataclasses.replace(g, streams=Bs)
+        cfg = dataclasses.replace(cfg, geom=g)
     t0 = time.time()
     big = md.dim >= 4096
     W = gen_weights_device(md) if big else gen_weights_parallel(md)
@@ -232,10 +237,10 @@ def run_ours(args, cfg):
         W = sg.gen_weights(md, seed=0, blocks=[0, 1])
     stream = stage.stream
     torch.cuda.set_stream(stream)      # everything below is ordered on the stage's stream
-    prompt = sg.gen_prompt(md, 0)
-    ls = sg.LatentStream(md.latent_channels, g.latent_h, g.latent_w, seed=1)
+    prompt = [sg.gen_prompt(md, b) for b in range(Bs)]
+    lss = [sg.LatentStream(md.latent_channels, g.latent_h, g.latent_w, seed=1 + b) for b in range(Bs)]
     R = 16
-    host_chunks = [ls.chunk(X, g.chunk_frames) for X in range(R)]
+    host_chunks = [np.stack([ls.chunk(X, g.chunk_frames) for ls in lss]) for X in range(R)]   # [Bs, C, T', h, w]
     dev_chunks = [torch.from_numpy(c).cuda() for c in host_chunks]
     out_dev = torch.empty(host_chunks[0].shape, dtype=torch.float32, device="cuda")
     n, K = g.steps, 1
@@ -288,7 +293,7 @@ def run_ours(args, cfg):
     step_ms = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
     total_ms = evs[0].elapsed_time(evs[-1])
     lat = [sum(step_ms[i:i + n * K]) for i in range(0, args.steps - n * K + 1)]
-    value = chunk_frames_px(cfg) * outs / (total_ms / 1e3)
+    value = chunk_frames_px(cfg) * Bs * outs / (total_ms / 1e3)
     # ---- end to end through the C-ABI with pinned host buffers
     pin_in = [torch.from_numpy(h).pin_memory() for h in host_chunks]
     pin_out = torch.empty(host_chunks[0].shape, dtype=torch.float32).pin_memory()
@@ -305,7 +310,7 @@ def run_ours(args, cfg):
     torch.cuda.synchronize()
     c += e2e_steps
     e2e_ms = t_a.elapsed_time(t_b)
-    e2e_value = chunk_frames_px(cfg) * outs_e2e / (e2e_ms / 1e3)
+    e2e_value = chunk_frames_px(cfg) * Bs * outs_e2e / (e2e_ms / 1e3)
     bytes_chunk = host_chunks[0].nbytes
     # ---- per-kernel-class device time (events around each launch), same workload
     prof_steps = min(args.steps, 50)
@@ -352,8 +357,9 @@ def run_ours(args, cfg):
                    "tokens_per_chunk": g.tokens_per_chunk(md), "steps_n": n, "sink_chunks": g.sink_chunks,
                    "window_chunks": g.window_chunks, "blocks": md.num_blocks, "dim": md.dim,
                    "parallelism": "pp1", "l2": "per-step working set >> L2 (weights 2.8GB+ streamed each step)",
-                   "px_frames_per_chunk": chunk_frames_px(cfg)},
-        "latent_chunks_per_s": outs / (total_ms / 1e3),
+                   "px_frames_per_chunk": chunk_frames_px(cfg), "streams": Bs},
+        "latent_chunks_per_s": Bs * outs / (total_ms / 1e3),
+        "per_stream_fps": chunk_frames_px(cfg) * outs / (total_ms / 1e3),
         "ttff_ms": ttff_ms,
         "ttff_with_buffering_ms": {"16fps": ttff_ms + 1e3 * chunk_frames_px(cfg) / 16.0,
                                    "30fps": ttff_ms + 1e3 * chunk_frames_px(cfg) / 30.0},
@@ -381,6 +387,8 @@ def main():
     ap.add_argument("--pp-backend", default="nccl", choices=["nccl", "gloo"],
                     help="stage transport for --gpus > 1 (gloo: host staging, several ranks on one GPU)")
     ap.add_argument("--lib", default=None, help="alternative libsdv2.so build (A/B timing)")
+    ap.add_argument("--streams", type=int, default=1,
+                    help="independent streams batched per call (SLO batch B; value = all streams' frames/s)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.lib:

@@ -61,13 +61,18 @@ typedef struct {
   int32_t norm_center;                                 /* 0 = RMSNorm, 1 = LayerNorm (affine-free) */
 } sdv2_model_desc;
 
-/* Stream geometry ("B x T' x H x W"; P:190 sink set size m; P:472 rolling window). */
+/* Stream geometry ("B x T' x H x W"; P:190 sink set size m; P:472 rolling window).
+ * `streams` independent latent streams (the SLO batch B of P:174-185; "different colors
+ * denote distinct latent streams", Fig. parallel) are batched into every call, each with
+ * its own noise controller, prompt, sink set and KV lanes.  A call holds streams x steps
+ * entries (<= 16): entry e = j * streams + b is step j of stream b and uses KV lane e. */
 typedef struct {
   int32_t latent_h, latent_w;   /* latent frame; divisible by the patch */
   int32_t chunk_frames;         /* T' latent frames per chunk (<= 16)   */
-  int32_t steps;                /* n = B denoising steps = in-flight entries = KV lanes (<= 8) */
+  int32_t steps;                /* n denoising steps in flight per stream (Stream Batch, <= 8) */
   int32_t sink_chunks;          /* m >= 0 sink chunks (first chunks, refreshed by P:190) */
   int32_t window_chunks;        /* W >= 1 rolling-window chunks, current chunk included */
+  int32_t streams;              /* B >= 1 streams per call; streams * steps <= 16 */
 } sdv2_geometry;
 
 /* Pipeline stage of this handle.  world = K stages; this rank owns DiT
@@ -93,7 +98,8 @@ typedef struct {
 /* Per-stream controls (P:190 tau; P:191 T_reset; P:210–219 k, sigma, s_min, s_max, lambda).
  * timesteps: host array of `steps` strictly decreasing values, t_0 in (0, 1000]; the
  * noise level of step j of chunk X is sigma = s_X * t_j / t_0 (reading R5).
- * seed keys the Philox4x32-10 noise (counter layout in DESIGN.md). */
+ * seed keys the Philox4x32-10 noise (counter layout in DESIGN.md); stream b uses the key
+ * (seed_lo32, seed_hi32 + b).  Every stream shares these controls. */
 typedef struct {
   const float* timesteps;
   int32_t num_timesteps;
@@ -120,9 +126,9 @@ typedef struct {
 /* Per-call schedule introspection (host-only; deterministic R2 schedule). */
 typedef struct {
   int64_t call;                  /* call index on this rank                         */
-  int32_t num_entries;           /* active entries this call (prefix j = 0..n-1)    */
+  int32_t num_entries;           /* active entries this call (prefix of e = j B + b) */
   int32_t steps;
-  int64_t chunk[8];              /* chunk X of entry j (-1 if inactive)             */
+  int64_t chunk[8];              /* chunk X of step j, every stream (-1 if inactive) */
   int64_t out_chunk;             /* chunk whose clean latent this call emits, or -1 */
   int64_t kernel_launches;       /* cumulative kernels this handle has launched      */
 } sdv2_tick_info;
@@ -184,8 +190,9 @@ sdv2_status sdv2_create(const sdv2_model_desc* md, const sdv2_geometry* g,
                         const sdv2_weights* w, void* workspace, size_t workspace_bytes,
                         int device, void* stream, const sdv2_exec_options* opts, sdv2_handle** out);
 
-/* Start a new stream: zero KV lanes, metadata and controller state; embed the prompt
- * (host [text_len, text_dim] fp32) and compute every local block's cross K/V. */
+/* Start new streams: zero KV lanes, metadata and controller states; embed the prompts
+ * (host [streams][text_len][text_dim] fp32, one per stream) and compute every local
+ * block's cross K/V. */
 sdv2_status sdv2_reset_stream(sdv2_handle* h, const sdv2_stream_desc* sd, const float* prompt_host);
 
 /* Switch prompt: takes effect from the next chunk admitted (the next
@@ -193,14 +200,16 @@ sdv2_status sdv2_reset_stream(sdv2_handle* h, const sdv2_stream_desc* sd, const 
  * are resident, so a switch must come at least (steps - 1) * world calls after the
  * previous one (the oldest chunk admitted under the version being overwritten has then
  * left the pipeline); an earlier switch returns SDV2_E_STATE and changes nothing.
- * SDV2_E_INVALID for a zero-norm prompt mean. */
-sdv2_status sdv2_set_prompt(sdv2_handle* h, const float* prompt_host);
+ * SDV2_E_INVALID for a zero-norm prompt mean or a stream index out of range.
+ * prompt_host: host [text_len, text_dim] fp32 for stream `stream`. */
+sdv2_status sdv2_set_prompt(sdv2_handle* h, int32_t stream, const float* prompt_host);
 
-/* One stage-tick.  Rank 0: chunk_latent [C, T', h, w] fp32 (host or device pointer)
- * is admitted as chunk X = call index.  Last rank: if this call emits a clean chunk,
- * its x0 is written to out_latent (host or device, [C, T', h, w] fp32) and
- * *out_chunk_index = its chunk index, else *out_chunk_index = -1 (known without a
- * device sync: the schedule is deterministic).  Other ranks pass NULL. */
+/* One stage-tick.  Rank 0: chunk_latent [streams][C, T', h, w] fp32 (host or device
+ * pointer): chunk X = call index of every stream is admitted.  Last rank: if this call
+ * emits clean chunks, their x0 are written to out_latent (host or device,
+ * [streams][C, T', h, w] fp32) and *out_chunk_index = their chunk index, else
+ * *out_chunk_index = -1 (known without a device sync: the schedule is deterministic).
+ * Other ranks pass NULL. */
 sdv2_status sdv2_denoise_chunk(sdv2_handle* h, const float* chunk_latent, float* out_latent,
                                int64_t* out_chunk_index);
 
@@ -211,7 +220,8 @@ const char* sdv2_status_string(sdv2_status s);
 const char* sdv2_last_error(const sdv2_handle* h);
 
 /* ---- test-only introspection (not on the timed path) ---- */
-/* Metadata of (local block, lane); also copies the controller state (s, d_hat). */
+/* Metadata of (local block, lane e = j * streams + b); also copies stream b's controller
+ * state (s, d_hat). */
 sdv2_status sdv2_get_cache_state(sdv2_handle* h, int32_t local_block, int32_t lane, sdv2_cache_state* out);
 /* If per_block_out != NULL (device, [local_blocks, n*L, dim] fp32) every following
  * call copies the residual stream x after each local block into it. */
@@ -259,6 +269,51 @@ sdv2_status sdv2_debug_attention(const void* q, const void* K, const void* V, vo
 sdv2_status sdv2_partition(const double* block_costs, int32_t num_blocks, int32_t stages,
                            double extra_first, double extra_last, int32_t* bounds_out,
                            double* max_stage_out);
+
+/* ---- SLO-aware batching scheduler (host only) ----
+ * A latency point is one MEASURED call latency L(T', B): chunk_frames = T' latent frames
+ * per chunk, streams = B streams batched per call (sdv2_geometry.streams).  Every stream
+ * emits one clean chunk per call in steady state, so its output rate is
+ * px_per_latent * T' / L frames/s (px_per_latent = 4: Wan VAE temporal factor, Q23). */
+typedef struct {
+  int32_t chunk_frames;
+  int32_t streams;
+  double latency_s;
+} sdv2_latency_point;
+
+typedef struct {
+  double target_fps;            /* f_SLO per stream, output frames/s                    */
+  double frame_deadline_s;      /* per-frame deadline; chunk deadline = it x px T'       */
+  int32_t px_per_latent;        /* output frames per latent frame (4)                    */
+} sdv2_slo;
+
+typedef struct {
+  int32_t chunk_frames;
+  int32_t streams;
+  double latency_s;
+  double fps;                   /* aggregate px B T' / L                                 */
+  int32_t feasible;             /* 0: no point meets the SLO (reported, never relaxed)   */
+} sdv2_batch_decision;
+
+/* Exhaustive search of the table: the (T', B) with B <= b_max and B T' <= buffered_frames
+ * ("B.T must not exceed the number of frames already collected") that keeps every
+ * stream at >= target_fps and within the chunk deadline, maximising aggregate fps; ties:
+ * smaller B, then smaller T'.  None feasible: B = 1 at the lowest latency, feasible = 0.
+ * SDV2_E_INVALID: empty table, buffered_frames < min T' (not enough input), bad args. */
+sdv2_status sdv2_slo_select(const sdv2_latency_point* table, int32_t n, const sdv2_slo* slo,
+                            int32_t buffered_frames, int32_t b_max, sdv2_batch_decision* out);
+
+/* Online adaptation ("continuously adapts B to the observed end-to-end latency"):
+ * AIMD on the caller-owned state; a violation halves streams (floor 1, infeasible = 1 if
+ * it was already 1), `streak` compliant calls add one (cap b_max). */
+typedef struct {
+  int32_t streams, chunk_frames, b_max, streak;
+  int32_t ok_run, infeasible;
+} sdv2_aimd_state;
+sdv2_status sdv2_slo_adapt(sdv2_aimd_state* st, double observed_latency_s, const sdv2_slo* slo);
+
+/* P:178-180 memory-bound latency model L = a + b (B T') fitted to the table (least squares). */
+sdv2_status sdv2_slo_fit(const sdv2_latency_point* table, int32_t n, double* a, double* b);
 
 #ifdef __cplusplus
 }

@@ -75,17 +75,17 @@ struct AttnTcArgs {
 
 // Stream-K geometry of the attention kernel.
 struct AttnGeo {
-  long long off[kMaxSteps + 1];   // tile offset of entry e's first unit
-  int J[kMaxSteps];               // key tiles per unit of entry e
+  long long off[kMaxEntries + 1];   // tile offset of entry e's first unit
+  int J[kMaxEntries];               // key tiles per unit of entry e
   long long T;                    // total tiles
   int QP;                         // query-tile groups per head (CL query tiles per group)
-  long long ubase[kMaxSteps + 1]; // first unit of entry e
+  long long ubase[kMaxEntries + 1]; // first unit of entry e
   long long Tr = 0;               // first tile of the stream-K split (after R whole rounds)
   int R = 0;                      // whole-unit rounds dealt round-robin
   __device__ void init(const AttnTcArgs& a, const TickDesc* td, int CL) {
     QP = (a.QT + CL - 1) / CL;
     off[0] = 0;
-    for (int e = 0; e < kMaxSteps; ++e) {
+    for (int e = 0; e < kMaxEntries; ++e) {
       int j = 0;
       if (e < a.n_entries && td->e[e].active) {
         const int Lk = a.cross ? a.Lk_cross : td->e[e].nvalid * a.L;
@@ -94,9 +94,9 @@ struct AttnGeo {
       J[e] = j;
       off[e + 1] = off[e] + (long long)a.H * QP * j;
     }
-    T = off[kMaxSteps];
+    T = off[kMaxEntries];
     ubase[0] = 0;
-    for (int e = 0; e < kMaxSteps; ++e) ubase[e + 1] = ubase[e] + (J[e] > 0 ? (long long)a.H * QP : 0);
+    for (int e = 0; e < kMaxEntries; ++e) ubase[e + 1] = ubase[e] + (J[e] > 0 ? (long long)a.H * QP : 0);
   }
   // Hybrid schedule over G CTAs: R = units / G rounds of whole units (unit c + k G for CTA
   // c: the G concurrently running units are consecutive, so they share a few heads' K/V in
@@ -105,19 +105,19 @@ struct AttnGeo {
   // a non-empty range (the merge waits on every CTA between a unit's first and last
   // owner) and a unit is cut into at most two pieces (cheap merges).
   __device__ void plan(bool rr, int G) {
-    R = rr ? int(ubase[kMaxSteps] / G) - 1 : 0;
+    R = rr ? int(ubase[kMaxEntries] / G) - 1 : 0;
     if (R < 0) R = 0;
     Tr = R > 0 ? unit_lo((long long)R * G) : 0;
   }
   __device__ long long unit_lo(long long u) const {   // first tile of unit u (u <= units)
     int e = 0;
-    while (e < kMaxSteps - 1 && u >= ubase[e + 1]) ++e;
-    return u >= ubase[kMaxSteps] ? T : off[e] + (u - ubase[e]) * J[e];
+    while (e < kMaxEntries - 1 && u >= ubase[e + 1]) ++e;
+    return u >= ubase[kMaxEntries] ? T : off[e] + (u - ubase[e]) * J[e];
   }
   // unit containing global tile g -> (e, unit-in-entry w, tile j)
   __device__ void locate(long long g, int& e, int& w, int& j) const {
     e = 0;
-    while (e < kMaxSteps - 1 && g >= off[e + 1]) ++e;
+    while (e < kMaxEntries - 1 && g >= off[e + 1]) ++e;
     const long long r = g - off[e];
     w = int(r / J[e]);
     j = int(r % J[e]);
@@ -271,7 +271,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
   long long t0, t1;
   if (a.per_unit) {
     const int e = c / (a.H * geo.QP), w = c % (a.H * geo.QP);
-    if (e >= kMaxSteps || geo.J[e] == 0) return;
+    if (e >= kMaxEntries || geo.J[e] == 0) return;
     t0 = geo.off[e] + (long long)w * geo.J[e];
     t1 = t0 + geo.J[e];
   } else {
@@ -370,7 +370,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
         while (g > t0) {
           const Seg s = seg_before(g);
           const int col = s.h * HD;
-          const int kv_row = a.kv_row0 + (a.cross ? (td->e[s.e].pver & 1) : s.e) * a.kv_lane_rows;
+          const int kv_row = a.kv_row0 + (a.cross ? td->e[s.e].xslot : s.e) * a.kv_lane_rows;
           if (sg > 0) tc::mbar_wait(q_empty, (sg - 1) & 1);
           if (tc::elect_one()) {
             if (CL > 1) {   // both CTAs' Q land on the even CTA's barrier
@@ -423,7 +423,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
         while (g > t0) {
           const Seg s = seg_before(g);
           const int col = s.h * HD;
-          const int kv_row = a.kv_row0 + (a.cross ? (td->e[s.e].pver & 1) : s.e) * a.kv_lane_rows;
+          const int kv_row = a.kv_row0 + (a.cross ? td->e[s.e].xslot : s.e) * a.kv_lane_rows;
           for (int j = s.jb; j < s.je; ++j, ++gi) {
             const int st = gi % VS;
             tc::mbar_wait(v_empty + st, ((gi / VS) & 1) ^ 1);

@@ -12,20 +12,21 @@ void Control::reset(const CtlParams& p) {
   p_ = p;
   r_ = 0;
   calls_ = 0;
-  pver_ = 0;
-  sink_emb_.assign(p.m, {});
-  sink_set_.assign(p.m, false);
-  recs_.assign(kRecRing, ChunkRecord{});
-  lanes_.assign(p.n, LaneMeta{});
+  st_.assign(p.B, StreamState{});
+  for (auto& S : st_) {
+    S.sink_emb.assign(p.m, {});
+    S.recs.assign(kRecRing, ChunkRecord{});
+  }
+  lanes_.assign(size_t(p.n) * p.B, LaneMeta{});
   for (auto& L : lanes_) {
     for (int s = 0; s < kMaxSlots; ++s) L.tag[s] = -1;
     std::memset(L.pos, 0, sizeof(L.pos));
   }
 }
 
-void Control::set_prompt_mean(const std::vector<double>& h, int32_t pver) {
-  h_ = h;
-  pver_ = pver;
+void Control::set_prompt_mean(int b, const std::vector<double>& h, int32_t pver) {
+  st_[b].h = h;
+  st_[b].pver = pver;
 }
 
 static double cosine(const std::vector<double>& a, const std::vector<double>& b) {
@@ -38,30 +39,27 @@ static double cosine(const std::vector<double>& a, const std::vector<double>& b)
   return ab / (std::sqrt(aa) * std::sqrt(bb));
 }
 
-// Chunk admission:
-//   reset: while X T' - r T_reset > T_reset: r += 1 (repeated wrap of P:191)
+// Chunk admission of stream b; r / rebase are the call's (every
+// stream admits chunk X = call, so the RoPE reset count is common):
 //   positions p_f = X T' + f - r T_reset
 //   X < m: sink slot X (anchor X T' + f), s_X <- h_X
 //   X >= m: refresh every sink with cos(h_X, s_i) < tau (ties keep), ring slot (X-m) mod W
-ChunkRecord Control::admit(int64_t X) {
+ChunkRecord Control::admit(int b, int64_t X, int32_t r, bool rebase) {
+  StreamState& S = st_[b];
   ChunkRecord rec;
   rec.X = X;
-  while (X * p_.T - int64_t(r_) * p_.T_reset > p_.T_reset) {
-    ++r_;
-    rec.rebase = true;
-  }
-  rec.r = r_;
-  for (int f = 0; f < p_.T; ++f) rec.pos[f] = int32_t(X * p_.T + f - int64_t(r_) * p_.T_reset);
-  rec.pver = pver_;
+  rec.rebase = rebase;
+  rec.r = r;
+  for (int f = 0; f < p_.T; ++f) rec.pos[f] = int32_t(X * p_.T + f - int64_t(r) * p_.T_reset);
+  rec.pver = S.pver;
   if (X < p_.m) {
     rec.sink_fill = int32_t(X);
-    sink_emb_[X] = h_;
-    sink_set_[X] = true;
+    S.sink_emb[X] = S.h;
   } else {
     for (int i = 0; i < p_.m; ++i) {
-      if (cosine(h_, sink_emb_[i]) < p_.tau) {
+      if (cosine(S.h, S.sink_emb[i]) < p_.tau) {
         rec.refresh_mask |= (1u << i);
-        sink_emb_[i] = h_;
+        S.sink_emb[i] = S.h;
       }
     }
     rec.ring_slot = int32_t((X - p_.m) % p_.W);
@@ -99,37 +97,48 @@ void Control::apply(LaneMeta& L, const ChunkRecord& rec) {
 }
 
 // Call c on this rank (reading R2): micro-batch mu = c holds entries (c - jK, j) for
-// j = 0..n-1 with c - jK >= 0; the active entries are always the prefix j < n_active.
+// j = 0..n-1 with c - jK >= 0, for each of the B streams (entry e = j B + b); the active
+// entries are always the prefix e < B n_active_steps.
 void Control::plan_call(TickDesc* td) {
   const int64_t c = calls_;
-  ChunkRecord rec0 = admit(c);
-  recs_[c % kRecRing] = rec0;
+  // reset: while X T' - r T_reset > T_reset: r += 1 (repeated wrap of P:191), X = c
+  bool rebase = false;
+  while (c * p_.T - int64_t(r_) * p_.T_reset > p_.T_reset) {
+    ++r_;
+    rebase = true;
+  }
+  for (int b = 0; b < p_.B; ++b) st_[b].recs[c % kRecRing] = admit(b, c, r_, rebase);
   std::memset(td, 0, sizeof(*td));
   td->call_lo = int32_t(c);
   td->out_entry = -1;
   int na = 0;
   for (int j = 0; j < p_.n; ++j) {
     const int64_t X = entry_chunk(c, j);
-    EntryDesc& e = td->e[j];
-    e.j = j;
-    if (X < 0) {
-      e.active = 0;
-      e.X = -1;
-      continue;
+    for (int b = 0; b < p_.B; ++b) {
+      const int ei = j * p_.B + b;
+      EntryDesc& e = td->e[ei];
+      e.j = j;
+      e.stream = b;
+      if (X < 0) {
+        e.active = 0;
+        e.X = -1;
+        continue;
+      }
+      const ChunkRecord& rec = st_[b].recs[X % kRecRing];
+      LaneMeta& L = lanes_[ei];
+      apply(L, rec);
+      e.X = int32_t(X);
+      e.active = 1;
+      e.write_slot = rec.sink_fill >= 0 ? rec.sink_fill : p_.m + rec.ring_slot;
+      e.nvalid = L.nvalid;
+      e.refresh_mask = int32_t(rec.refresh_mask);
+      e.rebase = rec.rebase ? 1 : 0;
+      e.pver = rec.pver;
+      e.xslot = 2 * b + (rec.pver & 1);
+      for (int f = 0; f < p_.T; ++f) e.pos[f] = rec.pos[f];
+      ++na;
     }
-    const ChunkRecord& rec = recs_[X % kRecRing];
-    LaneMeta& L = lanes_[j];
-    apply(L, rec);
-    e.X = int32_t(X);
-    e.active = 1;
-    e.write_slot = rec.sink_fill >= 0 ? rec.sink_fill : p_.m + rec.ring_slot;
-    e.nvalid = L.nvalid;
-    e.refresh_mask = int32_t(rec.refresh_mask);
-    e.rebase = rec.rebase ? 1 : 0;
-    e.pver = rec.pver;
-    for (int f = 0; f < p_.T; ++f) e.pos[f] = rec.pos[f];
-    ++na;
-    if (j == p_.n - 1) td->out_entry = j;
+    if (X >= 0 && j == p_.n - 1) td->out_entry = j * p_.B;
   }
   td->n_active = na;
   ++calls_;

@@ -18,14 +18,19 @@
 namespace sdv2 {
 
 constexpr int kMaxSteps = 8;      // n
+constexpr int kMaxEntries = 16;   // entries per call = streams B x steps n (Stream Batch x SLO batch)
 constexpr int kMaxFrames = 16;    // T'
 constexpr int kMaxSlots = 64;     // m + W
 constexpr int kRecRing = 128;     // chunk records kept (>= (n-1)K + 1)
 
 // Per-entry device descriptor (uploaded every call; POD, identical on host/device).
+// Entry e = j * B + b is step j of stream b (step-major, so the active entries of a
+// call are always a prefix); its KV lane is e.
 struct EntryDesc {
   int32_t X;            // chunk index (Philox counter word 0, s-table index)
-  int32_t j;            // step = lane
+  int32_t j;            // step
+  int32_t stream;       // b: the latent stream (controller, prompt, noise key of its own)
+  int32_t xslot;        // prompt K/V slot of the cross-attention: 2 b + (pver & 1)
   int32_t active;
   int32_t write_slot;   // physical slot the chunk's K/V go to (sink slot or m + ring slot)
   int32_t nvalid;       // valid slots of the lane after the write (a prefix)
@@ -36,11 +41,11 @@ struct EntryDesc {
 };
 
 struct TickDesc {
-  int32_t n_active;
+  int32_t n_active;     // active entries (a prefix; a multiple of B)
   int32_t call_lo;
-  int32_t out_entry;    // entry index that emits a clean chunk this call (-1 none)
+  int32_t out_entry;    // first of the B entries that emit a clean chunk this call (-1 none)
   int32_t pad;
-  EntryDesc e[kMaxSteps];
+  EntryDesc e[kMaxEntries];
 };
 
 struct ChunkRecord {
@@ -66,19 +71,22 @@ struct LaneMeta {
 struct CtlParams {
   int T = 1, m = 1, W = 1, n = 1, K = 1, rank = 0, T_reset = 1;
   double tau = 0.95;
+  int B = 1;            // streams batched per call (all admitted in lockstep: chunk X = call)
 };
 
 class Control {
  public:
   void reset(const CtlParams& p);
-  // Prompt in effect from the next admitted chunk: h = mean-pooled prompt (fp64, reading Q8).
-  void set_prompt_mean(const std::vector<double>& h, int32_t pver);
-  // One call (stage-tick) on this rank: admits chunk X = call index (R2), applies the
-  // chunk records of every active entry to its lane and fills the device descriptor.
+  // Prompt of stream b in effect from its next admitted chunk: h = mean-pooled prompt
+  // (fp64, reading Q8).
+  void set_prompt_mean(int b, const std::vector<double>& h, int32_t pver);
+  // One call (stage-tick) on this rank: admits chunk X = call index of every stream (R2),
+  // applies the chunk records of every active entry to its lane and fills the device
+  // descriptor.
   void plan_call(TickDesc* td);
   int64_t calls() const { return calls_; }
-  const LaneMeta& lane(int j) const { return lanes_[j]; }
-  const ChunkRecord& record(int64_t X) const { return recs_[X % kRecRing]; }
+  const LaneMeta& lane(int e) const { return lanes_[e]; }
+  const ChunkRecord& record(int b, int64_t X) const { return st_[b].recs[X % kRecRing]; }
   int32_t resets() const { return r_; }
   const CtlParams& params() const { return p_; }
   // Entry chunk of step j at call c under R2: X = c - j K (valid if >= 0).
@@ -87,18 +95,21 @@ class Control {
   int64_t out_chunk(int64_t c) const { return c - int64_t(p_.n - 1) * p_.K; }
 
  private:
-  ChunkRecord admit(int64_t X);
+  ChunkRecord admit(int b, int64_t X, int32_t r, bool rebase);
   void apply(LaneMeta& L, const ChunkRecord& rec);
 
+  // per-stream admission state
+  struct StreamState {
+    std::vector<std::vector<double>> sink_emb;
+    std::vector<double> h;
+    int32_t pver = 0;
+    std::vector<ChunkRecord> recs;
+  };
   CtlParams p_;
   int32_t r_ = 0;
   int64_t calls_ = 0;
-  std::vector<std::vector<double>> sink_emb_;
-  std::vector<bool> sink_set_;
-  std::vector<double> h_;
-  int32_t pver_ = 0;
-  std::vector<ChunkRecord> recs_;
-  std::vector<LaneMeta> lanes_;
+  std::vector<StreamState> st_;
+  std::vector<LaneMeta> lanes_;   // [n * B], lane e = j * B + b
 };
 
 // Exact min-max contiguous partition (DP over prefix sums), earliest-heavy tie-break.

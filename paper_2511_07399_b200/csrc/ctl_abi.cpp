@@ -22,38 +22,41 @@ sdv2_status sdv2_partition(const double* block_costs, int32_t num_blocks, int32_
 }
 
 void* sdv2ctl_new(int32_t T, int32_t m, int32_t W, int32_t n, int32_t K, int32_t rank,
-                  int32_t T_reset, double tau) {
+                  int32_t T_reset, double tau, int32_t B) {
   if (T < 1 || T > kMaxFrames || m < 0 || W < 1 || m + W > kMaxSlots || n < 1 || n > kMaxSteps ||
-      K < 1 || T_reset < 1)
+      K < 1 || T_reset < 1 || B < 1 || B * n > kMaxEntries || int64_t(n - 1) * K + 1 > kRecRing)
     return nullptr;
   auto* c = new Control();
   CtlParams p;
-  p.T = T; p.m = m; p.W = W; p.n = n; p.K = K; p.rank = rank; p.T_reset = T_reset; p.tau = tau;
+  p.T = T; p.m = m; p.W = W; p.n = n; p.K = K; p.rank = rank; p.T_reset = T_reset; p.tau = tau; p.B = B;
   c->reset(p);
   return c;
 }
 
 void sdv2ctl_free(void* c) { delete static_cast<Control*>(c); }
 
-int32_t sdv2ctl_set_prompt_mean(void* c, const double* h, int32_t dim, int32_t pver) {
-  static_cast<Control*>(c)->set_prompt_mean(std::vector<double>(h, h + dim), pver);
+int32_t sdv2ctl_set_prompt_mean(void* c, int32_t stream, const double* h, int32_t dim, int32_t pver) {
+  auto* ctl = static_cast<Control*>(c);
+  if (stream < 0 || stream >= ctl->params().B) return -1;
+  ctl->set_prompt_mean(stream, std::vector<double>(h, h + dim), pver);
   return 0;
 }
 
-// One call; writes the device descriptor fields of every entry into out[n][8 + kMaxFrames]:
-// X, j, active, write_slot, nvalid, refresh_mask, rebase, pver, pos[0..kMaxFrames).
+// One call; writes the device descriptor fields of every entry e = j B + b into
+// out[B n][10 + kMaxFrames]: X, j, active, write_slot, nvalid, refresh_mask, rebase, pver,
+// stream, xslot, pos[0..kMaxFrames).
 int32_t sdv2ctl_call(void* c, int32_t* out, int64_t* out_chunk) {
   auto* ctl = static_cast<Control*>(c);
   TickDesc td;
   const int64_t call = ctl->calls();
   ctl->plan_call(&td);
-  const int n = ctl->params().n;
-  for (int j = 0; j < n; ++j) {
-    const EntryDesc& e = td.e[j];
-    int32_t* o = out + j * (8 + kMaxFrames);
+  const int ne = ctl->params().n * ctl->params().B;
+  for (int i = 0; i < ne; ++i) {
+    const EntryDesc& e = td.e[i];
+    int32_t* o = out + i * (10 + kMaxFrames);
     o[0] = e.X; o[1] = e.j; o[2] = e.active; o[3] = e.write_slot; o[4] = e.nvalid;
-    o[5] = e.refresh_mask; o[6] = e.rebase; o[7] = e.pver;
-    for (int f = 0; f < kMaxFrames; ++f) o[8 + f] = e.pos[f];
+    o[5] = e.refresh_mask; o[6] = e.rebase; o[7] = e.pver; o[8] = e.stream; o[9] = e.xslot;
+    for (int f = 0; f < kMaxFrames; ++f) o[10 + f] = e.pos[f];
   }
   if (out_chunk) *out_chunk = td.out_entry >= 0 ? ctl->out_chunk(call) : -1;
   return td.n_active;

@@ -336,18 +336,23 @@ __global__ void __launch_bounds__(256) rms_rows2_kernel(TA* __restrict__ y, cons
 }
 
 // ----------------------------------------------------------------------------
-// Motion-aware noise controller, 1 CTA: per-frame d (fp64 accumulation),
-// window max over the last k+1 values, clip, EMA s_X, sigma of every entry (R5).
+// Motion-aware noise controller, 1 CTA per stream b: per-frame d (fp64
+// accumulation), window max over the last k+1 values, clip, EMA s_X, sigma of every
+// entry of the stream (R5).  chunk / prev / st point at stream 0's; CTHW = chunk stride.
 // ----------------------------------------------------------------------------
-__global__ void __launch_bounds__(1024) motion_kernel(const float* __restrict__ chunk, float* prev, CtrlState* st,
-                                                      float* sig, float* sign, const TickDesc* td, StreamCfg cfg,
-                                                      int CHW, int HW, int T) {
+__global__ void __launch_bounds__(1024) motion_kernel(const float* __restrict__ chunk_all, float* prev_all,
+                                                      CtrlState* st_all, float* sig, float* sign, const TickDesc* td,
+                                                      StreamCfg cfg, int CHW, int HW, int T, int n_entries) {
   pdl_wait();
   pdl_trigger();
   __shared__ double red[32];
   const int tid = threadIdx.x, nt = blockDim.x;
+  const int b = blockIdx.x;
+  const float* chunk = chunk_all + size_t(b) * CHW;
   const int C = CHW / (HW * T);
-  const int X = td->e[0].X;
+  float* prev = prev_all + size_t(b) * C * HW;
+  CtrlState* st = st_all + b;
+  const int X = td->e[b].X;
   for (int f = 0; f < T; ++f) {
     double acc = 0.0;
     for (int i = tid * 4; i < C * HW; i += nt * 4) {
@@ -390,26 +395,34 @@ __global__ void __launch_bounds__(1024) motion_kernel(const float* __restrict__ 
     st->s = s;
     st->d_hat = dh;
     st->s_table[X & 63] = s;
-    for (int e = 0; e < cfg.n; ++e) {
+    for (int e = 0; e < n_entries; ++e) {
       const EntryDesc& E = td->e[e];
-      if (!E.active) continue;
+      if (!E.active || E.stream != b) continue;
       sig[e] = sigma_of(st, cfg, E.X, E.j);
       sign[e] = (E.j + 1 < cfg.n) ? sigma_of(st, cfg, E.X, E.j + 1) : 0.f;
     }
   }
 }
 
-// x_{X,0} = (1 - sigma_{X,0}) v_X + sigma_{X,0} eps_{X,0}  (O4), all SMs.
+// Philox key of stream b: (seed_lo, seed_hi + b) (noise source Q21).
+__device__ __forceinline__ unsigned long long stream_key(unsigned long long seed, int b) {
+  return seed + (static_cast<unsigned long long>(b) << 32);
+}
+
+// x_{X,0} = (1 - sigma_{X,0}) v_X + sigma_{X,0} eps_{X,0}  (O4), all SMs; grid.y = stream
+// b, whose step-0 entry is e = b.
 __global__ void __launch_bounds__(256) blend_kernel(const float* __restrict__ chunk, float* __restrict__ lat0,
                                                     const float* __restrict__ sig, const TickDesc* __restrict__ td,
                                                     unsigned long long seed, int CTHW) {
   pdl_wait();
   pdl_trigger();
-  const int X = td->e[0].X;
-  const float s0 = sig[0];
+  const int b = blockIdx.y;
+  const int X = td->e[b].X;
+  const float s0 = sig[b];
+  const unsigned long long key = stream_key(seed, b);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < CTHW; i += gridDim.x * blockDim.x) {
-    const float eps = float(gauss_noise(seed, uint32_t(X), 0u, uint32_t(i)));
-    lat0[i] = (1.f - s0) * chunk[i] + s0 * eps;
+    const float eps = float(gauss_noise(key, uint32_t(X), 0u, uint32_t(i)));
+    lat0[size_t(b) * CTHW + i] = (1.f - s0) * chunk[size_t(b) * CTHW + i] + s0 * eps;
   }
 }
 
@@ -430,8 +443,9 @@ __global__ void patchify_kernel(const float* __restrict__ lat, float* __restrict
 }
 
 // Head tail (C.7, C.8, O5): v_hat[c, f, 2i+a, 2jj+b] = y[tau][(a*2+b) C + c]; x0 = x_sigma -
-// sigma v_hat; the last step writes the clean output, the others (1 - s') x0 + s' eps_{X,j+1}
-// into ring-closure slot j.  One thread per latent element, all SMs.
+// sigma v_hat; the last step writes the clean output of its stream b (out[b]), the
+// others (1 - s') x0 + s' eps_{X,j+1} into ring-closure slot e (= j B + b; consumed as
+// entry e + B at the next micro-step).  One thread per latent element, all SMs.
 __global__ void __launch_bounds__(256) flow_kernel(const float* __restrict__ y, const float* __restrict__ lat,
                                                    const float* __restrict__ sig, const float* __restrict__ sign,
                                                    float* __restrict__ out, float* __restrict__ ring_out,
@@ -450,18 +464,18 @@ __global__ void __launch_bounds__(256) flow_kernel(const float* __restrict__ y, 
     const int p = ((yy & 1) * 2 + (xx & 1)) * C + c;
     const float x0 = lat[size_t(e) * CTHW + idx] - sig[e] * y[size_t(e * L + tau) * P + p];
     if (E.j == n - 1) {
-      out[idx] = x0;
+      out[size_t(E.stream) * CTHW + idx] = x0;
     } else {
       const float s1 = sign[e];
-      const float eps1 = float(gauss_noise(seed, uint32_t(E.X), uint32_t(E.j + 1), uint32_t(idx)));
-      ring_out[size_t(E.j) * CTHW + idx] = (1.f - s1) * x0 + s1 * eps1;
+      const float eps1 = float(gauss_noise(stream_key(seed, E.stream), uint32_t(E.X), uint32_t(E.j + 1), uint32_t(idx)));
+      ring_out[size_t(e) * CTHW + idx] = (1.f - s1) * x0 + s1 * eps1;
     }
   }
 }
 
 // out[e][r] = W[r,:] . act(in[e,:]) + b[r], act = SiLU if pre_silu; the activated input
 // vectors are staged once per CTA in smem; 8 warps x 4 rows per CTA.
-template <typename TW>
+template <typename TW, int NMAX = kMaxEntries>
 __global__ void __launch_bounds__(256) gemv2_kernel(const TW* __restrict__ W, const float* __restrict__ b,
                                                     const float* __restrict__ in, float* __restrict__ out, int n,
                                                     int R, int Kd, int pre_silu) {
@@ -478,18 +492,18 @@ __global__ void __launch_bounds__(256) gemv2_kernel(const TW* __restrict__ W, co
   for (int rr = 0; rr < 4; ++rr) {
     const int r = (blockIdx.x * 8 + warp) * 4 + rr;
     if (r >= R) break;
-    float acc[kMaxSteps];
+    float acc[NMAX];
 #pragma unroll
-    for (int e = 0; e < kMaxSteps; ++e) acc[e] = 0.f;
+    for (int e = 0; e < NMAX; ++e) acc[e] = 0.f;
     const TW* wr = W + size_t(r) * Kd;
     for (int k = lane; k < Kd; k += 32) {
       const float wv = to_f(wr[k]);
 #pragma unroll
-      for (int e = 0; e < kMaxSteps; ++e)
+      for (int e = 0; e < NMAX; ++e)
         if (e < n) acc[e] += wv * xs[e * Kd + k];
     }
 #pragma unroll
-    for (int e = 0; e < kMaxSteps; ++e) {
+    for (int e = 0; e < NMAX; ++e) {
       if (e < n) {
         const float s = warp_sum(acc[e]);
         if (lane == 0) out[size_t(e) * R + r] = s + b[r];

@@ -37,15 +37,16 @@ __device__ __forceinline__ float sigma_of(const CtrlState* st, const StreamCfg& 
 }
 
 // Sigma of every entry on ranks that do not run the controller is carried in the
-// packet; rank 0 also needs the ring-closure latents assembled: lat[j] = ring_in[j-1].
+// packet; rank 0 also needs the ring-closure latents assembled: entry e >= B (step j >= 1
+// of stream e % B) continues ring slot e - B of the previous micro-step.
 __global__ void assemble_kernel(const float* __restrict__ ring_in, float* __restrict__ lat, const TickDesc* td,
-                                int n, int CTHW) {
+                                int n_entries, int B, int CTHW) {
   pdl_wait();
   pdl_trigger();
-  const int j = blockIdx.y + 1;
-  if (j >= n || !td->e[j].active) return;
-  const float4* src = reinterpret_cast<const float4*>(ring_in + size_t(j - 1) * CTHW);
-  float4* dst = reinterpret_cast<float4*>(lat + size_t(j) * CTHW);
+  const int e = blockIdx.y + B;
+  if (e >= n_entries || !td->e[e].active) return;
+  const float4* src = reinterpret_cast<const float4*>(ring_in + size_t(e - B) * CTHW);
+  float4* dst = reinterpret_cast<float4*>(lat + size_t(e) * CTHW);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < CTHW / 4; i += gridDim.x * blockDim.x) dst[i] = src[i];
 }
 
@@ -114,7 +115,8 @@ __device__ __forceinline__ void rope_cs(const RopeTabs& R, int pair, int pt, int
 }
 
 // RoPE phase re-base (R3): every ring slot of a re-basing lane, in every local
-// block, is rotated on its temporal pairs by R(-T_reset).  Grid: (token-rows, lane).
+// block, is rotated on its temporal pairs by R(-T_reset).  Grid: (token-rows, lane);
+// n = lanes per block (B n).
 template <typename TA>
 __global__ void __launch_bounds__(256) rebase_kernel(TA* __restrict__ K, const TickDesc* __restrict__ td, RopeTabs R,
                                                      int nblocks, int n, int S, int m, int W, int L, int d, int hd,
@@ -262,7 +264,7 @@ struct AttnArgs {
   int ldk;
   void* o; int ldo;
   int L;                             // query rows per entry
-  int cross;                         // 0: keys = lane e, nvalid*L rows; 1: keys = version pver, Lk rows
+  int cross;                         // 0: keys = lane e, nvalid*L rows; 1: keys = prompt slot xslot, Lk rows
   int Lk_cross;
   float scale;
 };
@@ -288,7 +290,7 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(AttnArgs a, const TickDe
   size_t kv_off;
   if (a.cross) {
     Lk = a.Lk_cross;
-    kv_off = size_t(E.pver & 1) * a.kv_lane_stride;
+    kv_off = size_t(E.xslot) * a.kv_lane_stride;
   } else {
     Lk = E.nvalid * a.L;
     kv_off = size_t(e) * a.kv_lane_stride;

@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <type_traits>
 #include <utility>
 #include <cstdio>
 #include <cstring>
@@ -87,6 +88,8 @@ struct sdv2_handle {
   sdv2_precision prec;
   int K = 1, rank = 0, b0 = 0, b1 = 0, nb = 0;
   int d, H, hd, F, C, T, hh, ww, L, n, m, W, S, Lt, Dt, CTHW, Mmax, P;
+  int B = 1;                  // streams batched per call (SLO batch)
+  int NE = 1;                 // entries per call = B n (entry e = j B + b = KV lane e)
   int hn, wn, ct, ch, cw;
   size_t ta;  // bytes per activation element
   cudaStream_t stream = nullptr;
@@ -99,18 +102,18 @@ struct sdv2_handle {
   char* packet_base;          // tick state (packet layout)
   Packet st;
   char* act_io[2][2];         // [in/out][parity]
-  float* ring[2][2];          // [in/out][parity] ring-closure latents [n-1, CTHW]
-  float* lat_in;              // staged caller chunk [CTHW]
-  float* prev_frame;          // [C h w]
-  float* out_stage;           // [CTHW]
-  CtrlState* ctrl;
-  float* emb;                 // [n, 256]
+  float* ring[2][2];          // [in/out][parity] ring-closure latents [B (n-1), CTHW]
+  float* lat_in;              // staged caller chunks [B, CTHW]
+  float* prev_frame;          // [B, C h w]
+  float* out_stage;           // [B, CTHW]
+  CtrlState* ctrl;            // [B]
+  float* emb;                 // [B n, 256]
   float* u;                   // patchified tokens [Mmax, 4C] fp32
   float* yh;                  // head output [Mmax, 4C] fp32
   float* attn_part;           // stream-K attention partials
   int* attn_flags;            // [kMaxSMs] split-unit hand-off flags (zero between launches)
   void* head_w_tw;            // head weight [4C, d] TW
-  float* t1;                  // [n, d]
+  float* t1;                  // [B n, d]
   void* a;                    // [Mmax, d] TA
   void* qkv;                  // [Mmax, 3d] TA
   void* q;                    // [Mmax, d] TA
@@ -118,8 +121,8 @@ struct sdv2_handle {
   void* hbuf;                 // [Mmax, F] TA
   float* staging;             // weight staging (aliases the activation scratch)
   size_t staging_elems;
-  void* Kc; void* Vc;         // KV lanes [nb][n][S][L][d] TA
-  void* Kx; void* Vx;         // prompt K/V [2][nb][Lt][d] TA
+  void* Kc; void* Vc;         // KV lanes [nb][B n][S][L][d] TA
+  void* Kx; void* Vx;         // prompt K/V [B][2 versions][nb][Lt][d] TA
   float* prompt;              // [Lt, Dt]
   float* ctx;                 // [Lt, d]
   float* ctx_tmp;             // [Lt, d]
@@ -136,7 +139,7 @@ struct sdv2_handle {
   bool stream_ready = false;
   StreamCfg scfg;
   int T_reset = 1;
-  int pver = 0;
+  int pver[kMaxEntries] = {};                 // prompt version per stream
   float* tap = nullptr;
   sdv2_tick_info info;
   std::string err;
@@ -148,9 +151,9 @@ struct sdv2_handle {
   bool graphs = true;
   bool pdl = true;        // programmatic dependent launch (sdv2_exec_options.pdl): +2 % fps measured
   bool tune = true;       // create-time GEMM tile tuning (sdv2_exec_options.tune_gemms)
-  int64_t last_switch_call = -1;   // call index of the last sdv2_set_prompt (-1: none since reset)
-  cudaGraphExec_t graph_exec[2 * (kMaxSteps + 1)] = {};
-  int64_t graph_launches[2 * (kMaxSteps + 1)] = {};
+  int64_t last_switch_call[kMaxEntries];   // call index of stream b's last sdv2_set_prompt (-1: none)
+  cudaGraphExec_t graph_exec[2 * (kMaxEntries + 1)] = {};
+  int64_t graph_launches[2 * (kMaxEntries + 1)] = {};
   // profiling (sdv2_profile_enable): event pairs around each launch, per class
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -230,7 +233,8 @@ size_t carve(sdv2_handle* h, void* base) {
   }
   // packet (tick state) — contiguous so it can be shipped as one message
   {
-    const size_t x = size_t(h->Mmax) * d, e0 = size_t(h->n) * 6 * d, e = size_t(h->n) * d, lat = size_t(h->n) * h->CTHW;
+    const size_t x = size_t(h->Mmax) * d, e0 = size_t(h->NE) * 6 * d, e = size_t(h->NE) * d,
+                 lat = size_t(h->NE) * h->CTHW;
     const size_t sz = (x + e0 + e + 2 * 64 + lat) * 4;
     h->st.bytes = sz;
     h->packet_base = cv.take<char>(sz);
@@ -244,19 +248,19 @@ size_t carve(sdv2_handle* h, void* base) {
     for (int io = 0; io < 2; ++io)
       for (int par = 0; par < 2; ++par) h->act_io[io][par] = h->K > 1 ? cv.take<char>(sz) : nullptr;
   }
-  const size_t ring_elems = size_t(h->n > 1 ? h->n - 1 : 1) * h->CTHW;
+  const size_t ring_elems = size_t(h->n > 1 ? h->n - 1 : 1) * h->B * h->CTHW;
   for (int io = 0; io < 2; ++io)
     for (int par = 0; par < 2; ++par) h->ring[io][par] = cv.take<float>(ring_elems);
-  h->lat_in = cv.take<float>(h->CTHW);
-  h->prev_frame = cv.take<float>(size_t(h->C) * h->hh * h->ww);
-  h->out_stage = cv.take<float>(h->CTHW);
-  h->ctrl = cv.take<CtrlState>(1);
-  h->emb = cv.take<float>(size_t(h->n) * h->md.freq_dim);
+  h->lat_in = cv.take<float>(size_t(h->B) * h->CTHW);
+  h->prev_frame = cv.take<float>(size_t(h->B) * h->C * h->hh * h->ww);
+  h->out_stage = cv.take<float>(size_t(h->B) * h->CTHW);
+  h->ctrl = cv.take<CtrlState>(h->B);
+  h->emb = cv.take<float>(size_t(h->NE) * h->md.freq_dim);
   h->u = cv.take<float>(size_t(h->Mmax) * h->P);
   h->yh = cv.take<float>(size_t(h->Mmax) * h->P);
   h->attn_part = cv.take<float>(attn_scratch_floats(kMaxSMs, h->hd));
   h->attn_flags = cv.take<int>(kMaxSMs);
-  h->t1 = cv.take<float>(size_t(h->n) * d);
+  h->t1 = cv.take<float>(size_t(h->NE) * d);
   // activation scratch, aliased by the weight staging buffer during create
   {
     const size_t act = (size_t(h->Mmax) * d * 3 + size_t(h->Mmax) * 3 * d + size_t(h->Mmax) * F) * h->ta + 5 * 1024;
@@ -275,10 +279,10 @@ size_t carve(sdv2_handle* h, void* base) {
     h->o = sub.take<char>(size_t(h->Mmax) * d * h->ta);
     h->hbuf = sub.take<char>(size_t(h->Mmax) * F * h->ta);
   }
-  const size_t kv = size_t(h->nb) * h->n * h->S * h->L * d;
+  const size_t kv = size_t(h->nb) * h->NE * h->S * h->L * d;
   h->Kc = cv.take<char>(kv * h->ta);
   h->Vc = cv.take<char>(kv * h->ta);
-  const size_t px = size_t(2) * h->nb * h->Lt * d;
+  const size_t px = size_t(2) * h->B * h->nb * h->Lt * d;
   h->Kx = cv.take<char>(px * h->ta);
   h->Vx = cv.take<char>(px * h->ta);
   h->prompt = cv.take<float>(size_t(h->Lt) * h->Dt);
@@ -309,6 +313,7 @@ sdv2_status fill_dims(sdv2_handle* h, const sdv2_model_desc* md, const sdv2_geom
   if (g->window_chunks < 1 || g->sink_chunks < 0) { *why = "window_chunks < 1"; return SDV2_E_SHAPE; }
   if (g->chunk_frames < 1 || g->chunk_frames > kMaxFrames) return SDV2_E_SHAPE;
   if (g->steps < 1 || g->steps > kMaxSteps) return SDV2_E_SHAPE;
+  if (g->streams < 1 || g->streams * g->steps > kMaxEntries) { *why = "streams * steps must be in [1, 16]"; return SDV2_E_SHAPE; }
   if (g->sink_chunks + g->window_chunks > kMaxSlots || g->sink_chunks > 31) return SDV2_E_SHAPE;
   h->C = md->latent_channels; h->T = g->chunk_frames; h->hh = g->latent_h; h->ww = g->latent_w;
   h->hn = h->hh / 2; h->wn = h->ww / 2;
@@ -317,7 +322,9 @@ sdv2_status fill_dims(sdv2_handle* h, const sdv2_model_desc* md, const sdv2_geom
   h->Lt = md->text_len; h->Dt = md->text_dim;
   h->CTHW = h->C * h->T * h->hh * h->ww;
   if (h->CTHW % 4 || (h->hh * h->ww) % 4) return SDV2_E_SHAPE;
-  h->Mmax = h->n * h->L;
+  h->B = g->streams;
+  h->NE = h->B * h->n;
+  h->Mmax = h->NE * h->L;
   h->P = 4 * h->C;
   const int c = h->hd / 2;
   h->ct = c - 2 * (c / 3); h->ch = c / 3; h->cw = c / 3;
@@ -447,13 +454,13 @@ sdv2_status attention(sdv2_handle* h, const AttnArgs& aa, int Mrows_entries, dou
       long long kv_rows;
       if (aa.cross) {
         Kb = h->Kx; Vb = h->Vx;
-        kv_rows = 2LL * h->nb * h->Lt;
+        kv_rows = 2LL * h->B * h->nb * h->Lt;
         ta.kv_row0 = bl * h->Lt;
         ta.kv_lane_rows = h->nb * h->Lt;
       } else {
         Kb = h->Kc; Vb = h->Vc;
-        kv_rows = (long long)h->nb * h->n * h->S * h->L;
-        ta.kv_row0 = bl * h->n * h->S * h->L;
+        kv_rows = (long long)h->nb * h->NE * h->S * h->L;
+        ta.kv_row0 = bl * h->NE * h->S * h->L;
         ta.kv_lane_rows = h->S * h->L;
       }
       return tc_attention(h->stream, h->aplan, aa.q, h->Mmax, Kb, Vb, kv_rows, h->d, h->hd, tiles, ta, h->td_dev,
@@ -535,7 +542,7 @@ sdv2_status run_block(sdv2_handle* h, int bl, int rows, int n_act) {
   ep.out = h->qkv; ep.ldo = 3 * d; ep.bias = B.bqkv;
   TRY(gemm_act(h, h->a, B.wqkv, rows, 3 * d, d, EPI_STORE, ep));
   // 3–4. q/k RMSNorm + RoPE + KV lane write
-  const size_t lane_elems = size_t(h->n) * h->S * h->L * d;
+  const size_t lane_elems = size_t(h->NE) * h->S * h->L * d;
   TA* Kb = static_cast<TA*>(h->Kc) + bl * lane_elems;
   TA* Vb = static_cast<TA*>(h->Vc) + bl * lane_elems;
   {
@@ -593,7 +600,7 @@ sdv2_status run_block(sdv2_handle* h, int bl, int rows, int n_act) {
 // Prompt conditioning (C.3): ctx = W_x2 GELU(W_x1 P + b) + b; per block K_c = RMS(ctx W_ck^T + b),
 // V_c = ctx W_cv^T + b into prompt version slot `ver & 1`.
 template <typename TA>
-sdv2_status embed_prompt(sdv2_handle* h, const float* prompt_host, int ver) {
+sdv2_status embed_prompt(sdv2_handle* h, const float* prompt_host, int b_stream, int ver) {
   const int d = h->d, Lt = h->Lt;
   CK(cudaMemcpyAsync(h->prompt, prompt_host, size_t(Lt) * h->Dt * 4, cudaMemcpyHostToDevice, h->stream));
   EpiArgs ep{};
@@ -604,8 +611,9 @@ sdv2_status embed_prompt(sdv2_handle* h, const float* prompt_host, int ver) {
   const size_t px = size_t(Lt) * d;
   for (int b = 0; b < h->nb; ++b) {
     const BlockW& B = h->bw[b];
-    TA* Kd = static_cast<TA*>(h->Kx) + (size_t(ver & 1) * h->nb + b) * px;
-    TA* Vd = static_cast<TA*>(h->Vx) + (size_t(ver & 1) * h->nb + b) * px;
+    const size_t slot = size_t(2 * b_stream + (ver & 1));   // EntryDesc::xslot
+    TA* Kd = static_cast<TA*>(h->Kx) + (slot * h->nb + b) * px;
+    TA* Vd = static_cast<TA*>(h->Vx) + (slot * h->nb + b) * px;
     ep.out = h->ctx_tmp; ep.bias = B.bck;
     TRY((gemm_simt<float, TA, float>(h, h->ctx, static_cast<const TA*>(B.wck), Lt, d, d, d, EPI_STORE, ep)));
     launch_k(h->pdl, rms_rows_kernel<float, TA>, dim3((Lt + 7) / 8), dim3(256), 0, h->stream, h->ctx_tmp, Kd, B.gck, Lt, d, d, h->md.eps);
@@ -616,7 +624,7 @@ sdv2_status embed_prompt(sdv2_handle* h, const float* prompt_host, int ver) {
   return SDV2_OK;
 }
 
-sdv2_status set_prompt_common(sdv2_handle* h, const float* prompt_host, int ver) {
+sdv2_status set_prompt_common(sdv2_handle* h, const float* prompt_host, int b_stream, int ver) {
   // h = mean-pooled prompt, fp64 (reading Q8)
   std::vector<double> mean(h->Dt, 0.0);
   for (int t = 0; t < h->Lt; ++t)
@@ -630,9 +638,9 @@ sdv2_status set_prompt_common(sdv2_handle* h, const float* prompt_host, int ver)
     h->err = "zero-norm prompt mean";
     return SDV2_E_INVALID;
   }
-  if (h->prec == SDV2_FP32) TRY(embed_prompt<float>(h, prompt_host, ver));
-  else TRY(embed_prompt<bf16>(h, prompt_host, ver));
-  h->ctl.set_prompt_mean(mean, ver);
+  if (h->prec == SDV2_FP32) TRY(embed_prompt<float>(h, prompt_host, b_stream, ver));
+  else TRY(embed_prompt<bf16>(h, prompt_host, b_stream, ver));
+  h->ctl.set_prompt_mean(b_stream, mean, ver);
   return SDV2_OK;
 }
 
@@ -645,16 +653,17 @@ sdv2_status tick_body(sdv2_handle* h, int na, int par) {
   if (first) {
     ProfScope ps(h, 5, 0.0);
     // motion-aware noise controller then the step-0 blend on all SMs
-    launch_k(h->pdl, motion_kernel, dim3(1), dim3(1024), 0, h->stream, h->lat_in, h->prev_frame, h->ctrl, h->st.sig, h->st.sign, h->td_dev,
-                                            h->scfg, h->CTHW, h->hh * h->ww, h->T);
+    launch_k(h->pdl, motion_kernel, dim3(h->B), dim3(1024), 0, h->stream, h->lat_in, h->prev_frame, h->ctrl, h->st.sig, h->st.sign, h->td_dev,
+             h->scfg, h->CTHW, h->hh * h->ww, h->T, h->NE);
     CKL();
-    launch_k(h->pdl, blend_kernel, dim3((h->CTHW + 255) / 256), dim3(256), 0, h->stream, h->lat_in, h->st.lat, h->st.sig, h->td_dev,
-                                                               h->scfg.seed, h->CTHW);
+    launch_k(h->pdl, blend_kernel, dim3((h->CTHW + 255) / 256, h->B), dim3(256), 0, h->stream, h->lat_in, h->st.lat, h->st.sig, h->td_dev,
+             h->scfg.seed, h->CTHW);
     CKL();
-    if (na > 1) {
+    if (na > h->B) {
       // K = 1: the ring packet of call c-1 was written to ring[1][(c-1)&1] == ring[1][par^1]
       const float* rin = h->K == 1 ? h->ring[1][par ^ 1] : h->ring[0][par];
-      launch_k(h->pdl, assemble_kernel, dim3(dim3(64, h->n - 1)), dim3(256), 0, h->stream, rin, h->st.lat, h->td_dev, h->n, h->CTHW);
+      launch_k(h->pdl, assemble_kernel, dim3(64, h->NE - h->B), dim3(256), 0, h->stream, rin, h->st.lat, h->td_dev, h->NE,
+               h->B, h->CTHW);
       CKL();
     }
     // patchify + patch embedding (C.1): x = u W_pe^T + b_pe, fp32 (K = 4C)
@@ -670,13 +679,20 @@ sdv2_status tick_body(sdv2_handle* h, int na, int par) {
     CKL();
     const int d = h->d;
     // time MLP (C.2): e = W_t2 SiLU(W_t1 emb + b) + b; e0 = W_tp SiLU(e) + b
-    launch_k(h->pdl, gemv2_kernel<float>, dim3((d + 31) / 32), dim3(256), size_t(na) * h->md.freq_dim * 4, h->stream, 
-        h->gw[G_T1_W], h->gw[G_T1_B], h->emb, h->t1, na, d, h->md.freq_dim, 0);
-    launch_k(h->pdl, gemv2_kernel<float>, dim3((d + 31) / 32), dim3(256), size_t(na) * d * 4, h->stream, h->gw[G_T2_W], h->gw[G_T2_B], h->t1,
-                                                                               h->st.e, na, d, d, 1);
+    // the entry count is a template bound (registers): 4 / 8 / 16
+    auto gemvs = [&](auto nmax) {
+      constexpr int NM = decltype(nmax)::value;
+      launch_k(h->pdl, gemv2_kernel<float, NM>, dim3((d + 31) / 32), dim3(256), size_t(na) * h->md.freq_dim * 4, h->stream,
+               h->gw[G_T1_W], h->gw[G_T1_B], h->emb, h->t1, na, d, h->md.freq_dim, 0);
+      launch_k(h->pdl, gemv2_kernel<float, NM>, dim3((d + 31) / 32), dim3(256), size_t(na) * d * 4, h->stream,
+               h->gw[G_T2_W], h->gw[G_T2_B], h->t1, h->st.e, na, d, d, 1);
+      launch_k(h->pdl, gemv2_kernel<TA, NM>, dim3((6 * d + 31) / 32), dim3(256), size_t(na) * d * 4, h->stream,
+               static_cast<const TA*>(h->tp_w), h->gw[G_TP_B], h->st.e, h->st.e0, na, 6 * d, d, 1);
+    };
+    if (na <= 4) gemvs(std::integral_constant<int, 4>{});
+    else if (na <= 8) gemvs(std::integral_constant<int, 8>{});
+    else gemvs(std::integral_constant<int, 16>{});
     h->launches += 2;
-    launch_k(h->pdl, gemv2_kernel<TA>, dim3((6 * d + 31) / 32), dim3(256), size_t(na) * d * 4, h->stream, 
-        static_cast<const TA*>(h->tp_w), h->gw[G_TP_B], h->st.e, h->st.e0, na, 6 * d, d, 1);
     CKL();
   } else {
     CK(cudaMemcpyAsync(h->packet_base, h->act_io[0][par], h->st.bytes, cudaMemcpyDeviceToDevice, h->stream));
@@ -733,18 +749,18 @@ sdv2_status tick(sdv2_handle* h, const float* chunk_latent, float* out_latent, i
   h->info.call = call;
   h->info.num_entries = na;
   h->info.steps = h->n;
-  for (int j = 0; j < 8; ++j) h->info.chunk[j] = (j < h->n && tdh->e[j].active) ? tdh->e[j].X : -1;
+  for (int j = 0; j < 8; ++j) h->info.chunk[j] = (j < h->n && tdh->e[j * h->B].active) ? tdh->e[j * h->B].X : -1;
   h->info.out_chunk = (last && tdh->out_entry >= 0) ? h->ctl.out_chunk(call) : -1;
   if (out_chunk) *out_chunk = h->info.out_chunk;
 
-  if (first) CK(cudaMemcpyAsync(h->lat_in, chunk_latent, size_t(h->CTHW) * 4, cudaMemcpyDefault, h->stream));
+  if (first) CK(cudaMemcpyAsync(h->lat_in, chunk_latent, size_t(h->B) * h->CTHW * 4, cudaMemcpyDefault, h->stream));
   // RoPE re-base (rare: once every T_reset frames) of every local block's ring slots of
   // the re-basing lanes, before any block of this call writes or attends (R3).
   bool any_rebase = false;
-  for (int j = 0; j < h->n; ++j) any_rebase |= (tdh->e[j].active && tdh->e[j].rebase);
+  for (int e = 0; e < h->NE; ++e) any_rebase |= (tdh->e[e].active && tdh->e[e].rebase);
   if (any_rebase) {
-    rebase_kernel<TA><<<dim3(512, h->n), 256, 0, h->stream>>>(static_cast<TA*>(h->Kc), h->td_dev, h->rt, h->nb, h->n,
-                                                               h->S, h->m, h->W, h->L, h->d, h->hd, h->T_reset);
+    rebase_kernel<TA><<<dim3(512, h->NE), 256, 0, h->stream>>>(static_cast<TA*>(h->Kc), h->td_dev, h->rt, h->nb, h->NE,
+                                                                h->S, h->m, h->W, h->L, h->d, h->hd, h->T_reset);
     CKL();
   }
   const bool use_graph = h->graphs && !h->prof && !h->tap && h->stream != nullptr;
@@ -772,7 +788,7 @@ sdv2_status tick(sdv2_handle* h, const float* chunk_latent, float* out_latent, i
     TRY(tick_body<TA>(h, na, par));
   }
   if (last && tdh->out_entry >= 0 && out_latent)
-    CK(cudaMemcpyAsync(out_latent, h->out_stage, size_t(h->CTHW) * 4, cudaMemcpyDefault, h->stream));
+    CK(cudaMemcpyAsync(out_latent, h->out_stage, size_t(h->B) * h->CTHW * 4, cudaMemcpyDefault, h->stream));
   h->info.kernel_launches = h->launches;
   return SDV2_OK;
 }
@@ -909,7 +925,7 @@ sdv2_status sdv2_create(const sdv2_model_desc* md, const sdv2_geometry* g, const
     const BlockW& B = h->bw[0];
     const int d = h->d;
     for (int na = 1; na <= h->n; ++na) {
-      const int M = na * h->L;
+      const int M = na * h->B * h->L;
       EpiArgs ep{};
       ep.L = h->L; ep.mod = B.mod; ep.e0 = h->st.e0; ep.gate_row = 2;
       // weights of every local block (the timed launches cycle through them)
@@ -938,8 +954,12 @@ sdv2_status sdv2_create(const sdv2_model_desc* md, const sdv2_geometry* g, const
     }
     if (cudaStreamSynchronize(h->stream) != cudaSuccess) return fail(SDV2_E_CUDA);
   }
-  cudaFuncSetAttribute(gemv2_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaFuncSetAttribute(gemv2_kernel<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(gemv2_kernel<float, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(gemv2_kernel<float, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(gemv2_kernel<float, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(gemv2_kernel<bf16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(gemv2_kernel<bf16, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(gemv2_kernel<bf16, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   *out = h;
   return SDV2_OK;
 }
@@ -973,6 +993,7 @@ sdv2_status sdv2_reset_stream(sdv2_handle* h, const sdv2_stream_desc* sd, const 
   h->scfg.seed = sd->seed;
   CtlParams p;
   p.T = h->T; p.m = h->m; p.W = h->W; p.n = h->n; p.K = h->K; p.rank = h->rank; p.T_reset = h->T_reset;
+  p.B = h->B;
   p.tau = sd->sink_tau;
   h->ctl.reset(p);
   // RoPE tables (C.6): temporal positions -t_off..t_off, height 0..hn-1, width 0..wn-1; fp64 -> fp32
@@ -1015,49 +1036,51 @@ sdv2_status sdv2_reset_stream(sdv2_handle* h, const sdv2_stream_desc* sd, const 
       }
   }
   // zero lanes, controller state
-  const size_t kv = size_t(h->nb) * h->n * h->S * h->L * h->d * h->ta;
+  const size_t kv = size_t(h->nb) * h->NE * h->S * h->L * h->d * h->ta;
   CK(cudaMemsetAsync(h->Kc, 0, kv, h->stream));
   CK(cudaMemsetAsync(h->Vc, 0, kv, h->stream));
   // Attention key tiles are 128 rows and may extend past a lane's valid keys into other
   // slots / blocks / prompt versions: those rows get P = 0, but must hold finite values
   // (0 x NaN = NaN in the PV MMA), so every K/V buffer starts zeroed.
-  const size_t px = size_t(2) * h->nb * h->Lt * h->d * h->ta;
+  const size_t px = size_t(2) * h->B * h->nb * h->Lt * h->d * h->ta;
   CK(cudaMemsetAsync(h->Kx, 0, px, h->stream));
   CK(cudaMemsetAsync(h->Vx, 0, px, h->stream));
-  CK(cudaMemsetAsync(h->ctrl, 0, sizeof(CtrlState), h->stream));
   CK(cudaMemsetAsync(h->packet_base, 0, h->st.bytes, h->stream));
   {
-    CtrlState cs;
-    std::memset(&cs, 0, sizeof(cs));
-    cs.s = double(sd->s_max);   // s_{-1} = s_max (Q15)
-    CK(cudaMemcpyAsync(h->ctrl, &cs, sizeof(cs), cudaMemcpyHostToDevice, h->stream));
+    std::vector<CtrlState> cs(h->B);
+    std::memset(cs.data(), 0, sizeof(CtrlState) * h->B);
+    for (auto& c : cs) c.s = double(sd->s_max);   // s_{-1} = s_max (Q15)
+    CK(cudaMemcpyAsync(h->ctrl, cs.data(), sizeof(CtrlState) * h->B, cudaMemcpyHostToDevice, h->stream));
     CK(cudaStreamSynchronize(h->stream));
   }
-  h->pver = 0;
-  h->last_switch_call = -1;
-  sdv2_status s = set_prompt_common(h, prompt_host, 0);
-  if (s != SDV2_OK) return s;
+  for (int b = 0; b < h->B; ++b) {
+    h->pver[b] = 0;
+    h->last_switch_call[b] = -1;
+    sdv2_status s = set_prompt_common(h, prompt_host + size_t(b) * h->Lt * h->Dt, b, 0);
+    if (s != SDV2_OK) return s;
+  }
   h->stream_ready = true;
   return SDV2_OK;
 }
 
-sdv2_status sdv2_set_prompt(sdv2_handle* h, const float* prompt_host) {
-  if (!h || !prompt_host) return SDV2_E_INVALID;
+sdv2_status sdv2_set_prompt(sdv2_handle* h, int32_t stream, const float* prompt_host) {
+  if (!h || !prompt_host || stream < 0 || stream >= h->B) return SDV2_E_INVALID;
   if (!h->stream_ready) return SDV2_E_STATE;
+  const int b = stream;
   // Versions alternate between two resident slots: the switch to version v overwrites
   // the slot of version v-2, whose last chunk was admitted at call c_{v-1} - 1 and is
   // processed (entry j = n-1) at call c_{v-1} - 1 + (n-1) K.  The overwrite is ordered
   // before call c_v, so it is safe iff c_v - c_{v-1} >= (n-1) K.
   const int64_t now = h->ctl.calls();
-  if (h->last_switch_call >= 0 && now - h->last_switch_call < int64_t(h->n - 1) * h->K) {
-    h->err = "prompt switch too soon: " + std::to_string(now - h->last_switch_call) + " calls after the previous one, " +
+  if (h->last_switch_call[b] >= 0 && now - h->last_switch_call[b] < int64_t(h->n - 1) * h->K) {
+    h->err = "prompt switch too soon: " + std::to_string(now - h->last_switch_call[b]) + " calls after the previous one, " +
              std::to_string(int64_t(h->n - 1) * h->K) + " needed (two prompt versions are resident)";
     return SDV2_E_STATE;
   }
-  sdv2_status s = set_prompt_common(h, prompt_host, h->pver + 1);
+  sdv2_status s = set_prompt_common(h, prompt_host, b, h->pver[b] + 1);
   if (s == SDV2_OK) {
-    h->pver += 1;
-    h->last_switch_call = now;
+    h->pver[b] += 1;
+    h->last_switch_call[b] = now;
   }
   return s;
 }
@@ -1079,7 +1102,7 @@ sdv2_status sdv2_stage_io_buffers(sdv2_handle* h, int32_t parity, sdv2_stage_io*
   io->act_bytes = h->K > 1 ? h->st.bytes : 0;
   io->ring_in = h->ring[0][parity];
   io->ring_out = h->ring[1][parity];
-  io->ring_bytes = size_t(h->n > 1 ? h->n - 1 : 0) * h->CTHW * 4;
+  io->ring_bytes = size_t(h->n > 1 ? h->n - 1 : 0) * h->B * h->CTHW * 4;
   return SDV2_OK;
 }
 
@@ -1091,7 +1114,7 @@ sdv2_status sdv2_get_tick_info(const sdv2_handle* h, sdv2_tick_info* info) {
 }
 
 sdv2_status sdv2_get_cache_state(sdv2_handle* h, int32_t local_block, int32_t lane, sdv2_cache_state* st) {
-  if (!h || !st || local_block < 0 || local_block >= h->nb || lane < 0 || lane >= h->n) return SDV2_E_INVALID;
+  if (!h || !st || local_block < 0 || local_block >= h->nb || lane < 0 || lane >= h->NE) return SDV2_E_INVALID;
   const LaneMeta& L = h->ctl.lane(lane);
   std::memset(st, 0, sizeof(*st));
   st->num_slots = h->S;
@@ -1105,7 +1128,7 @@ sdv2_status sdv2_get_cache_state(sdv2_handle* h, int32_t local_block, int32_t la
   if (h->rank == 0) {
     CtrlState cs;
     CK(cudaStreamSynchronize(h->stream));
-    CK(cudaMemcpy(&cs, h->ctrl, sizeof(cs), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&cs, h->ctrl + lane % h->B, sizeof(cs), cudaMemcpyDeviceToHost));
     st->noise_rate = cs.s;
     st->d_hat = cs.d_hat;
   }
@@ -1119,10 +1142,10 @@ sdv2_status sdv2_set_block_tap(sdv2_handle* h, float* per_block_out) {
 }
 
 sdv2_status sdv2_kv_lane(sdv2_handle* h, int32_t local_block, int32_t lane, int32_t which, void** ptr, size_t* elems) {
-  if (!h || !ptr || !elems || local_block < 0 || local_block >= h->nb || lane < 0 || lane >= h->n) return SDV2_E_INVALID;
+  if (!h || !ptr || !elems || local_block < 0 || local_block >= h->nb || lane < 0 || lane >= h->NE) return SDV2_E_INVALID;
   const size_t per_lane = size_t(h->S) * h->L * h->d;
   char* base = static_cast<char*>(which ? h->Vc : h->Kc);
-  *ptr = base + ((size_t(local_block) * h->n + lane) * per_lane) * h->ta;
+  *ptr = base + ((size_t(local_block) * h->NE + lane) * per_lane) * h->ta;
   *elems = per_lane;
   return SDV2_OK;
 }

@@ -45,6 +45,11 @@ class StageTransport:
         self.pending = []
         self._stage = {}
         self.base = 0                   # stage calls made before the current run (buffer parity)
+        # ring-closure packets whose consumer call (producer + K) lies beyond the run that
+        # produced them: kept by the last rank, shipped to rank 0 when the run drains and
+        # copied into ring_in before the consuming call of a later run (exact chaining of
+        # runs, e.g. around an online re-partition).  global producer call -> tensor
+        self.ring_stash = {}
 
     def _buf(self, t):
         """Tensor used on the wire (a host copy when staging through the host)."""
@@ -69,12 +74,15 @@ class StageTransport:
                     wire.copy_(src)
                 ops.append(dist.P2POp(dist.isend, wire, r + 1))
             # ring packet of call c is consumed by rank 0 at call c + K
-            if r == K - 1 and K > 1 and cur["ring_out"].numel() and c + K < num_calls:
+            if r == K - 1 and K > 1 and cur["ring_out"].numel():
                 src = cur["ring_out"]
-                wire = self._buf(src)
-                if wire is not src:
-                    wire.copy_(src)
-                ops.append(dist.P2POp(dist.isend, wire, 0))
+                if c + K < num_calls:
+                    wire = self._buf(src)
+                    if wire is not src:
+                        wire.copy_(src)
+                    ops.append(dist.P2POp(dist.isend, wire, 0))
+                else:       # consumer in a later run: keep a copy (the parity buffer is reused)
+                    self.ring_stash[self.base + c] = src.clone()
         nxt = self.io((self.base + c + 1) & 1)
         if c + 1 >= num_calls:
             return ops, post
@@ -84,12 +92,16 @@ class StageTransport:
             ops.append(dist.P2POp(dist.irecv, wire, r - 1))
             if wire is not dst:
                 post.append((dst, wire))
-        if r == 0 and K > 1 and c + 1 >= K and nxt["ring_in"].numel():
+        g = self.base + c + 1                       # global index of the next call
+        if r == 0 and K > 1 and g >= K and nxt["ring_in"].numel():
             dst = nxt["ring_in"]
-            wire = self._buf(dst)
-            ops.append(dist.P2POp(dist.irecv, wire, K - 1))
-            if wire is not dst:
-                post.append((dst, wire))
+            if g - K < self.base:                   # produced in an earlier run: stashed here
+                dst.copy_(self.ring_stash.pop(g - K).to(dst.device))
+            else:
+                wire = self._buf(dst)
+                ops.append(dist.P2POp(dist.irecv, wire, K - 1))
+                if wire is not dst:
+                    post.append((dst, wire))
         return ops, post
 
     def post(self, c: int, num_calls: int):
@@ -123,14 +135,45 @@ class StageTransport:
                 keep.append((sends, ["send"] * len(sends), []))
         self.pending = keep
 
-    def drain(self):
-        """Wait for every outstanding transfer (end of a run)."""
+    def drain(self, num_calls: int):
+        """Wait for every outstanding transfer (end of a run of num_calls), then move the
+        ring packets whose consumers lie in a later run from the last rank to rank 0."""
         for works, _, post in self.pending:
             for w in works:
                 w.wait()
             for dst, wire in post:
                 dst.copy_(wire, non_blocking=False)
         self.pending = []
+        K, r, dist = self.world, self.rank, self.dist
+        if K < 2 or r not in (0, K - 1):
+            return
+        ring_bytes = self.io(0)["ring_in" if r == 0 else "ring_out"].numel()
+        if not ring_bytes:
+            return
+        end = self.base + num_calls
+        producers = list(range(max(self.base, end - K), end))   # produced in this run, consumed later
+        ops, post = [], []
+        for p in producers:
+            if r == K - 1:
+                src = self.ring_stash.pop(p)
+                wire = self._buf(src)
+                if wire is not src:
+                    wire.copy_(src)
+                ops.append(dist.P2POp(dist.isend, wire, 0))
+            else:
+                dev = self.io(0)["ring_in"].device
+                buf = self.torch.empty(ring_bytes, dtype=self.torch.uint8, device=dev)
+                wire = self._buf(buf) if self.host else buf
+                ops.append(dist.P2POp(dist.irecv, wire, K - 1))
+                post.append((p, buf, wire))
+        if self.host and self.device is not None:
+            self.torch.cuda.synchronize(self.device)
+        for w in (dist.batch_isend_irecv(ops) if ops else []):
+            w.wait()
+        for p, buf, wire in post:
+            if wire is not buf:
+                buf.copy_(wire)
+            self.ring_stash[p] = buf
 
 
 def stage_io_tensors(stage, workspace):
@@ -165,10 +208,12 @@ def run_pipelined(stage, transport: StageTransport, chunks, out_cb, num_calls: i
     Every transfer of a run is matched inside the run, so the pipeline is drained when
     it returns (a barrier between runs is safe; a barrier inside one would deadlock:
     rank s waits for rank s-1's call c before its own call c).  Ring-closure packets
-    whose consumer call lies beyond the run are not sent; rank 0 then re-noises from
-    its previous ring buffer (timing-equivalent; numerics tests use one run)."""
+    whose consumer call lies beyond the run are stashed and delivered when the run
+    drains, so consecutive runs continue the stream exactly (tests/test_pipeline_cpu.py)."""
     import contextlib
     transport.base = getattr(stage, "calls", 0)
+    if num_calls < 1:
+        return []
     stream = getattr(stage, "stream", None)
     ctx = transport.torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()
     with ctx:   # NCCL waits and host-staging copies are ordered on the stage's stream
@@ -184,7 +229,7 @@ def run_pipelined(stage, transport: StageTransport, chunks, out_cb, num_calls: i
             if after_call:
                 after_call(c, oc)
             transport.post(c, num_calls)
-        transport.drain()
+        transport.drain(num_calls)
     return outs
 
 

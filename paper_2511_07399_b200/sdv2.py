@@ -34,7 +34,8 @@ class ModelDescC(ctypes.Structure):
 
 class GeometryC(ctypes.Structure):
     _fields_ = [("latent_h", ctypes.c_int32), ("latent_w", ctypes.c_int32), ("chunk_frames", ctypes.c_int32),
-                ("steps", ctypes.c_int32), ("sink_chunks", ctypes.c_int32), ("window_chunks", ctypes.c_int32)]
+                ("steps", ctypes.c_int32), ("sink_chunks", ctypes.c_int32), ("window_chunks", ctypes.c_int32),
+                ("streams", ctypes.c_int32)]
 
 
 class PipelineC(ctypes.Structure):
@@ -91,7 +92,7 @@ def _declare(lib):
                                 ctypes.c_int, ctypes.POINTER(WeightsC), P, ctypes.c_size_t, ctypes.c_int, P,
                                 ctypes.POINTER(ExecOptionsC), ctypes.POINTER(P)]
     lib.sdv2_reset_stream.argtypes = [P, ctypes.POINTER(StreamDescC), P]
-    lib.sdv2_set_prompt.argtypes = [P, P]
+    lib.sdv2_set_prompt.argtypes = [P, ctypes.c_int32, P]
     lib.sdv2_denoise_chunk.argtypes = [P, P, P, ctypes.POINTER(ctypes.c_int64)]
     lib.sdv2_stage_io_buffers.argtypes = [P, ctypes.c_int32, ctypes.POINTER(StageIOC)]
     lib.sdv2_get_tick_info.argtypes = [P, ctypes.POINTER(TickInfoC)]
@@ -159,7 +160,8 @@ def model_desc_c(md) -> ModelDescC:
 
 
 def geometry_c(g) -> GeometryC:
-    return GeometryC(g.latent_h, g.latent_w, g.chunk_frames, g.steps, g.sink_chunks, g.window_chunks)
+    return GeometryC(g.latent_h, g.latent_w, g.chunk_frames, g.steps, g.sink_chunks, g.window_chunks,
+                     getattr(g, "streams", 1))
 
 
 def partition(costs: Sequence[float], stages: int, extra_first=0.0, extra_last=0.0):
@@ -183,10 +185,10 @@ def ctl_lib():
             raise RuntimeError(f"{CTL_LIB_PATH} is missing: run `python -m paper_2511_07399_b200.build`")
         L = ctypes.CDLL(CTL_LIB_PATH)
         L.sdv2ctl_new.restype = ctypes.c_void_p
-        L.sdv2ctl_new.argtypes = [ctypes.c_int32] * 7 + [ctypes.c_double]
+        L.sdv2ctl_new.argtypes = [ctypes.c_int32] * 7 + [ctypes.c_double, ctypes.c_int32]
         L.sdv2ctl_free.argtypes = [ctypes.c_void_p]
-        L.sdv2ctl_set_prompt_mean.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.c_int32,
-                                              ctypes.c_int32]
+        L.sdv2ctl_set_prompt_mean.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.POINTER(ctypes.c_double),
+                                              ctypes.c_int32, ctypes.c_int32]
         L.sdv2ctl_call.restype = ctypes.c_int32
         L.sdv2ctl_call.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int64)]
         L.sdv2ctl_lane_state.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.POINTER(CacheStateC)]
@@ -202,27 +204,33 @@ def ctl_lib():
 class HostControl:
     """The library's host control plane driven without a GPU (tests)."""
 
-    def __init__(self, T, m, W, n, K=1, rank=0, T_reset=4, tau=0.95):
+    def __init__(self, T, m, W, n, K=1, rank=0, T_reset=4, tau=0.95, B=1):
         self.L = ctl_lib()
-        self.n = n
-        self.h = self.L.sdv2ctl_new(T, m, W, n, K, rank, T_reset, tau)
+        self.n, self.B = n, B
+        self.h = self.L.sdv2ctl_new(T, m, W, n, K, rank, T_reset, tau, B)
         if not self.h:
             raise SDV2Error("invalid control parameters")
         self.F = self.L.sdv2ctl_max_frames()
 
-    def set_prompt_mean(self, h, pver):
+    def set_prompt_mean(self, h, pver, stream=0):
         a = np.ascontiguousarray(h, dtype=np.float64)
-        self.L.sdv2ctl_set_prompt_mean(self.h, a.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), a.size, pver)
+        st = self.L.sdv2ctl_set_prompt_mean(self.h, stream, a.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                            a.size, pver)
+        if st != 0:
+            raise SDV2Error("stream out of range")
 
     def call(self):
-        out = (ctypes.c_int32 * (self.n * (8 + self.F)))()
+        """One call; entries e = j B + b."""
+        w = 10 + self.F
+        out = (ctypes.c_int32 * (self.n * self.B * w))()
         oc = ctypes.c_int64()
         na = self.L.sdv2ctl_call(self.h, out, ctypes.byref(oc))
         ents = []
-        for j in range(self.n):
-            o = out[j * (8 + self.F):(j + 1) * (8 + self.F)]
+        for i in range(self.n * self.B):
+            o = out[i * w:(i + 1) * w]
             ents.append({"X": o[0], "j": o[1], "active": o[2], "write_slot": o[3], "nvalid": o[4],
-                         "refresh_mask": o[5], "rebase": o[6], "pver": o[7], "pos": list(o[8:])})
+                         "refresh_mask": o[5], "rebase": o[6], "pver": o[7], "stream": o[8], "xslot": o[9],
+                         "pos": list(o[10:])})
         return na, ents, oc.value
 
     def lane_state(self, lane):
@@ -292,18 +300,24 @@ class Stage:
         del keep
 
     # ---------------------------------------------------------------- stream
-    def reset_stream(self, sd, prompt: np.ndarray):
+    def reset_stream(self, sd, prompt):
+        """prompt: one [text_len, text_dim] array per stream (a list), or a single array
+        when the handle has one stream."""
         ts = (ctypes.c_float * len(sd.timesteps))(*sd.timesteps)
         self._ts = ts
         c = StreamDescC(ts, len(sd.timesteps), sd.rope_reset_frames, sd.motion_k, sd.motion_sigma, sd.s_min,
                         sd.s_max, sd.ema_lambda, sd.sink_tau, sd.seed)
-        p = np.ascontiguousarray(prompt, dtype=np.float32)
+        B = getattr(self.geom, "streams", 1)
+        ps = list(prompt) if isinstance(prompt, (list, tuple)) else [prompt]
+        if len(ps) != B:
+            raise SDV2Error(f"{len(ps)} prompts for {B} streams")
+        p = np.ascontiguousarray(np.stack([np.asarray(x, dtype=np.float32) for x in ps]), dtype=np.float32)
         _check(self.L.sdv2_reset_stream(self.h, ctypes.byref(c), ctypes.c_void_p(p.ctypes.data)), self.h)
         self.calls = 0
 
-    def set_prompt(self, prompt: np.ndarray):
+    def set_prompt(self, prompt: np.ndarray, stream: int = 0):
         p = np.ascontiguousarray(prompt, dtype=np.float32)
-        _check(self.L.sdv2_set_prompt(self.h, ctypes.c_void_p(p.ctypes.data)), self.h)
+        _check(self.L.sdv2_set_prompt(self.h, stream, ctypes.c_void_p(p.ctypes.data)), self.h)
 
     def denoise_chunk(self, chunk_ptr: Optional[int], out_ptr: Optional[int]) -> int:
         """chunk_ptr / out_ptr: raw host or device addresses (or None).  Returns the chunk
@@ -365,3 +379,74 @@ class Stage:
             self.close()
         except Exception:
             pass
+
+
+# ------------------------------------------------------------------ SLO batching (N2)
+class LatencyPointC(ctypes.Structure):
+    _fields_ = [("chunk_frames", ctypes.c_int32), ("streams", ctypes.c_int32), ("latency_s", ctypes.c_double)]
+
+
+class SloC(ctypes.Structure):
+    _fields_ = [("target_fps", ctypes.c_double), ("frame_deadline_s", ctypes.c_double),
+                ("px_per_latent", ctypes.c_int32)]
+
+
+class BatchDecisionC(ctypes.Structure):
+    _fields_ = [("chunk_frames", ctypes.c_int32), ("streams", ctypes.c_int32), ("latency_s", ctypes.c_double),
+                ("fps", ctypes.c_double), ("feasible", ctypes.c_int32)]
+
+
+class AimdStateC(ctypes.Structure):
+    _fields_ = [("streams", ctypes.c_int32), ("chunk_frames", ctypes.c_int32), ("b_max", ctypes.c_int32),
+                ("streak", ctypes.c_int32), ("ok_run", ctypes.c_int32), ("infeasible", ctypes.c_int32)]
+
+
+def _host_lib():
+    """The host-only entry points live in both libraries; prefer the full one when built."""
+    L = lib() if os.path.exists(_LIB_PATH) else ctl_lib()
+    if not getattr(L, "_slo_declared", False):
+        L.sdv2_slo_select.argtypes = [ctypes.POINTER(LatencyPointC), ctypes.c_int32, ctypes.POINTER(SloC),
+                                      ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(BatchDecisionC)]
+        L.sdv2_slo_select.restype = ctypes.c_int
+        L.sdv2_slo_adapt.argtypes = [ctypes.POINTER(AimdStateC), ctypes.c_double, ctypes.POINTER(SloC)]
+        L.sdv2_slo_adapt.restype = ctypes.c_int
+        L.sdv2_slo_fit.argtypes = [ctypes.POINTER(LatencyPointC), ctypes.c_int32, ctypes.POINTER(ctypes.c_double),
+                                   ctypes.POINTER(ctypes.c_double)]
+        L.sdv2_slo_fit.restype = ctypes.c_int
+        L._slo_declared = True
+    return L
+
+
+def _table_c(table):
+    items = sorted(table.items())
+    arr = (LatencyPointC * len(items))(*[LatencyPointC(t, b, lat) for (t, b), lat in items])
+    return arr, len(items)
+
+
+def slo_select(table, target_fps, frame_deadline_s, buffered_frames, b_max, px_per_latent=4):
+    """table {(T', B): measured call latency s} -> decision dict (library scheduler)."""
+    arr, n = _table_c(table)
+    out = BatchDecisionC()
+    slo = SloC(target_fps, frame_deadline_s, px_per_latent)
+    _check(_host_lib().sdv2_slo_select(arr, n, ctypes.byref(slo), buffered_frames, b_max, ctypes.byref(out)))
+    return {"T": out.chunk_frames, "B": out.streams, "latency": out.latency_s, "fps": out.fps,
+            "feasible": bool(out.feasible)}
+
+
+class SloAdapter:
+    """AIMD online adaptation of the batch size (library state machine)."""
+
+    def __init__(self, B, T, b_max, streak, target_fps, frame_deadline_s, px_per_latent=4):
+        self.st = AimdStateC(B, T, b_max, streak, 0, 0)
+        self.slo = SloC(target_fps, frame_deadline_s, px_per_latent)
+
+    def adapt(self, observed_latency_s):
+        _check(_host_lib().sdv2_slo_adapt(ctypes.byref(self.st), observed_latency_s, ctypes.byref(self.slo)))
+        return {"B": self.st.streams, "infeasible": bool(self.st.infeasible)}
+
+
+def slo_fit(table):
+    arr, n = _table_c(table)
+    a, b = ctypes.c_double(), ctypes.c_double()
+    _check(_host_lib().sdv2_slo_fit(arr, n, ctypes.byref(a), ctypes.byref(b)))
+    return a.value, b.value

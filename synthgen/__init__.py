@@ -55,6 +55,7 @@ class Geometry:
     steps: int                    # n = B (stream batch = in-flight denoising steps)
     sink_chunks: int              # m
     window_chunks: int            # W
+    streams: int = 1              # B: independent streams batched per call (SLO batch, N2)
 
     def tokens_per_chunk(self, md: ModelDesc) -> int:
         return (self.chunk_frames // md.patch_t) * (self.latent_h // md.patch_h) * (self.latent_w // md.patch_w)

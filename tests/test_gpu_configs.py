@@ -215,3 +215,50 @@ def test_tuned_handles_bitwise_equal_13b():
     assert sorted(a) == sorted(b) and a
     for X in a:
         assert np.array_equal(a[X], b[X]), X
+
+
+# ------------------------------------------- multi-stream batching (N2)
+def _check_streams(cfg, B, n_chunks, switches, prec, dtype=np.float64, n_oracle=None):
+    from gpu_harness import multi_inputs, run_gpu_streams, stream_oracles
+    W, chunks, prompts = multi_inputs(cfg, B, n_chunks, switches)
+    recs = stream_oracles(cfg, W, chunks, prompts, switches, dtype=dtype, n_oracle=n_oracle)
+    outs, taps, meta = run_gpu_streams(cfg, W, chunks, prompts, switches, prec)
+    worst = 0.0
+    for b in range(B):
+        for (X, j), tl in taps[b].items():
+            if X >= len(recs[b]):
+                continue
+            for blk in range(cfg.model.num_blocks):
+                err = rel_l2(tl[blk], recs[b][X]["entries"][j]["taps"][blk])
+                worst = max(worst, err)
+                assert err <= TOL[prec], (b, X, j, blk, err)
+        for X, o in outs[b].items():
+            if X < len(recs[b]):
+                assert rel_l2(o, recs[b][X]["out"]) <= TOL[prec], (b, X)
+        for (X, j), (slots, s_rate, dh) in meta[b].items():
+            if X >= len(recs[b]):
+                continue
+            assert slots == {s: (t, p[0]) for s, (t, p) in recs[b][X]["lane_state"][(0, j)].items()}, (b, X, j)
+            if j == 0:
+                assert s_rate == pytest.approx(recs[b][X]["motion"]["s"], rel=1e-6)
+    assert all(len(outs[b]) > 0 for b in range(B))
+    return worst
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("prec", [SDV2_FP32, SDV2_BF16])
+def test_multi_stream_tiny(prec):
+    """3 streams x 2 steps batched per call; every stream has its own latents, controller,
+    Philox key, prompts and prompt switches (so its own sink refreshes): each equals its
+    own oracle run."""
+    cfg = sg.CONFIGS["tiny"]
+    _check_streams(cfg, 3, 10, [(6,), (3,), ()], prec)
+
+
+@pytest.mark.gpu
+def test_multi_stream_13b_bf16():
+    """configs[1] block shapes, 4 streams x 1 step (M = 6240 rows per call), 1 block."""
+    cfg = _cfg("wan13_480p_1step", nblocks=1, num_chunks=3)
+    cfg = dataclasses.replace(cfg, stream=dataclasses.replace(cfg.stream, rope_reset_frames=4))
+    worst = _check_streams(cfg, 4, 3, [(), (2,), (), (1,)], SDV2_BF16, dtype=np.float32)
+    print(f"1.3B B=4: worst block rel-L2 {worst:.3e}")

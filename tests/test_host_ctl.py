@@ -144,3 +144,47 @@ def test_partition_examples_and_bruteforce(golden_dir):
         assert bounds[0] == 0 and bounds[-1] == B and all(bounds[i] < bounds[i + 1] for i in range(K))
     with pytest.raises(Exception):
         partition([1.0, 1.0], 3)
+
+
+@pytest.mark.parametrize("T,m,W,T_reset,n,K,B", [(1, 1, 4, 6, 2, 1, 3), (2, 2, 3, 8, 2, 2, 2), (1, 1, 2, 3, 1, 1, 8),
+                                                 (1, 0, 2, 4, 4, 1, 4)])
+def test_multi_stream_replay_matches_independent_oracles(T, m, W, T_reset, n, K, B):
+    """B streams batched per call (SLO batch; "different colors denote distinct
+    latent streams", Fig. parallel): entry e = j B + b of the library's call equals stream b's
+    own oracle control plane at chunk c - jK (each stream has its own prompts, so its own
+    sink refreshes and prompt versions), and lane e holds stream b's lane state."""
+    geom = sg.Geometry(8, 8, T, n, m, W)
+    rng = np.random.default_rng(11 + B)
+    N = 400
+    prompts = [rng.standard_normal(4) for _ in range(5)]
+    hs, pidx, refs = [], [], []
+    for b in range(B):
+        sw = sorted(set(int(x) for x in rng.integers(1, N, size=4)))
+        pi = [sum(1 for s in sw if X >= s) for X in range(N)]
+        h = [prompts[(pi[X] + b) % len(prompts)] for X in range(N)]
+        hs.append(h)
+        pidx.append(pi)
+        refs.append(_oracle_lane_states(geom, T_reset, 0.95, h))
+    hc = HostControl(T, m, W, n, K, 0, T_reset, 0.95, B=B)
+    S = m + W
+    for c in range(N):
+        for b in range(B):
+            hc.set_prompt_mean(hs[b][c], pidx[b][c], stream=b)
+        na, ents, oc = hc.call()
+        assert na == B * sum(1 for j in range(n) if c - j * K >= 0)
+        assert oc == (c - (n - 1) * K if c - (n - 1) * K >= 0 else -1)
+        for j in range(n):
+            X = c - j * K
+            for b in range(B):
+                e = ents[j * B + b]
+                assert e["active"] == (X >= 0) and e["stream"] == b and e["j"] == j
+                if X < 0:
+                    continue
+                act = refs[b][X][0]
+                assert e["X"] == X and e["pos"][:T] == act["pos"] and bool(e["rebase"]) == act["rebase"]
+                assert e["pver"] == pidx[b][X] and e["xslot"] == 2 * b + (pidx[b][X] & 1)
+                assert e["refresh_mask"] == sum(1 << i for i, r in enumerate(act["refresh"]) if r)
+                if c % 31 == 0 or act["rebase"] or e["refresh_mask"]:
+                    _check_lane(hc.lane_state(j * B + b), refs[b][X][1], refs[b][X][2], S)
+    with pytest.raises(Exception):
+        HostControl(T, m, W, 8, K, 0, T_reset, 0.95, B=3)      # 24 entries > 16
