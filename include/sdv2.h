@@ -75,10 +75,16 @@ typedef struct {
   int32_t streams;              /* B >= 1 streams per call; streams * steps <= 16 */
 } sdv2_geometry;
 
-/* Pipeline stage of this handle.  world = K stages; this rank owns DiT
- * blocks [block_begin, block_end).  NULL desc = single stage owning every block. */
+/* Pipeline stage of this handle.  world = K stages; this rank runs DiT
+ * blocks [block_begin, block_end).  NULL desc = single stage owning every block.
+ * Online re-partitioning ("dynamically reallocates blocks between devices"):
+ * the handle keeps weights, prompt K/V and KV lanes for the resident blocks
+ * [resident_begin, resident_end) ⊇ [block_begin, block_end) (0, 0 = the block range), so
+ * sdv2_set_block_range can move the boundary inside it after the moved blocks' KV lanes
+ * were copied in (sdv2_block_kv).  local_block arguments below index the resident range. */
 typedef struct {
   int32_t world, rank, block_begin, block_end;
+  int32_t resident_begin, resident_end;
 } sdv2_pipeline_desc;
 
 /* Weights: fp32 values that are bf16-representable, nn.Linear
@@ -87,7 +93,7 @@ typedef struct {
  * Order: the 15 global tensors
  *   patch_w[d,4C] patch_b[d] txt1_w[d,Dt] txt1_b[d] txt2_w[d,d] txt2_b[d]
  *   t1_w[d,256] t1_b[d] t2_w[d,d] t2_b[d] tp_w[6d,d] tp_b[6d] head_mod[2,d] head_w[4C,d] head_b[4C]
- * then, for each block b in [block_begin, block_end), the 27 block tensors
+ * then, for each RESIDENT block b (sdv2_pipeline_desc), the 27 block tensors
  *   mod[6,d] wq bq wk bk wv bv wo bo gq gk n3_g n3_b wcq bcq wck bck wcv bcv wco bco gcq gck
  *   w1[F,d] b1[F] w2[d,F] b2[d]            ([d,d] / [d] unless stated)            */
 typedef struct {
@@ -234,6 +240,19 @@ sdv2_status sdv2_kv_lane(sdv2_handle* h, int32_t local_block, int32_t lane, int3
 /* CUDA-graph replay of the per-call device work (default on; keyed by the number of
  * active entries and the call parity; not used while profiling or tapping). */
 sdv2_status sdv2_set_graphs(sdv2_handle* h, int32_t enable);
+/* Mean device time per call of each resident block's span (class 4) since profiling was
+ * enabled; out[i] = resident block resident_begin + i (0 if it did not run).  count >=
+ * resident blocks.  Feeds the online block scheduler (sdv2_rebalance). */
+sdv2_status sdv2_profile_block_ms(sdv2_handle* h, double* out, int32_t count);
+/* Change the active block range inside the resident range (between calls; synchronises
+ * the stream and drops the captured call graphs).  The caller must first copy into this
+ * handle the KV lanes of every block that becomes active here, from its previous owner
+ * (the control-plane metadata is replicated on every rank, so only K / V move). */
+sdv2_status sdv2_set_block_range(sdv2_handle* h, int32_t block_begin, int32_t block_end);
+/* K (which = 0) or V (1) lane storage of resident global block `block`: one contiguous
+ * device range [streams * steps lanes][m + W slots][L][dim] of the precision's element
+ * type (the unit an online re-partition moves between ranks). */
+sdv2_status sdv2_block_kv(sdv2_handle* h, int32_t block, int32_t which, void** ptr, size_t* bytes);
 /* Enable (1, resets the accumulators) or disable (0) per-class event timing. */
 sdv2_status sdv2_profile_enable(sdv2_handle* h, int32_t enable);
 /* Synchronises the stream and returns the accumulated per-class times. */
@@ -269,6 +288,17 @@ sdv2_status sdv2_debug_attention(const void* q, const void* K, const void* V, vo
 sdv2_status sdv2_partition(const double* block_costs, int32_t num_blocks, int32_t stages,
                            double extra_first, double extra_last, int32_t* bounds_out,
                            double* max_stage_out);
+
+/* Online DiT-block scheduler: ema[b] <- alpha * measured[b] +
+ * (1 - alpha) * ema[b] (ema[b] == 0: first sample), then the exact min-max partition of
+ * the smoothed times with the first / last stage extras; the new bounds (K+1 entries) are
+ * adopted (changed = 1) only if they lower the predicted max stage time by more than
+ * (hysteresis + 1e-9) x the current partition's, else new_bounds = cur_bounds.  Never increases the
+ * predicted max stage time.  pred_cur / pred_new may be NULL. */
+sdv2_status sdv2_rebalance(const double* measured_block_ms, int32_t num_blocks, int32_t stages,
+                           double extra_first, double extra_last, double alpha, double hysteresis,
+                           double* ema, const int32_t* cur_bounds, int32_t* new_bounds, int32_t* changed,
+                           double* pred_cur, double* pred_new);
 
 /* ---- SLO-aware batching scheduler (host only) ----
  * A latency point is one MEASURED call latency L(T', B): chunk_frames = T' latent frames

@@ -28,7 +28,8 @@ def _stale(out, srcs):
 def build(force=False, verbose_ptxas=False):
     hdrs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
     hdrs.append(os.path.join(HERE, "..", "include", "sdv2.h"))
-    ctl_srcs = [os.path.join(CSRC, "ctl.cpp"), os.path.join(CSRC, "ctl_abi.cpp"), os.path.join(CSRC, "slo.cpp")]
+    ctl_srcs = [os.path.join(CSRC, "ctl.cpp"), os.path.join(CSRC, "ctl_abi.cpp"), os.path.join(CSRC, "slo.cpp"),
+                os.path.join(CSRC, "balance.cpp")]
     ctl_out = os.path.join(HERE, "libsdv2_ctl.so")
     if force or _stale(ctl_out, ctl_srcs + hdrs):
         _run(["g++", "-std=c++17", "-O2", "-shared", "-fPIC", "-o", ctl_out] + ctl_srcs)

@@ -86,7 +86,9 @@ struct sdv2_handle {
   sdv2_model_desc md;
   sdv2_geometry g;
   sdv2_precision prec;
-  int K = 1, rank = 0, b0 = 0, b1 = 0, nb = 0;
+  int K = 1, rank = 0, b0 = 0, b1 = 0, nb = 0;   // active global blocks [b0, b1); nb = resident count
+  int r0 = 0;                                     // first resident (weights + KV carved) global block
+  int a0 = 0, a1 = 0;                             // active range as resident-local indices
   int d, H, hd, F, C, T, hh, ww, L, n, m, W, S, Lt, Dt, CTHW, Mmax, P;
   int B = 1;                  // streams batched per call (SLO batch)
   int NE = 1;                 // entries per call = B n (entry e = j B + b = KV lane e)
@@ -158,9 +160,11 @@ struct sdv2_handle {
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_next = 0;
-  struct ProfRec { int cls; double flops; cudaEvent_t a, b; };
+  struct ProfRec { int cls; double flops; cudaEvent_t a, b; int blk; };
   std::vector<ProfRec> prof_recs;
   sdv2_profile prof_acc;
+  std::vector<double> prof_blk_ms;     // [nb] summed block-span ms (class 4) per resident block
+  std::vector<int64_t> prof_blk_n;
 };
 
 namespace {
@@ -169,8 +173,9 @@ struct ProfScope {
   sdv2_handle* h;
   int cls;
   double flops;
+  int blk;
   cudaEvent_t a = nullptr;
-  ProfScope(sdv2_handle* h_, int c, double f) : h(h_), cls(c), flops(f) {
+  ProfScope(sdv2_handle* h_, int c, double f, int blk_ = -1) : h(h_), cls(c), flops(f), blk(blk_) {
     if (!h->prof) return;
     if (h->ev_next + 2 > h->ev_pool.size()) {
       for (int i = 0; i < 256; ++i) {
@@ -186,7 +191,7 @@ struct ProfScope {
     if (!h->prof || !a) return;
     cudaEvent_t b = h->ev_pool[h->ev_next++];
     cudaEventRecord(b, h->stream);
-    h->prof_recs.push_back({cls, flops, a, b});
+    h->prof_recs.push_back({cls, flops, a, b, blk});
   }
 };
 }  // namespace
@@ -337,13 +342,28 @@ sdv2_status fill_dims(sdv2_handle* h, const sdv2_model_desc* md, const sdv2_geom
       return SDV2_E_INVALID;
     }
     h->K = pp->world; h->rank = pp->rank; h->b0 = pp->block_begin; h->b1 = pp->block_end;
+    if (pp->resident_begin == 0 && pp->resident_end == 0) {
+      h->r0 = h->b0;
+      h->nb = h->b1 - h->b0;
+    } else {
+      if (pp->resident_begin < 0 || pp->resident_end > md->num_blocks || pp->resident_begin > h->b0 ||
+          pp->resident_end < h->b1) {
+        *why = "resident range must contain the block range";
+        return SDV2_E_INVALID;
+      }
+      h->r0 = pp->resident_begin;
+      h->nb = pp->resident_end - pp->resident_begin;
+    }
   } else {
     h->K = 1; h->rank = 0; h->b0 = 0; h->b1 = md->num_blocks;
+    h->r0 = 0;
+    h->nb = md->num_blocks;
   }
+  h->a0 = h->b0 - h->r0;
+  h->a1 = h->b1 - h->r0;
   // the control plane keeps the records of the last kRecRing admitted chunks; the oldest
   // in-flight entry is (n-1) K calls old
   if (int64_t(h->n - 1) * h->K + 1 > kRecRing) { *why = "(steps - 1) * world + 1 exceeds the chunk-record ring"; return SDV2_E_INVALID; }
-  h->nb = h->b1 - h->b0;
   return SDV2_OK;
 }
 
@@ -455,8 +475,8 @@ sdv2_status attention(sdv2_handle* h, const AttnArgs& aa, int Mrows_entries, dou
       if (aa.cross) {
         Kb = h->Kx; Vb = h->Vx;
         kv_rows = 2LL * h->B * h->nb * h->Lt;
-        ta.kv_row0 = bl * h->Lt;
-        ta.kv_lane_rows = h->nb * h->Lt;
+        ta.kv_row0 = bl * 2 * h->B * h->Lt;     // prompt K/V [nb][2B slots][Lt][d]
+        ta.kv_lane_rows = h->Lt;
       } else {
         Kb = h->Kc; Vb = h->Vc;
         kv_rows = (long long)h->nb * h->NE * h->S * h->L;
@@ -580,8 +600,9 @@ sdv2_status run_block(sdv2_handle* h, int bl, int rows, int n_act) {
     CKL();
   }
   const size_t px = size_t(h->Lt) * d;
-  aa.q = h->q; aa.K = static_cast<TA*>(h->Kx) + bl * px; aa.V = static_cast<TA*>(h->Vx) + bl * px;
-  aa.kv_lane_stride = size_t(h->nb) * px; aa.cross = 1; aa.Lk_cross = h->Lt;
+  aa.q = h->q; aa.K = static_cast<TA*>(h->Kx) + size_t(bl) * 2 * h->B * px;
+  aa.V = static_cast<TA*>(h->Vx) + size_t(bl) * 2 * h->B * px;
+  aa.kv_lane_stride = px; aa.cross = 1; aa.Lk_cross = h->Lt;
   TRY(attention(h, aa, n_act, 4.0 * double(rows) * h->Lt * d, bl));
   // 7. cross out projection, ungated residual
   ep.out = h->st.x; ep.ldo = d; ep.bias = B.bco;
@@ -592,7 +613,7 @@ sdv2_status run_block(sdv2_handle* h, int bl, int rows, int n_act) {
   TRY(gemm_act(h, h->a, B.w1, rows, h->F, d, EPI_GELU, ep));
   ep.out = h->st.x; ep.ldo = d; ep.bias = B.b2; ep.mod = B.mod; ep.e0 = h->st.e0; ep.gate_row = 5;
   TRY(gemm_act(h, h->hbuf, B.w2, rows, d, h->F, EPI_RES_GATE, ep));
-  if (h->tap) CK(cudaMemcpyAsync(h->tap + size_t(bl) * h->Mmax * d, h->st.x, size_t(rows) * d * 4,
+  if (h->tap) CK(cudaMemcpyAsync(h->tap + size_t(bl - h->a0) * h->Mmax * d, h->st.x, size_t(rows) * d * 4,
                                  cudaMemcpyDeviceToDevice, h->stream));
   return SDV2_OK;
 }
@@ -612,8 +633,8 @@ sdv2_status embed_prompt(sdv2_handle* h, const float* prompt_host, int b_stream,
   for (int b = 0; b < h->nb; ++b) {
     const BlockW& B = h->bw[b];
     const size_t slot = size_t(2 * b_stream + (ver & 1));   // EntryDesc::xslot
-    TA* Kd = static_cast<TA*>(h->Kx) + (slot * h->nb + b) * px;
-    TA* Vd = static_cast<TA*>(h->Vx) + (slot * h->nb + b) * px;
+    TA* Kd = static_cast<TA*>(h->Kx) + (size_t(b) * 2 * h->B + slot) * px;
+    TA* Vd = static_cast<TA*>(h->Vx) + (size_t(b) * 2 * h->B + slot) * px;
     ep.out = h->ctx_tmp; ep.bias = B.bck;
     TRY((gemm_simt<float, TA, float>(h, h->ctx, static_cast<const TA*>(B.wck), Lt, d, d, d, EPI_STORE, ep)));
     launch_k(h->pdl, rms_rows_kernel<float, TA>, dim3((Lt + 7) / 8), dim3(256), 0, h->stream, h->ctx_tmp, Kd, B.gck, Lt, d, d, h->md.eps);
@@ -697,8 +718,8 @@ sdv2_status tick_body(sdv2_handle* h, int na, int par) {
   } else {
     CK(cudaMemcpyAsync(h->packet_base, h->act_io[0][par], h->st.bytes, cudaMemcpyDeviceToDevice, h->stream));
   }
-  for (int b = 0; b < h->nb; ++b) {
-    ProfScope ps(h, 4, 0.0);
+  for (int b = h->a0; b < h->a1; ++b) {
+    ProfScope ps(h, 4, 0.0, b);
     TRY(run_block<TA>(h, b, rows, na));
   }
   if (!last) {
@@ -759,7 +780,8 @@ sdv2_status tick(sdv2_handle* h, const float* chunk_latent, float* out_latent, i
   bool any_rebase = false;
   for (int e = 0; e < h->NE; ++e) any_rebase |= (tdh->e[e].active && tdh->e[e].rebase);
   if (any_rebase) {
-    rebase_kernel<TA><<<dim3(512, h->NE), 256, 0, h->stream>>>(static_cast<TA*>(h->Kc), h->td_dev, h->rt, h->nb, h->NE,
+    rebase_kernel<TA><<<dim3(512, h->NE), 256, 0, h->stream>>>(
+        static_cast<TA*>(h->Kc) + size_t(h->a0) * h->NE * h->S * h->L * h->d, h->td_dev, h->rt, h->a1 - h->a0, h->NE,
                                                                 h->S, h->m, h->W, h->L, h->d, h->hd, h->T_reset);
     CKL();
   }
@@ -1163,6 +1185,8 @@ sdv2_status sdv2_profile_enable(sdv2_handle* h, int32_t enable) {
   h->prof_recs.clear();
   h->ev_next = 0;
   std::memset(&h->prof_acc, 0, sizeof(h->prof_acc));
+  h->prof_blk_ms.assign(h->nb, 0.0);
+  h->prof_blk_n.assign(h->nb, 0);
   return SDV2_OK;
 }
 
@@ -1172,9 +1196,17 @@ sdv2_status sdv2_profile_read(sdv2_handle* h, sdv2_profile* out) {
   // SDV2_PROF_DETAIL=1: per (class, work) breakdown on stderr (one line per GEMM shape)
   const bool detail = getenv("SDV2_PROF_DETAIL") != nullptr;
   std::map<std::pair<int, double>, std::pair<int, double>> det;
+  if (int(h->prof_blk_ms.size()) != h->nb) {
+    h->prof_blk_ms.assign(h->nb, 0.0);
+    h->prof_blk_n.assign(h->nb, 0);
+  }
   for (auto& r : h->prof_recs) {
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, r.a, r.b));
+    if (r.blk >= 0 && r.blk < h->nb) {
+      h->prof_blk_ms[r.blk] += ms;
+      h->prof_blk_n[r.blk] += 1;
+    }
     h->prof_acc.launches[r.cls] += 1;
     h->prof_acc.ms[r.cls] += ms;
     h->prof_acc.flops[r.cls] += r.flops;
@@ -1191,6 +1223,44 @@ sdv2_status sdv2_profile_read(sdv2_handle* h, sdv2_profile* out) {
   h->prof_recs.clear();
   h->ev_next = 0;
   *out = h->prof_acc;
+  return SDV2_OK;
+}
+
+sdv2_status sdv2_profile_block_ms(sdv2_handle* h, double* out, int32_t count) {
+  if (!h || !out || count < h->nb) return SDV2_E_INVALID;
+  sdv2_profile tmp;
+  sdv2_status s = sdv2_profile_read(h, &tmp);   // folds pending event pairs into the accumulators
+  if (s != SDV2_OK) return s;
+  for (int i = 0; i < h->nb; ++i) out[i] = h->prof_blk_n[i] ? h->prof_blk_ms[i] / double(h->prof_blk_n[i]) : 0.0;
+  return SDV2_OK;
+}
+
+sdv2_status sdv2_set_block_range(sdv2_handle* h, int32_t block_begin, int32_t block_end) {
+  if (!h) return SDV2_E_INVALID;
+  if (block_begin < h->r0 || block_end > h->r0 + h->nb || block_begin >= block_end) {
+    h->err = "block range outside the resident range";
+    return SDV2_E_INVALID;
+  }
+  if (block_begin == h->b0 && block_end == h->b1) return SDV2_OK;
+  CK(cudaStreamSynchronize(h->stream));
+  h->b0 = block_begin;
+  h->b1 = block_end;
+  h->a0 = block_begin - h->r0;
+  h->a1 = block_end - h->r0;
+  for (auto& g : h->graph_exec)   // the captured call bodies loop over the old range
+    if (g) {
+      cudaGraphExecDestroy(g);
+      g = nullptr;
+    }
+  return SDV2_OK;
+}
+
+sdv2_status sdv2_block_kv(sdv2_handle* h, int32_t block, int32_t which, void** ptr, size_t* bytes) {
+  if (!h || !ptr || !bytes || block < h->r0 || block >= h->r0 + h->nb || which < 0 || which > 1) return SDV2_E_INVALID;
+  const size_t per_block = size_t(h->NE) * h->S * h->L * h->d;
+  char* base = static_cast<char*>(which ? h->Vc : h->Kc);
+  *ptr = base + size_t(block - h->r0) * per_block * h->ta;
+  *bytes = per_block * h->ta;
   return SDV2_OK;
 }
 

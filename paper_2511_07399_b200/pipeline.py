@@ -233,6 +233,41 @@ def run_pipelined(stage, transport: StageTransport, chunks, out_cb, num_calls: i
     return outs
 
 
+def migrate_blocks(stage, rank: int, world: int, old_bounds, new_bounds, host_staging: bool = False, device=None):
+    """Online re-partition: move the KV lanes of every block whose owner changes
+    from its old stage to its new one (one grouped send/recv batch; the control-plane
+    metadata and the prompt K/V of resident blocks are already on every rank), then switch
+    this rank's active block range.  Called between drained runs (run_pipelined), so no
+    call of either rank is in flight."""
+    import torch
+    import torch.distributed as dist
+    owner = lambda bounds, b: next(s for s in range(world) if bounds[s] <= b < bounds[s + 1])
+    ws = stage.workspace
+    base = ws.data_ptr()
+    if device is not None:
+        torch.cuda.synchronize(device)
+    ops, post = [], []
+    for b in range(old_bounds[0], old_bounds[-1]):
+        o, n = owner(old_bounds, b), owner(new_bounds, b)
+        if o == n or rank not in (o, n):
+            continue
+        for which in (0, 1):
+            ptr, nbytes = stage.block_kv(b, which)
+            t = ws[ptr - base:ptr - base + nbytes]
+            wire = t.cpu() if host_staging else t
+            if rank == o:
+                ops.append(dist.P2POp(dist.isend, wire, n))
+            else:
+                ops.append(dist.P2POp(dist.irecv, wire, o))
+                if wire is not t:
+                    post.append((t, wire))
+    for w in (dist.batch_isend_irecv(ops) if ops else []):
+        w.wait()
+    for t, wire in post:
+        t.copy_(wire)
+    stage.set_block_range(new_bounds[rank], new_bounds[rank + 1])
+
+
 def balanced_ranges(num_blocks: int, world: int, block_ms: float, first_extra_ms: float, last_extra_ms: float):
     """Exact min-max partition of the blocks with the first / last stage
     extras (noise controller + embeddings / head) from measured times."""
@@ -288,7 +323,7 @@ def run_pipeline_bench(args, cfg):
     import torch.distributed as dist
     import synthgen as sg
     from . import build as B
-    from .sdv2 import SDV2_BF16, Stage
+    from .sdv2 import SDV2_BF16, Stage, rebalance
     sys_path_root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     import sys
     if sys_path_root not in sys.path:
@@ -320,10 +355,15 @@ def run_pipeline_bench(args, cfg):
     prompt = sg.gen_prompt(md, 0)
     fill = n * K
 
+    # resident blocks: the whole model for 1.3B (online re-partition anywhere), +-2 blocks
+    # around the provisional range for 14B (weights generated per rank)
+    margin = md.num_blocks if md.dim < 4096 else 2
+
     def make_stage(ranges):
         b0, b1 = ranges[rank]
-        W = _stage_weights(md, range(b0, b1), f"cuda:{dev_index}")
-        st = Stage(md, g, W, precision=SDV2_BF16, pipeline=(world, rank, b0, b1), device=dev_index)
+        r0, r1 = max(0, b0 - margin), min(md.num_blocks, b1 + margin)
+        W = _stage_weights(md, range(r0, r1), f"cuda:{dev_index}")
+        st = Stage(md, g, W, precision=SDV2_BF16, pipeline=(world, rank, b0, b1, r0, r1), device=dev_index)
         del W
         torch.cuda.empty_cache()
         st.reset_stream(sd, prompt)
@@ -342,26 +382,39 @@ def run_pipeline_bench(args, cfg):
     stage.profile_enable(True)
     base = stage.calls
     run_pipelined(stage, tr, lambda c: ptr_in(base + c), lambda c: out_dev.data_ptr(), ncal)
+    blk_res = stage.profile_block_ms()                 # per resident block, 0 where not run here
     prof = stage.profile_read()
     stage.profile_enable(False)
-    nbl = ranges0[rank][1] - ranges0[rank][0]
-    blk = prof["blocks"]["ms"] / max(1, prof["blocks"]["launches"])
     ext = prof["stage_extras"]["ms"] / ncal
-    rows = _gather(dist, [blk, ext, nbl], backend)
-    block_ms = sum(r[0] for r in rows) / world
-    first_extra, last_extra = rows[0][1], rows[-1][1]
-    ranges, stage_max = balanced_ranges(md.num_blocks, world, block_ms, first_extra, last_extra)
-    balance = {"block_ms": block_ms, "first_extra_ms": first_extra, "last_extra_ms": last_extra,
-               "provisional": ranges0, "predicted_stage_ms": stage_max}
-    if ranges != ranges0:
-        stage.close()
-        del stage, tr
-        torch.cuda.empty_cache()
-        stage, tr = make_stage(ranges)
-    else:
-        stage.reset_stream(sd, prompt)
-        tr = StageTransport(rank, world, stage_io_tensors(stage, stage.workspace), host_staging=host_staging,
-                            device=dev_index)
+    r0 = stage.resident[0]
+    mine = [0.0] * md.num_blocks
+    for i, v in enumerate(blk_res):
+        mine[r0 + i] = v
+    rows = _gather(dist, mine + [ext], backend)
+    measured = [sum(r[b] for r in rows) for b in range(md.num_blocks)]   # each block timed on its owner
+    first_extra, last_extra = rows[0][-1], rows[-1][-1]
+    bounds0 = [ranges0[0][0]] + [r[1] for r in ranges0]
+    ema = [0.0] * md.num_blocks
+    bounds, changed, pred_cur, pred_new = rebalance(measured, world, bounds0, ema, first_extra, last_extra,
+                                                    alpha=1.0, hysteresis=0.02)
+    ranges = [(bounds[s], bounds[s + 1]) for s in range(world)]
+    balance = {"block_ms": measured, "first_extra_ms": first_extra, "last_extra_ms": last_extra,
+               "provisional": ranges0, "predicted_stage_ms": pred_new, "predicted_stage_ms_provisional": pred_cur,
+               "moved_online": False}
+    if changed:
+        fits = all(stage_res[0] <= b0 and b1 <= stage_res[1] for stage_res, (b0, b1) in
+                   zip(_gather(dist, list(stage.resident), backend), ranges))
+        if fits:      # online: move the KV lanes of the moved blocks, no re-creation (N3)
+            migrate_blocks(stage, rank, world, bounds0, bounds, host_staging=host_staging, device=dev_index)
+            balance["moved_online"] = True
+        else:
+            stage.close()
+            del stage, tr
+            torch.cuda.empty_cache()
+            stage, tr = make_stage(ranges)
+    stage.reset_stream(sd, prompt)
+    tr = StageTransport(rank, world, stage_io_tensors(stage, stage.workspace), host_staging=host_staging,
+                        device=dev_index)
     stream = stage.stream
     dist.barrier()
 

@@ -40,7 +40,7 @@ class GeometryC(ctypes.Structure):
 
 class PipelineC(ctypes.Structure):
     _fields_ = [("world", ctypes.c_int32), ("rank", ctypes.c_int32), ("block_begin", ctypes.c_int32),
-                ("block_end", ctypes.c_int32)]
+                ("block_end", ctypes.c_int32), ("resident_begin", ctypes.c_int32), ("resident_end", ctypes.c_int32)]
 
 
 class WeightsC(ctypes.Structure):
@@ -112,6 +112,12 @@ def _declare(lib):
     lib.sdv2_set_graphs.argtypes = [P, ctypes.c_int32]
     lib.sdv2_set_graphs.restype = ctypes.c_int
     lib.sdv2_profile_read.argtypes = [P, ctypes.POINTER(ProfileC)]
+    lib.sdv2_set_block_range.argtypes = [P, ctypes.c_int32, ctypes.c_int32]
+    lib.sdv2_set_block_range.restype = ctypes.c_int
+    lib.sdv2_block_kv.argtypes = [P, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(P), ctypes.POINTER(ctypes.c_size_t)]
+    lib.sdv2_block_kv.restype = ctypes.c_int
+    lib.sdv2_profile_block_ms.argtypes = [P, ctypes.POINTER(ctypes.c_double), ctypes.c_int32]
+    lib.sdv2_profile_block_ms.restype = ctypes.c_int
     for f in ("sdv2_profile_enable", "sdv2_profile_read", "sdv2_create", "sdv2_reset_stream", "sdv2_set_prompt", "sdv2_denoise_chunk", "sdv2_stage_io_buffers",
               "sdv2_get_tick_info", "sdv2_destroy", "sdv2_get_cache_state", "sdv2_set_block_tap", "sdv2_kv_lane",
               "sdv2_partition"):
@@ -260,10 +266,15 @@ class Stage:
         if pipeline is None:
             self._pp = None
             b0, b1 = 0, md.num_blocks
+            r0, r1 = b0, b1
         else:
-            self._pp = PipelineC(*pipeline)
-            b0, b1 = pipeline[2], pipeline[3]
+            # (world, rank, block_begin, block_end[, resident_begin, resident_end])
+            pl = tuple(pipeline) + ((0, 0) if len(pipeline) == 4 else ())
+            self._pp = PipelineC(*pl)
+            b0, b1 = pl[2], pl[3]
+            r0, r1 = (pl[4], pl[5]) if pl[4:6] != (0, 0) else (b0, b1)
         self.block_range = (b0, b1)
+        self.resident = (r0, r1)
         ppp = ctypes.byref(self._pp) if self._pp is not None else None
         nbytes = self.L.sdv2_workspace_bytes(ctypes.byref(self._mdc), ctypes.byref(self._gc), ppp, precision)
         if nbytes == 0:
@@ -272,7 +283,7 @@ class Stage:
         self.workspace = torch.empty(nbytes + 1024, dtype=torch.uint8, device=f"cuda:{device}")
         # a dedicated (capturable) stream: per-call device work is replayed from CUDA graphs
         self.stream = stream if stream is not None else torch.cuda.Stream(device)
-        names = list(GLOBAL_ORDER) + [f"blocks.{b}.{t}" for b in range(b0, b1) for t in BLOCK_ORDER]
+        names = list(GLOBAL_ORDER) + [f"blocks.{b}.{t}" for b in range(r0, r1) for t in BLOCK_ORDER]
         keep = []
         ptrs = (ctypes.c_void_p * len(names))()
         for i, nme in enumerate(names):
@@ -363,6 +374,24 @@ class Stage:
         _check(self.L.sdv2_set_block_tap(self.h, ctypes.c_void_p(tensor.data_ptr()) if tensor is not None else None),
                self.h)
 
+    def set_block_range(self, b0, b1):
+        _check(self.L.sdv2_set_block_range(self.h, b0, b1), self.h)
+        self.block_range = (b0, b1)
+
+    def block_kv(self, block, which):
+        """(device pointer, bytes) of resident block `block`'s K (0) / V (1) lanes."""
+        p = ctypes.c_void_p()
+        n = ctypes.c_size_t()
+        _check(self.L.sdv2_block_kv(self.h, block, which, ctypes.byref(p), ctypes.byref(n)), self.h)
+        return p.value, n.value
+
+    def profile_block_ms(self):
+        """Mean ms per call of every resident block's span since profile_enable(True)."""
+        nres = self.resident[1] - self.resident[0]
+        out = (ctypes.c_double * nres)()
+        _check(self.L.sdv2_profile_block_ms(self.h, out, nres), self.h)
+        return list(out)
+
     def kv_lane(self, local_block, lane, which):
         p = ctypes.c_void_p()
         n = ctypes.c_size_t()
@@ -450,3 +479,29 @@ def slo_fit(table):
     a, b = ctypes.c_double(), ctypes.c_double()
     _check(_host_lib().sdv2_slo_fit(arr, n, ctypes.byref(a), ctypes.byref(b)))
     return a.value, b.value
+
+
+# ------------------------------------------------------- online block scheduler (N3)
+def rebalance(measured_block_ms, stages, cur_bounds, ema, extra_first=0.0, extra_last=0.0, alpha=0.5,
+              hysteresis=0.05):
+    """Library policy sdv2_rebalance.  `ema` (list, updated in place) carries the smoothed
+    per-block times between calls.  Returns (new_bounds, changed, pred_cur, pred_new)."""
+    L = lib() if os.path.exists(_LIB_PATH) else ctl_lib()
+    if not getattr(L, "_rb_declared", False):
+        D = ctypes.POINTER(ctypes.c_double)
+        I = ctypes.POINTER(ctypes.c_int32)
+        L.sdv2_rebalance.argtypes = [D, ctypes.c_int32, ctypes.c_int32, ctypes.c_double, ctypes.c_double,
+                                     ctypes.c_double, ctypes.c_double, D, I, I, I, D, D]
+        L.sdv2_rebalance.restype = ctypes.c_int
+        L._rb_declared = True
+    nb = len(measured_block_ms)
+    m = (ctypes.c_double * nb)(*measured_block_ms)
+    e = (ctypes.c_double * nb)(*ema)
+    cb = (ctypes.c_int32 * (stages + 1))(*cur_bounds)
+    nbd = (ctypes.c_int32 * (stages + 1))()
+    ch = ctypes.c_int32()
+    pc, pn = ctypes.c_double(), ctypes.c_double()
+    _check(L.sdv2_rebalance(m, nb, stages, extra_first, extra_last, alpha, hysteresis, e, cb, nbd, ctypes.byref(ch),
+                            ctypes.byref(pc), ctypes.byref(pn)))
+    ema[:] = list(e)
+    return list(nbd), bool(ch.value), pc.value, pn.value
