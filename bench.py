@@ -85,6 +85,26 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
+def host_info():
+    """CPU model and BLAS threads of the oracle leg (SURVEY §8(d) oracle timing)."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    blas = None
+    try:
+        from threadpoolctl import threadpool_info
+        blas = [{"api": i.get("internal_api"), "threads": i.get("num_threads")} for i in threadpool_info()
+                if i.get("user_api") == "blas"]
+    except Exception:
+        pass
+    return {"cpu_model": model, "blas": blas}
+
+
 def chunk_frames_px(cfg):
     return 4 * cfg.geom.chunk_frames
 
@@ -221,6 +241,14 @@ def run_ours(args, cfg):
     B.build()
     torch.cuda.set_device(local)
     md, g, sd = cfg.model, cfg.geom, cfg.stream
+    if args.window or args.denoise_steps:
+        import dataclasses
+        if args.window:
+            g = dataclasses.replace(g, window_chunks=args.window)
+        if args.denoise_steps:   # E10 "no Stream Batch": n = 1 ticks, one per denoising step
+            g = dataclasses.replace(g, steps=args.denoise_steps)
+            sd = dataclasses.replace(sd, timesteps=sg.SCHEDULES[args.denoise_steps])
+        cfg = dataclasses.replace(cfg, geom=g, stream=sd)
     Bs = args.streams
     if Bs > 1:     # SLO batch: Bs independent streams per call
         import dataclasses
@@ -230,7 +258,7 @@ def run_ours(args, cfg):
     big = md.dim >= 4096
     W = gen_weights_device(md) if big else gen_weights_parallel(md)
     t_gen = time.time() - t0
-    stage = Stage(md, g, W, precision=SDV2_BF16, device=local)
+    stage = Stage(md, g, W, precision=SDV2_BF16, device=local, l2_persist=args.l2_persist)
     if big:   # free the fp32 device copies; the oracle baseline regenerates 2 blocks on host
         del W
         torch.cuda.empty_cache()
@@ -312,6 +340,36 @@ def run_ours(args, cfg):
     e2e_ms = t_a.elapsed_time(t_b)
     e2e_value = chunk_frames_px(cfg) * Bs * outs_e2e / (e2e_ms / 1e3)
     bytes_chunk = host_chunks[0].nbytes
+    # ---- per-chunk latency: host CLOCK_MONOTONIC from the call that submits
+    # chunk X to the host seeing output X complete, over >= 1024 chunks; the host keeps at
+    # most one call queued ahead of the GPU (closed loop at the saturating input rate)
+    lat_chunks = args.latency_chunks
+    host_lat = None
+    if lat_chunks > 0:
+        submit, done = {}, {}
+        prev = None
+        for i in range(lat_chunks + n - 1):
+            X = c + i
+            submit[X] = time.monotonic()
+            oc = stage.denoise_chunk(dev_chunks[X % R].data_ptr(), out_dev.data_ptr())
+            e = torch.cuda.Event()
+            e.record(stream)
+            if prev is not None:
+                prev[1].synchronize()
+                if prev[0] >= 0:
+                    done[prev[0]] = time.monotonic()
+            prev = (oc, e)
+        prev[1].synchronize()
+        if prev[0] >= 0:
+            done[prev[0]] = time.monotonic()
+        c += lat_chunks + n - 1
+        # out index oc is a chunk index counted from the stream start: map to submit keys
+        lats = sorted((done[X] - submit[X]) * 1e3 for X in done if X in submit)
+        if lats:
+            host_lat = {"p50": float(np.percentile(lats, 50)), "p99": float(np.percentile(lats, 99)),
+                        "max": float(lats[-1]), "chunks": len(lats),
+                        "definition": "host CLOCK_MONOTONIC, submit of chunk X -> completion of output X; "
+                                      "host at most one call ahead of the GPU"}
     # ---- per-kernel-class device time (events around each launch), same workload
     prof_steps = min(args.steps, 50)
     stage.profile_enable(True)
@@ -345,6 +403,7 @@ def run_ours(args, cfg):
         tsec = oracle_entry_seconds(cfg, {k: v for k, v in W.items()}, list(range(nbl)))
         per_chunk = tsec * (md.num_blocks / nbl) * n
         cpu = {"value": chunk_frames_px(cfg) / per_chunk, "unit": "frames/s", "cores": cores, "kind": "oracle",
+               "host": host_info(),
                "sample": (f"one steady-state entry (full m+W window) of {cfg.name} through {nbl} of "
                           f"{md.num_blocks} blocks, NumPy fp32 on {cores} cores; x{n} steps per clean chunk"
                           + (" (block-extrapolated)" if nbl < md.num_blocks else ""))}
@@ -363,8 +422,10 @@ def run_ours(args, cfg):
         "ttff_ms": ttff_ms,
         "ttff_with_buffering_ms": {"16fps": ttff_ms + 1e3 * chunk_frames_px(cfg) / 16.0,
                                    "30fps": ttff_ms + 1e3 * chunk_frames_px(cfg) / 30.0},
-        "latency_ms": {"p50": float(np.percentile(lat, 50)), "p99": float(np.percentile(lat, 99)),
-                       "max": float(np.max(lat))} if lat else None,
+        "latency_ms": host_lat,
+        "latency_device_ms": {"p50": float(np.percentile(lat, 50)), "p99": float(np.percentile(lat, 99)),
+                              "max": float(np.max(lat)), "definition": "sum of n device-timed stage-ticks"}
+        if lat else None,
         "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": bytes_chunk,
                 "d2h_bytes_per_step": bytes_chunk},
         "gpu_launches": launches,
@@ -387,6 +448,13 @@ def main():
     ap.add_argument("--pp-backend", default="nccl", choices=["nccl", "gloo"],
                     help="stage transport for --gpus > 1 (gloo: host staging, several ranks on one GPU)")
     ap.add_argument("--lib", default=None, help="alternative libsdv2.so build (A/B timing)")
+    ap.add_argument("--no-l2-persist", dest="l2_persist", action="store_false",
+                    help="no persisting-L2 window on the residual stream (A/B)")
+    ap.add_argument("--window", type=int, default=0, help="override W (rolling-window chunks)")
+    ap.add_argument("--denoise-steps", type=int, default=0, choices=[0, 1, 2, 4],
+                    help="override n (in-flight denoising steps = Stream Batch size)")
+    ap.add_argument("--latency-chunks", type=int, default=1024,
+                    help="chunks of the host-clock per-chunk latency phase (0: skip)")
     ap.add_argument("--streams", type=int, default=1,
                     help="independent streams batched per call (SLO batch B; value = all streams' frames/s)")
     args = ap.parse_args()

@@ -174,11 +174,16 @@ typedef struct sdv2_handle sdv2_handle;
  *                    shape at create (CUDA-graph replay on the real buffers) and keep
  *                    the fastest; 0 = the tile-balance model's pick, no timing.
  *   pdl          [1] programmatic dependent launch between the call's kernels.
- *   graphs       [1] replay the per-call device work from CUDA graphs. */
+ *   graphs       [1] replay the per-call device work from CUDA graphs.
+ *   l2_persist   [1] mark the tick packet (fp32 residual stream x, embeddings) as
+ *                    persisting in L2 (stream access-policy window; sets the process's
+ *                    persisting-L2 limit) so the residual epilogues and norms re-read it
+ *                    from L2 instead of HBM (+0.5-0.8 % fps measured at 1.3B 480p). */
 typedef struct {
   int32_t tune_gemms;
   int32_t pdl;
   int32_t graphs;
+  int32_t l2_persist;
 } sdv2_exec_options;
 
 /* Bytes of device workspace a handle needs (0 on invalid descriptors). */

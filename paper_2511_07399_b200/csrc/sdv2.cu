@@ -153,6 +153,7 @@ struct sdv2_handle {
   bool graphs = true;
   bool pdl = true;        // programmatic dependent launch (sdv2_exec_options.pdl): +2 % fps measured
   bool tune = true;       // create-time GEMM tile tuning (sdv2_exec_options.tune_gemms)
+  bool l2_persist = true;    // sdv2_exec_options.l2_persist
   int64_t last_switch_call[kMaxEntries];   // call index of stream b's last sdv2_set_prompt (-1: none)
   cudaGraphExec_t graph_exec[2 * (kMaxEntries + 1)] = {};
   int64_t graph_launches[2 * (kMaxEntries + 1)] = {};
@@ -869,6 +870,7 @@ sdv2_status sdv2_create(const sdv2_model_desc* md, const sdv2_geometry* g, const
     h->tune = opts->tune_gemms != 0;
     h->pdl = opts->pdl != 0;
     h->graphs = opts->graphs != 0;
+    h->l2_persist = opts->l2_persist != 0;
   }
   h->ws_bytes = workspace_bytes;
   if (cudaSetDevice(device) != cudaSuccess) {
@@ -939,6 +941,27 @@ sdv2_status sdv2_create(const sdv2_model_desc* md, const sdv2_geometry* g, const
         !attn_plan_init(h->aplan, h->gplan.encode, std::min(h->gplan.num_sms, kMaxSMs), h->attn_flags)) {
       h->err = "attention plan initialisation failed";
       return fail(SDV2_E_CUDA);
+    }
+  }
+  if (h->l2_persist) {
+    // the packet (x [M, d] fp32 first) as a persisting L2 window on the handle's stream;
+    // captured call graphs inherit the window as a kernel-node attribute
+    int maxp = 0, maxwin = 0;
+    cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, device);
+    cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, device);
+    const size_t win = std::min(h->st.bytes, size_t(maxwin));
+    if (maxp > 0 && win > 0) {
+      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min(size_t(maxp), win));
+      cudaStreamAttrValue v{};
+      v.accessPolicyWindow.base_ptr = h->packet_base;
+      v.accessPolicyWindow.num_bytes = win;
+      v.accessPolicyWindow.hitRatio = std::min(1.0f, float(maxp) / float(win));
+      v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      if (cudaStreamSetAttribute(h->stream, cudaStreamAttributeAccessPolicyWindow, &v) != cudaSuccess) {
+        h->err = "cannot set the L2 access-policy window";
+        return fail(SDV2_E_CUDA);
+      }
     }
   }
   if (h->prec == SDV2_BF16 && h->tune) {

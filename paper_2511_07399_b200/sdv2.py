@@ -55,7 +55,8 @@ class StreamDescC(ctypes.Structure):
 
 
 class ExecOptionsC(ctypes.Structure):
-    _fields_ = [("tune_gemms", ctypes.c_int32), ("pdl", ctypes.c_int32), ("graphs", ctypes.c_int32)]
+    _fields_ = [("tune_gemms", ctypes.c_int32), ("pdl", ctypes.c_int32), ("graphs", ctypes.c_int32),
+                ("l2_persist", ctypes.c_int32)]
 
 
 class StageIOC(ctypes.Structure):
@@ -255,7 +256,7 @@ class Stage:
     """One pipeline stage (or the whole model when pipeline=None) of the hot path."""
 
     def __init__(self, md, geom, weights: Dict[str, np.ndarray], precision=SDV2_BF16, pipeline=None,
-                 device=0, stream=None, tune_gemms=True, pdl=True, graphs=True):
+                 device=0, stream=None, tune_gemms=True, pdl=True, graphs=True, l2_persist=True):
         import torch
         self.torch = torch
         self.md, self.geom = md, geom
@@ -297,7 +298,7 @@ class Stage:
             keep.append(a)
         w = WeightsC(ptrs, len(names))
         h = ctypes.c_void_p()
-        self._opts = ExecOptionsC(int(tune_gemms), int(pdl), int(graphs))
+        self._opts = ExecOptionsC(int(tune_gemms), int(pdl), int(graphs), int(l2_persist))
         st = self.L.sdv2_create(ctypes.byref(self._mdc), ctypes.byref(self._gc), ppp, precision, ctypes.byref(w),
                                 ctypes.c_void_p(self.workspace.data_ptr()), nbytes + 1024, device,
                                 ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(self._opts), ctypes.byref(h))
