@@ -215,6 +215,18 @@ sdv2_status sdv2_reset_stream(sdv2_handle* h, const sdv2_stream_desc* sd, const 
  * prompt_host: host [text_len, text_dim] fp32 for stream `stream`. */
 sdv2_status sdv2_set_prompt(sdv2_handle* h, int32_t stream, const float* prompt_host);
 
+/* Chunk embedding h_t of the sink refresh ("given a new chunk embedding h_t").
+ * The default reading (Q8) is the mean-pooled prompt embedding, set by reset_stream /
+ * set_prompt.  The visual reading (N4): before each call the caller passes stream b's
+ * embedding of the chunk it is about to admit (e.g. sdv2_chunk_embedding of the latent);
+ * every rank must receive the same values (the control plane is replicated).  Any
+ * dimension >= 1; the sinks compare against embeddings of the same dimension.
+ * SDV2_E_INVALID: zero norm, bad stream. */
+sdv2_status sdv2_set_chunk_embedding(sdv2_handle* h, int32_t stream, const double* emb, int32_t dim);
+/* Host helper: out[c] = mean over T' x h x w of channel c of a host chunk [C, T', h, w]
+ * fp32, accumulated in fp64 in index order (the visual chunk embedding of N4). */
+sdv2_status sdv2_chunk_embedding(const float* chunk_host, int32_t C, int32_t T, int32_t H, int32_t W, double* out);
+
 /* One stage-tick.  Rank 0: chunk_latent [streams][C, T', h, w] fp32 (host or device
  * pointer): chunk X = call index of every stream is admitted.  Last rank: if this call
  * emits clean chunks, their x0 are written to out_latent (host or device,

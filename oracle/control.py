@@ -66,6 +66,14 @@ def rope_position(t: int, T_reset: int) -> int:
     return t
 
 
+# ------------------------------------- visual chunk embedding (N4 / Q8-visual)
+def visual_embedding(chunk) -> np.ndarray:
+    """h_X[c] = mean over (T', h, w) of latent channel c, fp64 (the visual reading of the
+    paper's "chunk embedding h_t"; the default reading Q8 is the mean-pooled prompt)."""
+    a = np.asarray(chunk, dtype=np.float64)
+    return a.reshape(a.shape[0], -1).mean(axis=1)
+
+
 # ----------------------------------------------- sink refresh (P:190, R4/Q9)
 def cosine(a, b) -> float:
     a = np.asarray(a, dtype=np.float64)

@@ -80,6 +80,9 @@ class Control {
   // Prompt of stream b in effect from its next admitted chunk: h = mean-pooled prompt
   // (fp64, reading Q8).
   void set_prompt_mean(int b, const std::vector<double>& h, int32_t pver);
+  // Visual reading of the chunk embedding h_t (N4): the embedding stream b's next
+  // admitted chunk is compared against its sinks with (the prompt version is unchanged).
+  void set_chunk_embedding(int b, const std::vector<double>& h) { st_[b].h = h; }
   // One call (stage-tick) on this rank: admits chunk X = call index of every stream (R2),
   // applies the chunk records of every active entry to its lane and fills the device
   // descriptor.

@@ -79,4 +79,25 @@ int32_t sdv2ctl_lane_state(void* c, int32_t lane, sdv2_cache_state* st) {
 
 int32_t sdv2ctl_max_frames(void) { return kMaxFrames; }
 
+int32_t sdv2ctl_set_chunk_embedding(void* c, int32_t stream, const double* h, int32_t dim) {
+  auto* ctl = static_cast<Control*>(c);
+  if (stream < 0 || stream >= ctl->params().B || !h || dim < 1) return -1;
+  ctl->set_chunk_embedding(stream, std::vector<double>(h, h + dim));
+  return 0;
+}
+
+// Visual chunk embedding (N4, reading Q8-visual in DESIGN.md): h_c = mean over the chunk's
+// T' frames and h x w pixels of latent channel c, accumulated in fp64 in index order.
+sdv2_status sdv2_chunk_embedding(const float* chunk_host, int32_t C, int32_t T, int32_t H, int32_t W, double* out) {
+  if (!chunk_host || !out || C < 1 || T < 1 || H < 1 || W < 1) return SDV2_E_INVALID;
+  const size_t per = size_t(T) * H * W;
+  for (int c = 0; c < C; ++c) {
+    double acc = 0.0;
+    const float* p = chunk_host + size_t(c) * per;
+    for (size_t i = 0; i < per; ++i) acc += double(p[i]);
+    out[c] = acc / double(per);
+  }
+  return SDV2_OK;
+}
+
 }  // extern "C"

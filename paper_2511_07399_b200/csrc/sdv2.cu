@@ -22,6 +22,7 @@
 #include "ctl.h"
 #include "gemm_tc.cuh"
 #include "attn_tc.cuh"
+#include "xattn_tc.cuh"
 #include "elem.cuh"
 #include "kernels.cuh"
 
@@ -446,6 +447,23 @@ sdv2_status attention(sdv2_handle* h, const AttnArgs& aa, int Mrows_entries, dou
     if (h->hd == 64) attn_simt_kernel<float, 64><<<grid, 128, 0, h->stream>>>(aa, h->td_dev);
     else attn_simt_kernel<float, 128><<<grid, 128, 0, h->stream>>>(aa, h->td_dev);
   } else {
+    if (aa.cross && h->Lt <= kXattnMaxJ * kAttnBKV) {
+      // prompt keys fit one TMEM row: exact single-pass cross-attention (xattn_tc.cuh)
+      ++h->launches;
+      XattnArgs xa{};
+      xa.L = h->L;
+      xa.H = h->H;
+      xa.QT = (h->L + kAttnBQ - 1) / kAttnBQ;
+      xa.n_entries = Mrows_entries;
+      xa.Lk = h->Lt;
+      xa.kv_row0 = bl * 2 * h->B * h->Lt;      // prompt K/V [nb][2B slots][Lt][d]
+      xa.kv_slot_rows = h->Lt;
+      xa.scale_log2 = 1.4426950408889634f / sqrtf(float(h->hd));
+      xa.o = aa.o;
+      xa.ldo = aa.ldo;
+      return tc_cross_attention(h->stream, h->aplan, aa.q, h->Mmax, h->Kx, h->Vx, 2LL * h->B * h->nb * h->Lt, h->d,
+                                h->hd, xa, h->td_dev, &h->err, h->pdl) ? SDV2_OK : SDV2_E_CUDA;
+    }
     if (tc_attn_enabled()) {
       ++h->launches;
       AttnTcArgs ta{};
@@ -938,7 +956,8 @@ sdv2_status sdv2_create(const sdv2_model_desc* md, const sdv2_geometry* g, const
   if (h->prec == SDV2_BF16) {
     if (!tc_gemm_plan(h->gplan, &h->err)) return fail(SDV2_E_CUDA);
     if (cudaMemsetAsync(h->attn_flags, 0, kMaxSMs * sizeof(int), h->stream) != cudaSuccess ||
-        !attn_plan_init(h->aplan, h->gplan.encode, std::min(h->gplan.num_sms, kMaxSMs), h->attn_flags)) {
+        !attn_plan_init(h->aplan, h->gplan.encode, std::min(h->gplan.num_sms, kMaxSMs), h->attn_flags) ||
+        !xattn_plan_init()) {
       h->err = "attention plan initialisation failed";
       return fail(SDV2_E_CUDA);
     }
@@ -1128,6 +1147,18 @@ sdv2_status sdv2_set_prompt(sdv2_handle* h, int32_t stream, const float* prompt_
     h->last_switch_call[b] = now;
   }
   return s;
+}
+
+sdv2_status sdv2_set_chunk_embedding(sdv2_handle* h, int32_t stream, const double* emb, int32_t dim) {
+  if (!h || !emb || dim < 1 || stream < 0 || stream >= h->B) return SDV2_E_INVALID;
+  double nrm = 0.0;
+  for (int i = 0; i < dim; ++i) nrm += emb[i] * emb[i];
+  if (!(nrm > 0.0)) {
+    h->err = "zero-norm chunk embedding";
+    return SDV2_E_INVALID;
+  }
+  h->ctl.set_chunk_embedding(stream, std::vector<double>(emb, emb + dim));
+  return SDV2_OK;
 }
 
 sdv2_status sdv2_denoise_chunk(sdv2_handle* h, const float* chunk_latent, float* out_latent, int64_t* out_chunk_index) {
@@ -1430,7 +1461,7 @@ extern "C" sdv2_status sdv2_debug_attention(const void* q, const void* K, const 
     if (!tc_gemm_plan(gp, &err)) return SDV2_E_CUDA;
     if (cudaMalloc(&flags, kMaxSMs * sizeof(int)) != cudaSuccess ||
         cudaMemset(flags, 0, kMaxSMs * sizeof(int)) != cudaSuccess ||
-        !attn_plan_init(ap, gp.encode, std::min(gp.num_sms, kMaxSMs), flags))
+        !attn_plan_init(ap, gp.encode, std::min(gp.num_sms, kMaxSMs), flags) || !xattn_plan_init())
       return SDV2_E_CUDA;
     ready = true;
   }
@@ -1463,6 +1494,24 @@ extern "C" sdv2_status sdv2_debug_attention(const void* q, const void* K, const 
   ta.kv_row0 = 0;
   ta.kv_lane_rows = 0;
   const long long tiles = (long long)H * ta.QT * ((Lk + kAttnBKV - 1) / kAttnBKV);
+  if (Lk <= kXattnMaxJ * kAttnBKV) {   // the product path's cross-attention kernel for short key sets
+    XattnArgs xa{};
+    xa.L = Lq;
+    xa.H = H;
+    xa.QT = (Lq + kAttnBQ - 1) / kAttnBQ;
+    xa.n_entries = 1;
+    xa.Lk = Lk;
+    xa.kv_row0 = 0;
+    xa.kv_slot_rows = 0;
+    xa.scale_log2 = 1.4426950408889634f / sqrtf(float(hd));
+    xa.o = o;
+    xa.ldo = H * hd;
+    if (!tc_cross_attention(s, ap, q, Lq, K, V, Lk, H * hd, hd, xa, static_cast<const TickDesc*>(scratch), &err)) {
+      fprintf(stderr, "sdv2_debug_attention: %s\n", err.c_str());
+      return SDV2_E_CUDA;
+    }
+    return SDV2_OK;
+  }
   ta.per_unit = getenv("SDV2_ATTN_PER_UNIT") ? atoi(getenv("SDV2_ATTN_PER_UNIT")) : 0;
   ta.rr = attn_rr();
   ta.dbg = getenv("SDV2_ATTN_DBG") ? atoi(getenv("SDV2_ATTN_DBG")) : 0;

@@ -331,6 +331,12 @@ class Stage:
         p = np.ascontiguousarray(prompt, dtype=np.float32)
         _check(self.L.sdv2_set_prompt(self.h, stream, ctypes.c_void_p(p.ctypes.data)), self.h)
 
+    def set_chunk_embedding(self, emb, stream: int = 0):
+        """Visual chunk embedding h_t for the next admitted chunk of `stream` (N4)."""
+        a = np.ascontiguousarray(emb, dtype=np.float64)
+        self.L.sdv2_set_chunk_embedding.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int32]
+        _check(self.L.sdv2_set_chunk_embedding(self.h, stream, ctypes.c_void_p(a.ctypes.data), a.size), self.h)
+
     def denoise_chunk(self, chunk_ptr: Optional[int], out_ptr: Optional[int]) -> int:
         """chunk_ptr / out_ptr: raw host or device addresses (or None).  Returns the chunk
         index emitted into out_ptr, or -1."""
@@ -506,3 +512,15 @@ def rebalance(measured_block_ms, stages, cur_bounds, ema, extra_first=0.0, extra
                             ctypes.byref(pc), ctypes.byref(pn)))
     ema[:] = list(e)
     return list(nbd), bool(ch.value), pc.value, pn.value
+
+
+def chunk_embedding(chunk: np.ndarray) -> np.ndarray:
+    """Library host helper sdv2_chunk_embedding: per-channel mean of a [C, T', h, w] chunk."""
+    L = lib() if os.path.exists(_LIB_PATH) else ctl_lib()
+    a = np.ascontiguousarray(chunk, dtype=np.float32)
+    C, T, H, W = a.shape
+    out = np.zeros(C, dtype=np.float64)
+    L.sdv2_chunk_embedding.argtypes = [ctypes.c_void_p] + [ctypes.c_int32] * 4 + [ctypes.c_void_p]
+    L.sdv2_chunk_embedding.restype = ctypes.c_int
+    _check(L.sdv2_chunk_embedding(ctypes.c_void_p(a.ctypes.data), C, T, H, W, ctypes.c_void_p(out.ctypes.data)))
+    return out

@@ -262,3 +262,47 @@ def test_multi_stream_13b_bf16():
     cfg = dataclasses.replace(cfg, stream=dataclasses.replace(cfg.stream, rope_reset_frames=4))
     worst = _check_streams(cfg, 4, 3, [(), (2,), (), (1,)], SDV2_BF16, dtype=np.float32)
     print(f"1.3B B=4: worst block rel-L2 {worst:.3e}")
+
+
+# ------------------------------------------- visual chunk embedding (N4)
+@pytest.mark.gpu
+@pytest.mark.parametrize("prec", [SDV2_FP32, SDV2_BF16])
+def test_visual_sink_embedding(prec):
+    """Sink refresh driven by the visual chunk embedding (per-channel mean of the latent,
+    P:190 / N4) instead of the prompt mean: a scene cut at chunk 5 refreshes the sink; the
+    GPU stream equals the oracle stream fed the same embeddings."""
+    import torch
+    from oracle import control as OC
+    from paper_2511_07399_b200.sdv2 import chunk_embedding
+    cfg = dataclasses.replace(sg.CONFIGS["tiny"], num_chunks=9, prompt_switch=())
+    md, g = cfg.model, cfg.geom
+    W = sg.gen_weights(md, seed=0)
+    a = sg.LatentStream(4, 8, 8, seed=1, speeds=(0.0, 0.25))
+    b = sg.LatentStream(4, 8, 8, seed=9, speeds=(0.0, 0.25))
+    chunks = [(a if X < 5 else b).chunk(X, 1) + (0.0 if X < 5 else 0.7) for X in range(cfg.num_chunks + g.steps - 1)]
+    prompt = sg.gen_prompt(md, 0)
+    o = StreamOracle(md, g, cfg.stream, W, dtype=np.float64)
+    o.set_prompt(prompt)
+    recs = []
+    for X in range(cfg.num_chunks):
+        o.h = OC.visual_embedding(chunks[X])
+        recs.append(o.step_chunk(X, chunks[X]))
+    assert any(any(r["act"]["refresh"]) for r in recs[5:])
+    stage = Stage(md, g, W, precision=prec)
+    stage.reset_stream(cfg.stream, prompt)
+    out = torch.zeros(chunks[0].shape, dtype=torch.float32, device="cuda")
+    got = {}
+    for c, v in enumerate(chunks):
+        stage.set_chunk_embedding(chunk_embedding(v))
+        oc = stage.denoise_chunk(torch.from_numpy(v).cuda().data_ptr(), out.data_ptr())
+        torch.cuda.synchronize()
+        if oc >= 0:
+            got[oc] = out.cpu().numpy().copy()
+        X = stage.tick_info()["chunk"][0]
+        if 0 <= X < cfg.num_chunks:
+            st = stage.cache_state(0, 0)
+            slots = {s: (st.tag[s], st.pos[s]) for s in range(st.num_slots) if st.tag[s] >= 0}
+            assert slots == {s: (t, p[0]) for s, (t, p) in recs[X]["lane_state"][(0, 0)].items()}, X
+    stage.close()
+    for X in range(cfg.num_chunks):
+        assert rel_l2(got[X], recs[X]["out"]) <= TOL[prec], X
