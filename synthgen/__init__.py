@@ -284,3 +284,75 @@ class LatentStream:
     def chunks(self, n: int, T: int) -> Iterator[np.ndarray]:
         for X in range(n):
             yield self.chunk(X, T)
+
+
+# ---------------------------------------------------------------------------
+# Stream-VAE stand-in: Wan-VAE-shaped causal 3D-conv encoder /
+# decoder, shapes and init law only (no arithmetic).  Channels per stage (Wan2.1 VAE:
+# base 96, multipliers 1, 2, 4), 3x3x3 causal convs, RMS gains.
+# ---------------------------------------------------------------------------
+@dataclasses.dataclass(frozen=True)
+class VaeDesc:
+    dims: Tuple[int, int, int] = (96, 192, 384)
+    latent_channels: int = 16
+    video_channels: int = 3
+    frames_per_chunk: int = 4     # video frames per latent frame (temporal factor 4)
+    eps: float = 1e-6
+
+
+VAE = VaeDesc()
+
+
+def vae_layers(vd: VaeDesc = VAE):
+    """Ordered layer list: (name, kind, cin, cout) with kind in {conv, res, norm, pool_s,
+    pool_st, up_s, up_st}.  res = RMS-SiLU-conv-RMS-SiLU-conv + skip (channels c)."""
+    c1, c2, c3 = vd.dims
+    enc = [("enc.conv_in", "conv", vd.video_channels, c1), ("enc.res1", "res", c1, c1), ("enc.p1", "pool_s", c1, c1),
+           ("enc.conv2", "conv", c1, c2), ("enc.res2", "res", c2, c2), ("enc.p2", "pool_st", c2, c2),
+           ("enc.conv3", "conv", c2, c3), ("enc.res3", "res", c3, c3), ("enc.p3", "pool_st", c3, c3),
+           ("enc.res4", "res", c3, c3), ("enc.norm_out", "norm", c3, c3),
+           ("enc.conv_out", "conv", c3, vd.latent_channels)]
+    dec = [("dec.conv_in", "conv", vd.latent_channels, c3), ("dec.res1", "res", c3, c3), ("dec.u1", "up_st", c3, c3),
+           ("dec.conv2", "conv", c3, c3), ("dec.res2", "res", c3, c3), ("dec.u2", "up_st", c3, c3),
+           ("dec.conv3", "conv", c3, c2), ("dec.res3", "res", c2, c2), ("dec.u3", "up_s", c2, c2),
+           ("dec.conv4", "conv", c2, c1), ("dec.res4", "res", c1, c1), ("dec.norm_out", "norm", c1, c1),
+           ("dec.conv_out", "conv", c1, vd.video_channels)]
+    return enc, dec
+
+
+def vae_tensor_specs(vd: VaeDesc = VAE):
+    """name -> (shape, law); conv weights [cout, 3, 3, 3, cin] and biases U(+-1/sqrt(27 cin)),
+    RMS gains 1 + 0.1 N(0, 1)."""
+    out = {}
+    enc, dec = vae_layers(vd)
+    for name, kind, ci, co in enc + dec:
+        if kind == "conv":
+            out[f"vae.{name}.w"] = ((co, 3, 3, 3, ci), ("u", 27 * ci))
+            out[f"vae.{name}.b"] = ((co,), ("u", 27 * ci))
+        elif kind == "res":
+            for k in ("1", "2"):
+                out[f"vae.{name}.n{k}"] = ((ci,), ("gain",))
+                out[f"vae.{name}.c{k}.w"] = ((ci, 3, 3, 3, ci), ("u", 27 * ci))
+                out[f"vae.{name}.c{k}.b"] = ((ci,), ("u", 27 * ci))
+        elif kind == "norm":
+            out[f"vae.{name}.g"] = ((ci,), ("gain",))
+    return out
+
+
+def gen_vae_weights(vd: VaeDesc = VAE, seed: int = 0) -> Dict[str, np.ndarray]:
+    out = {}
+    for name, (shape, law) in vae_tensor_specs(vd).items():
+        r = _rng(seed, name)
+        if law[0] == "u":
+            bound = 1.0 / np.sqrt(law[1])
+            a = r.uniform(-bound, bound, size=shape)
+        else:
+            a = 1.0 + 0.1 * r.standard_normal(size=shape)
+        out[name] = round_to_bf16(a.astype(np.float32))
+    return out
+
+
+def gen_video(vd: VaeDesc, frames: int, H: int, W: int, seed: int = 5) -> np.ndarray:
+    """A moving synthetic video [3, frames, H, W] fp32 (sinusoid field, translation + noise)."""
+    ls = LatentStream(vd.video_channels, H, W, seed=seed, speeds=(0.0, 1.0, 3.0), segment=4)
+    return np.stack([ls.frame(g) for g in range(frames)], axis=1)
