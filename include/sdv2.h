@@ -317,6 +317,33 @@ sdv2_status sdv2_rebalance(const double* measured_block_ms, int32_t num_blocks, 
                            double* ema, const int32_t* cur_bounds, int32_t* new_bounds, int32_t* changed,
                            double* pred_cur, double* pred_new);
 
+/* ---- Stream-VAE stand-in ("processes short video chunks
+ * (e.g., 4 frames) and caches intermediate features within each 3D convolution") ----
+ * Wan2.1-VAE-shaped causal 3D-conv encoder / decoder: 4 video frames [3][4][H][W] <-> one
+ * latent frame [latent_channels][1][H/8][W/8] (fp32, host or device pointers), every 3x3x3
+ * conv causal in time with a two-frame feature cache carried across chunks (so a streamed
+ * run equals the full-sequence causal VAE).  Layer list in DESIGN.md / oracle/vae.py.
+ * Weights: fp32, in layer order: conv (w [co][3][3][3][ci], b [co]); residual block (n1 [c],
+ * c1.w, c1.b, n2 [c], c2.w, c2.b); norm (g [c]) — synthgen.vae_tensor_specs order.
+ * The workspace is caller-owned (sdv2_vae_workspace_bytes), zeroed and carved at create. */
+typedef struct {
+  int32_t video_h, video_w;      /* multiples of 8 */
+  int32_t dims[3];               /* stage channels (96, 192, 384); each <= 384 */
+  int32_t latent_channels;       /* 16; <= 384 */
+  float eps;                     /* RMS epsilon */
+} sdv2_vae_desc;
+typedef struct sdv2_vae sdv2_vae;
+size_t sdv2_vae_workspace_bytes(const sdv2_vae_desc* d);
+sdv2_status sdv2_vae_create(const sdv2_vae_desc* d, const sdv2_weights* w, void* workspace, size_t workspace_bytes,
+                            int device, void* stream, sdv2_vae** out);
+/* New video stream: zero every convolution's feature cache. */
+sdv2_status sdv2_vae_reset(sdv2_vae* v);
+sdv2_status sdv2_vae_encode_chunk(sdv2_vae* v, const float* video, float* latent);
+sdv2_status sdv2_vae_decode_chunk(sdv2_vae* v, const float* latent, float* video);
+int64_t sdv2_vae_launches(const sdv2_vae* v);
+const char* sdv2_vae_last_error(const sdv2_vae* v);
+sdv2_status sdv2_vae_destroy(sdv2_vae* v);
+
 /* ---- SLO-aware batching scheduler (host only) ----
  * A latency point is one MEASURED call latency L(T', B): chunk_frames = T' latent frames
  * per chunk, streams = B streams batched per call (sdv2_geometry.streams).  Every stream

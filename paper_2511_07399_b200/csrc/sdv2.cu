@@ -23,6 +23,7 @@
 #include "gemm_tc.cuh"
 #include "attn_tc.cuh"
 #include "xattn_tc.cuh"
+#include "vae.cuh"
 #include "elem.cuh"
 #include "kernels.cuh"
 

@@ -524,3 +524,108 @@ def chunk_embedding(chunk: np.ndarray) -> np.ndarray:
     L.sdv2_chunk_embedding.restype = ctypes.c_int
     _check(L.sdv2_chunk_embedding(ctypes.c_void_p(a.ctypes.data), C, T, H, W, ctypes.c_void_p(out.ctypes.data)))
     return out
+
+
+# ------------------------------------------------------------ Stream-VAE stand-in (N1)
+class VaeDescC(ctypes.Structure):
+    _fields_ = [("video_h", ctypes.c_int32), ("video_w", ctypes.c_int32), ("dims", ctypes.c_int32 * 3),
+                ("latent_channels", ctypes.c_int32), ("eps", ctypes.c_float)]
+
+
+def vae_weight_order():
+    """Tensor names in the order sdv2_vae_create takes them (include/sdv2.h)."""
+    names = []
+    enc = [("enc.conv_in", "conv"), ("enc.res1", "res"), ("enc.conv2", "conv"), ("enc.res2", "res"),
+           ("enc.conv3", "conv"), ("enc.res3", "res"), ("enc.res4", "res"), ("enc.norm_out", "norm"),
+           ("enc.conv_out", "conv")]
+    dec = [("dec.conv_in", "conv"), ("dec.res1", "res"), ("dec.conv2", "conv"), ("dec.res2", "res"),
+           ("dec.conv3", "conv"), ("dec.res3", "res"), ("dec.conv4", "conv"), ("dec.res4", "res"),
+           ("dec.norm_out", "norm"), ("dec.conv_out", "conv")]
+    for name, kind in enc + dec:
+        p = f"vae.{name}."
+        if kind == "conv":
+            names += [p + "w", p + "b"]
+        elif kind == "res":
+            names += [p + "n1", p + "c1.w", p + "c1.b", p + "n2", p + "c2.w", p + "c2.b"]
+        else:
+            names += [p + "g"]
+    return names
+
+
+class StreamVAE:
+    """Library Stream-VAE handle: encode / decode 4-frame chunks with feature caches."""
+
+    def __init__(self, vd, H, W, weights, device=0, stream=None):
+        import torch
+        self.torch = torch
+        L = lib()
+        L.sdv2_vae_workspace_bytes.restype = ctypes.c_size_t
+        L.sdv2_vae_workspace_bytes.argtypes = [ctypes.POINTER(VaeDescC)]
+        L.sdv2_vae_create.argtypes = [ctypes.POINTER(VaeDescC), ctypes.POINTER(WeightsC), ctypes.c_void_p,
+                                      ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)]
+        for f in ("sdv2_vae_create", "sdv2_vae_reset", "sdv2_vae_encode_chunk", "sdv2_vae_decode_chunk",
+                  "sdv2_vae_destroy"):
+            getattr(L, f).restype = ctypes.c_int
+        L.sdv2_vae_reset.argtypes = [ctypes.c_void_p]
+        L.sdv2_vae_encode_chunk.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+        L.sdv2_vae_decode_chunk.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+        L.sdv2_vae_destroy.argtypes = [ctypes.c_void_p]
+        L.sdv2_vae_last_error.restype = ctypes.c_char_p
+        L.sdv2_vae_last_error.argtypes = [ctypes.c_void_p]
+        L.sdv2_vae_launches.restype = ctypes.c_int64
+        L.sdv2_vae_launches.argtypes = [ctypes.c_void_p]
+        self.L = L
+        self.vd, self.H, self.W = vd, H, W
+        self.desc = VaeDescC(H, W, (ctypes.c_int32 * 3)(*vd.dims), vd.latent_channels, vd.eps)
+        nbytes = L.sdv2_vae_workspace_bytes(ctypes.byref(self.desc))
+        if nbytes == 0:
+            raise SDV2Error("invalid Stream-VAE descriptor")
+        self.workspace = torch.empty(nbytes + 1024, dtype=torch.uint8, device=f"cuda:{device}")
+        self.stream = stream if stream is not None else torch.cuda.Stream(device)
+        names = vae_weight_order()
+        keep = [np.ascontiguousarray(weights[n], dtype=np.float32) for n in names]
+        ptrs = (ctypes.c_void_p * len(keep))(*[a.ctypes.data for a in keep])
+        w = WeightsC(ptrs, len(keep))
+        h = ctypes.c_void_p()
+        st = L.sdv2_vae_create(ctypes.byref(self.desc), ctypes.byref(w), ctypes.c_void_p(self.workspace.data_ptr()),
+                               nbytes + 1024, device, ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(h))
+        if st != 0:
+            msg = L.sdv2_vae_last_error(h).decode() if h.value else ""
+            if h.value:
+                L.sdv2_vae_destroy(h)
+            raise SDV2Error(f"{STATUS.get(st, st)}: {msg}")
+        self.h = h
+
+    def _sync_in(self):
+        cur = self.torch.cuda.current_stream()
+        if cur != self.stream:
+            self.stream.wait_stream(cur)
+
+    def reset(self):
+        _check(self.L.sdv2_vae_reset(self.h))
+
+    def encode_chunk(self, video_ptr, latent_ptr):
+        self._sync_in()
+        st = self.L.sdv2_vae_encode_chunk(self.h, ctypes.c_void_p(video_ptr), ctypes.c_void_p(latent_ptr))
+        if st != 0:
+            raise SDV2Error(f"{STATUS.get(st, st)}: {self.L.sdv2_vae_last_error(self.h).decode()}")
+
+    def decode_chunk(self, latent_ptr, video_ptr):
+        self._sync_in()
+        st = self.L.sdv2_vae_decode_chunk(self.h, ctypes.c_void_p(latent_ptr), ctypes.c_void_p(video_ptr))
+        if st != 0:
+            raise SDV2Error(f"{STATUS.get(st, st)}: {self.L.sdv2_vae_last_error(self.h).decode()}")
+
+    def launches(self):
+        return self.L.sdv2_vae_launches(self.h)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.sdv2_vae_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
