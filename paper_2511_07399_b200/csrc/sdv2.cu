@@ -80,6 +80,7 @@ struct Packet {
   float* sign;  // [n]
   float* lat;   // [n, CTHW]
   size_t bytes;
+  size_t nx = 0, ne0 = 0, ne = 0;   // element counts of x, e0, e
 };
 
 }  // namespace
@@ -201,6 +202,25 @@ struct ProfScope {
 
 namespace {
 
+// Point the packet fields at `base` (the layout is the same in every packet buffer).
+void set_packet(sdv2_handle* h, char* base) {
+  float* p = reinterpret_cast<float*>(base);
+  h->st.x = p; p += h->st.nx;
+  h->st.e0 = p; p += h->st.ne0;
+  h->st.e = p; p += h->st.ne;
+  h->st.sig = p; p += 64;
+  h->st.sign = p; p += 64;
+  h->st.lat = p;
+}
+
+// Where call parity `par` computes its packet: in place in the hand-off buffers, so no
+// stage copies the packet (K = 1: the handle's own packet; rank 0: the outgoing buffer;
+// ranks > 0: the received buffer, which is also what they send on).
+char* packet_for(sdv2_handle* h, int par) {
+  if (h->K == 1) return h->packet_base;
+  return h->rank == 0 ? h->act_io[1][par] : h->act_io[0][par];
+}
+
 size_t carve(sdv2_handle* h, void* base) {
   Carver cv(base);
   const size_t TWb = h->prec == SDV2_BF16 ? 2 : 4;
@@ -245,14 +265,9 @@ size_t carve(sdv2_handle* h, void* base) {
                  lat = size_t(h->NE) * h->CTHW;
     const size_t sz = (x + e0 + e + 2 * 64 + lat) * 4;
     h->st.bytes = sz;
+    h->st.nx = x; h->st.ne0 = e0; h->st.ne = e;
     h->packet_base = cv.take<char>(sz);
-    float* p = reinterpret_cast<float*>(h->packet_base);
-    h->st.x = p; p += x;
-    h->st.e0 = p; p += e0;
-    h->st.e = p; p += e;
-    h->st.sig = p; p += 64;
-    h->st.sign = p; p += 64;
-    h->st.lat = p;
+    set_packet(h, h->packet_base);
     for (int io = 0; io < 2; ++io)
       for (int par = 0; par < 2; ++par) h->act_io[io][par] = h->K > 1 ? cv.take<char>(sz) : nullptr;
   }
@@ -735,16 +750,12 @@ sdv2_status tick_body(sdv2_handle* h, int na, int par) {
     else gemvs(std::integral_constant<int, 16>{});
     h->launches += 2;
     CKL();
-  } else {
-    CK(cudaMemcpyAsync(h->packet_base, h->act_io[0][par], h->st.bytes, cudaMemcpyDeviceToDevice, h->stream));
   }
   for (int b = h->a0; b < h->a1; ++b) {
     ProfScope ps(h, 4, 0.0, b);
     TRY(run_block<TA>(h, b, rows, na));
   }
-  if (!last) {
-    CK(cudaMemcpyAsync(h->act_io[1][par], h->packet_base, h->st.bytes, cudaMemcpyDeviceToDevice, h->stream));
-  } else {
+  if (last) {
     ProfScope ps(h, 5, 0.0);
     // head (C.7): a = N(x)(1 + mod_h[1] + e) + mod_h[0] + e; y = a W_h^T + b_h (fp32 out);
     // then unpatchify + x0 + output / re-noise (C.8, O5)
@@ -785,6 +796,7 @@ sdv2_status tick(sdv2_handle* h, const float* chunk_latent, float* out_latent, i
   h->td_ev_used[slot] = true;
   const int na = tdh->n_active;
   const int par = int(call & 1);
+  set_packet(h, packet_for(h, par));   // captured graphs are keyed by parity: pointers match
   const bool first = h->rank == 0, last = h->rank == h->K - 1;
   // tick info (host, no sync: the schedule is deterministic)
   h->info.call = call;
@@ -1111,6 +1123,9 @@ sdv2_status sdv2_reset_stream(sdv2_handle* h, const sdv2_stream_desc* sd, const 
   CK(cudaMemsetAsync(h->Kx, 0, px, h->stream));
   CK(cudaMemsetAsync(h->Vx, 0, px, h->stream));
   CK(cudaMemsetAsync(h->packet_base, 0, h->st.bytes, h->stream));
+  for (int io = 0; io < 2; ++io)
+    for (int par = 0; par < 2; ++par)
+      if (h->act_io[io][par]) CK(cudaMemsetAsync(h->act_io[io][par], 0, h->st.bytes, h->stream));
   {
     std::vector<CtrlState> cs(h->B);
     std::memset(cs.data(), 0, sizeof(CtrlState) * h->B);
@@ -1175,7 +1190,7 @@ sdv2_status sdv2_denoise_chunk(sdv2_handle* h, const float* chunk_latent, float*
 sdv2_status sdv2_stage_io_buffers(sdv2_handle* h, int32_t parity, sdv2_stage_io* io) {
   if (!h || !io || parity < 0 || parity > 1) return SDV2_E_INVALID;
   io->act_in = h->act_io[0][parity];
-  io->act_out = h->act_io[1][parity];
+  io->act_out = h->rank == 0 ? h->act_io[1][parity] : h->act_io[0][parity];   // in place (packet_for)
   io->act_bytes = h->K > 1 ? h->st.bytes : 0;
   io->ring_in = h->ring[0][parity];
   io->ring_out = h->ring[1][parity];

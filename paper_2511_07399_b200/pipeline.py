@@ -51,11 +51,13 @@ class StageTransport:
         # runs, e.g. around an online re-partition).  global producer call -> tensor
         self.ring_stash = {}
 
-    def _buf(self, t):
-        """Tensor used on the wire (a host copy when staging through the host)."""
+    def _buf(self, t, role="recv"):
+        """Tensor used on the wire (a host copy when staging through the host).  Sends and
+        receives of the same device buffer get separate host copies: ranks > 0 send from
+        the buffer they received into (the packet is computed in place)."""
         if not self.host or t.device.type == "cpu":
             return t
-        key = (t.data_ptr(), t.numel())
+        key = (t.data_ptr(), t.numel(), role)
         if key not in self._stage:
             self._stage[key] = self.torch.empty(t.numel(), dtype=self.torch.uint8)
         return self._stage[key]
@@ -69,7 +71,7 @@ class StageTransport:
             cur = self.io((self.base + c) & 1)
             if r < K - 1 and cur["act_out"].numel():
                 src = cur["act_out"]
-                wire = self._buf(src)
+                wire = self._buf(src, "send")
                 if wire is not src:
                     wire.copy_(src)
                 ops.append(dist.P2POp(dist.isend, wire, r + 1))
@@ -77,7 +79,7 @@ class StageTransport:
             if r == K - 1 and K > 1 and cur["ring_out"].numel():
                 src = cur["ring_out"]
                 if c + K < num_calls:
-                    wire = self._buf(src)
+                    wire = self._buf(src, "send")
                     if wire is not src:
                         wire.copy_(src)
                     ops.append(dist.P2POp(dist.isend, wire, 0))
@@ -156,7 +158,7 @@ class StageTransport:
         for p in producers:
             if r == K - 1:
                 src = self.ring_stash.pop(p)
-                wire = self._buf(src)
+                wire = self._buf(src, "send")
                 if wire is not src:
                     wire.copy_(src)
                 ops.append(dist.P2POp(dist.isend, wire, 0))
