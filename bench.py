@@ -241,10 +241,12 @@ def run_ours(args, cfg):
     B.build()
     torch.cuda.set_device(local)
     md, g, sd = cfg.model, cfg.geom, cfg.stream
-    if args.window or args.denoise_steps:
+    if args.window or args.denoise_steps or args.chunk_frames:
         import dataclasses
         if args.window:
             g = dataclasses.replace(g, window_chunks=args.window)
+        if args.chunk_frames:   # T' latent frames per chunk (SLO table L(T', B))
+            g = dataclasses.replace(g, chunk_frames=args.chunk_frames)
         if args.denoise_steps:   # E10 "no Stream Batch": n = 1 ticks, one per denoising step
             g = dataclasses.replace(g, steps=args.denoise_steps)
             sd = dataclasses.replace(sd, timesteps=sg.SCHEDULES[args.denoise_steps])
@@ -444,6 +446,7 @@ def main():
     ap.add_argument("--no-l2-persist", dest="l2_persist", action="store_false",
                     help="no persisting-L2 window on the residual stream (A/B)")
     ap.add_argument("--window", type=int, default=0, help="override W (rolling-window chunks)")
+    ap.add_argument("--chunk-frames", type=int, default=0, help="override T' (latent frames per chunk)")
     ap.add_argument("--denoise-steps", type=int, default=0, choices=[0, 1, 2, 4],
                     help="override n (in-flight denoising steps = Stream Batch size)")
     ap.add_argument("--latency-chunks", type=int, default=1024,

@@ -123,7 +123,11 @@ typedef struct {
  * the library reads act_in/ring_in of parity c%2 and writes act_out/ring_out of parity
  * c%2.  Rank s>0 must receive, before its call c, the act packet rank s-1 produced at
  * its call c; rank 0 (world > 1) must receive, before its call c >= K, the ring packet
- * the last rank produced at its call c-K.  K = 1 needs no transport. */
+ * the last rank produced at its call c-K.  The packet is computed in place: on ranks
+ * s > 0 act_out == act_in (the received buffer is updated and sent on), so a send of call
+ * c must complete before the receive for call c+2 lands in the same parity buffer (NCCL
+ * groups on one communicator are ordered; pipeline.py waits a send one call later).
+ * K = 1 needs no transport. */
 typedef struct {
   void* act_in;  void* act_out;  size_t act_bytes;
   void* ring_in; void* ring_out; size_t ring_bytes;

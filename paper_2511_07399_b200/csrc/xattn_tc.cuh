@@ -16,7 +16,7 @@
 //   key-half warps of a row), then the exponential pass writes P (bf16, over its own S
 //   columns) tile by tile and each PV_t MMA starts as soon as P_t is in TMEM; P_0 (from
 //   registers) goes into slot 0 after PV_3 has read P_3 there.
-// Warp roles (320 threads): 0 TMA (Q double buffer, one K/V ring: K_0..K_{J-1} then
+// Warp roles (320 threads): 0 TMA (one Q tile, one 5-stage K/V ring: K_0..K_{J-1} then
 // V_0..V_{J-1}), 1 MMA issuer, 2..9 softmax / epilogue (TMEM lane quarter x key half).
 #pragma once
 #include "attn_tc.cuh"
@@ -24,14 +24,14 @@
 namespace sdv2 {
 
 constexpr int kXattnThreads = 320;
-constexpr int kXattnKV = 4;          // K/V ring stages
+constexpr int kXattnKV = 5;          // K/V ring stages: K_0..K_3 and V_0 in flight at unit start
 constexpr int kXattnMaxJ = 4;        // key tiles per unit (Lk <= 512)
 
 template <int HD>
 struct XattnSmem {
   static constexpr int Q = kAttnBQ * HD * 2;
   static constexpr int KV = kAttnBKV * HD * 2;
-  static constexpr int total = 2 * Q + kXattnKV * KV + 1024 + 512 + 3 * 1024 + 64;
+  static constexpr int total = Q + kXattnKV * KV + 1024 + 512 + 2 * 1024 + 64;
 };
 
 struct XattnArgs {
@@ -72,8 +72,8 @@ __global__ void __launch_bounds__(kXattnThreads, 1) xattn_tc_kernel(const __grid
   constexpr int NCH = HD / 64;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;                         // 2 stages
-  uint8_t* sKV = sQ + 2 * SM::Q;              // kXattnKV stages
+  uint8_t* sQ = smem;                         // one Q tile (a CTA rarely owns two units)
+  uint8_t* sKV = sQ + SM::Q;                  // kXattnKV stages
   uint64_t* bar = reinterpret_cast<uint64_t*>(sKV + kXattnKV * SM::KV);
   uint64_t* q_full = bar;                     // [2]
   uint64_t* q_empty = bar + 2;                // [2]
@@ -134,8 +134,8 @@ __global__ void __launch_bounds__(kXattnThreads, 1) xattn_tc_kernel(const __grid
       xattn_unit(a, u, e, h, qt);
       const int col = h * HD;
       const int kv_row = a.kv_row0 + td->e[e].xslot * a.kv_slot_rows;
-      const int qs = ui & 1;
-      tc::mbar_wait(q_empty + qs, ((ui >> 1) & 1) ^ 1);
+      const int qs = 0;
+      tc::mbar_wait(q_empty, (ui & 1) ^ 1);
       if (tc::elect_one()) {
         tc::mbar_expect_tx(q_full + qs, SM::Q);
         for (int ch = 0; ch < NCH; ++ch)
@@ -165,8 +165,8 @@ __global__ void __launch_bounds__(kXattnThreads, 1) xattn_tc_kernel(const __grid
     int kvi = 0, ui = 0;
     for (int u = c; u < units; u += G, ++ui) {
       const uint32_t ph = ui & 1;
-      const int qs = ui & 1;
-      tc::mbar_wait(q_full + qs, (ui >> 1) & 1);
+      const int qs = 0;
+      tc::mbar_wait(q_full, ui & 1);
       const uint32_t qa = tc::smem_u32(sQ + qs * SM::Q);
       // S_t = Q K_t^T (S_3 into slot 0 once the softmax copied S_0 out)
       for (int t = 0; t < J; ++t, ++kvi) {
