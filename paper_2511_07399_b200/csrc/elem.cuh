@@ -54,6 +54,7 @@ struct ModArgs {
   const float* modA; int sc_off, sh_off;
   const float* eA; int estride, esc_off, esh_off;
   float a0;
+  float* zero_rows = nullptr;   // if set, zero_rows[r] = 0 for every row (a downstream GEMM's atomic row sums)
 };
 
 template <typename TA, int NV>
@@ -77,7 +78,7 @@ __global__ void __launch_bounds__(256) norm_mod2_kernel(const float* __restrict_
     v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     A[i] = B[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (c < d && ok) {
-      v[i] = __ldcs(reinterpret_cast<const float4*>(xr + c));
+      v[i] = __ldcg(reinterpret_cast<const float4*>(xr + c));
       A[i] = __ldg(reinterpret_cast<const float4*>(m.modA + m.sc_off + c));
       B[i] = __ldg(reinterpret_cast<const float4*>(m.modA + m.sh_off + c));
       if (m.eA) {
@@ -108,6 +109,7 @@ __global__ void __launch_bounds__(256) norm_mod2_kernel(const float* __restrict_
   row_sum2(ss, dummy2, &red[1][0][0], sub);
   const float inv = rsqrtf(ss / float(d) + eps);
   if (!ok) return;
+  if (m.zero_rows && t == 0) m.zero_rows[r] = 0.f;
   TA* orow = out + size_t(r) * d;
 #pragma unroll
   for (int i = 0; i < NV; ++i) {

@@ -90,16 +90,22 @@ __device__ __forceinline__ void gemm_epilogue_chunk(const EpiArgs& ep, int r, in
       acc[i + 2] = s1.x;
       acc[i + 3] = s1.y;
     }
-    if (EPI == EPI_STORE || EPI == EPI_GELU) {
+    if (EPI == EPI_STORE || EPI == EPI_GELU || EPI == EPI_STORE_RSQ) {
       if constexpr (sizeof(TOut) == 2) {
         uint32_t pk[16];
+        float ssq = 0.f;
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           float2 a = make_float2(acc[2 * i], acc[2 * i + 1]);
           if (EPI == EPI_GELU && !(ep.dbg & 2)) a = gelu_tanh_fast2(a);
           __nv_bfloat162 h2 = __floats2bfloat162_rn(a.x, a.y);
           pk[i] = *reinterpret_cast<uint32_t*>(&h2);
+          if (EPI == EPI_STORE_RSQ) {   // of the stored (bf16) values, as the unfused RMS kernel read them
+            const float2 b = __bfloat1622float2(h2);
+            ssq += b.x * b.x + b.y * b.y;
+          }
         }
+        if (EPI == EPI_STORE_RSQ && r < M) atomicAdd(ep.rowsq + r, ssq);
         if (ep.dbg & 8) {   // test hook: each thread stores its row segment directly
           if (r < M) {
             uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<TOut*>(ep.out) + size_t(r) * ep.ldo + c0);
@@ -370,6 +376,46 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
           }
         }
       }
+      if (kResTMA && x_late) {
+        // The x tile overlays the operand ring (x_late: one tile per cluster).  Fetch each
+        // 32-column box as soon as the ring stages under its bytes are released by the last
+        // MMAs, so the fetch overlaps the tail of the mainloop instead of following it.
+        GemmSegIter it1 = segs;
+        GemmSeg g1;
+        if (it1.next(g1)) {
+          const int mb = (g1.t % num_mg) * MC + cr, nb = g1.t / num_mg;
+          const int nbox = BN / 32;
+          uint32_t freed = 0, issued = 0;
+          auto stage_of = [&](int off) {   // ring stage owning smem byte `off`
+            return off < kStages * kGemmSmemA ? off / kGemmSmemA : (off - kStages * kGemmSmemA) / kSmemB;
+          };
+          for (int q = 0; q < kStages; ++q) {
+            tc::mbar_wait(empty + stage, phase ^ 1);
+            freed |= 1u << stage;
+            // every lane takes the same decisions (freed is warp-uniform); one lane issues
+            uint32_t now = 0;
+            for (int i = 0; i < nbox; ++i) {
+              if ((issued >> i) & 1) continue;
+              const int lo = i * (kGemmBM * 128), hi = lo + kGemmBM * 128 - 1;
+              bool ok = true;
+              for (int st = stage_of(lo); st <= stage_of(hi) && ok; ++st) ok = (freed >> st) & 1;
+              if (ok) now |= 1u << i;
+            }
+            if (now && tc::elect_one()) {
+              if (issued == 0) tc::mbar_expect_tx(x_full, uint32_t(BN) * kGemmBM * 4);
+              for (int i = 0; i < nbox; ++i)
+                if ((now >> i) & 1)
+                  tc::tma_load_2d(sX + i * (kGemmBM * 128), &tmX, x_full, nb * BN + i * 32, mb * kGemmBM);
+            }
+            issued |= now;
+            __syncwarp();
+            if (++stage == kStages) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+      }
     }
   } else if (warp == 1) {
     if (cr == 0) {   // whole warp walks the loop; one elected lane issues (see tc::elect_one)
@@ -479,11 +525,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
       tc::tc_fence_after();
       const int r = mb * kGemmBM + row;
       const float* gsm = sGate + ((r < M ? r : M - 1) / ep.L > e_lo ? kGemmMaxBN : 0);
-      if (kResTMA && x_late && !partial && leader) {   // last MMA done: the operand ring is free
-        tc::mbar_expect_tx(x_full, uint32_t(BN) * kGemmBM * 4);
-        for (int c = 0; c < BN; c += 32)
-          tc::tma_load_2d(sX + (c / 32) * (kGemmBM * 128), &tmX, x_full, nb * BN + c, mb * kGemmBM);
-      }
       if (kResTMA && !partial) tc::mbar_wait(x_full, (nx++) & 1);
       const uint32_t tbase = tmem + (uint32_t(q * 32) << 16) + uint32_t(acc * BN);
       auto chunk = [&](const uint32_t(&v0)[32], int c) {
@@ -660,6 +701,7 @@ inline bool tc_gemm_plan(TmaGemmPlan& p, std::string* err) {
   gemm_set_attr<EPI_RES_GATE, bf16, 1>(); gemm_set_attr<EPI_RES_GATE, bf16, 2>();
   gemm_set_attr<EPI_RES, bf16, 1>(); gemm_set_attr<EPI_RES, bf16, 2>();
   gemm_set_attr<EPI_STORE, float, 1>(); gemm_set_attr<EPI_STORE, float, 2>();
+  gemm_set_attr<EPI_STORE_RSQ, bf16, 1>(); gemm_set_attr<EPI_STORE_RSQ, bf16, 2>();
   return true;
 }
 
@@ -770,6 +812,7 @@ inline cudaError_t gemm_dispatch(cudaStream_t s, int grid, const CUtensorMap& ma
     case EPI_GELU: return gemm_launch<EPI_GELU, bf16, MC>(s, grid, ma, mb, mx, M, N, K, BN, ep, sk);
     case EPI_RES_GATE: return gemm_launch<EPI_RES_GATE, bf16, MC>(s, grid, ma, mb, mx, M, N, K, BN, ep, sk);
     case EPI_STORE_F32: return gemm_launch<EPI_STORE, float, MC>(s, grid, ma, mb, mx, M, N, K, BN, ep, sk);
+    case EPI_STORE_RSQ: return gemm_launch<EPI_STORE_RSQ, bf16, MC>(s, grid, ma, mb, mx, M, N, K, BN, ep, sk);
     default: return gemm_launch<EPI_RES, bf16, MC>(s, grid, ma, mb, mx, M, N, K, BN, ep, sk);
   }
 }

@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(256) rebase_kernel(TA* __restrict__ K, const T
 //   EPI_RES:   x[r,c] += acc + b                                       (cross-O, C.5 7)
 // 64x64 tile, 256 threads (4x4 each), BK = 16.
 // ----------------------------------------------------------------------------
-enum { EPI_STORE = 0, EPI_GELU = 1, EPI_RES_GATE = 2, EPI_RES = 3, EPI_STORE_F32 = 4 };
+enum { EPI_STORE = 0, EPI_GELU = 1, EPI_RES_GATE = 2, EPI_RES = 3, EPI_STORE_F32 = 4, EPI_STORE_RSQ = 5 };
 
 struct EpiArgs {
   void* out;            // TOut* (STORE/GELU) or float* x (RES*)
@@ -162,6 +162,7 @@ struct EpiArgs {
   const float* e0;      // [n, 6, d] (RES_GATE)
   int gate_row;         // 2 (g1) or 5 (g2)
   int L;                // rows per entry
+  float* rowsq;         // EPI_STORE_RSQ: per-row sum of squares of the stored bf16 row (atomic, zeroed upstream)
   long long* trace;     // test hook only (tc GEMM): clock64 stamps of CTA 0 / 1, nullptr = off
   int dbg;              // test hook only (tc GEMM epilogue timing): bit 0 no global stores,
                         // bit 1 no GELU, bit 2 one TMEM load in flight; 0 in the product path

@@ -67,6 +67,7 @@ struct BlockW {
   void* wcv; float* bcv;
   void* wco; float* bco;
   float *gcq, *gck;
+  float* gkq;                 // [d] g_ck * g_cq: prompt K with the cross-q gain folded in (fused q RMS)
   void* w1; float* b1;        // [F, d]
   void* w2; float* b2;        // [d, F]
 };
@@ -116,6 +117,7 @@ struct sdv2_handle {
   float* u;                   // patchified tokens [Mmax, 4C] fp32
   float* yh;                  // head output [Mmax, 4C] fp32
   float* attn_part;           // stream-K attention partials
+  float* rowsq;               // [Mmax] sum of squares of the raw cross q rows (fused q RMS)
   int* attn_flags;            // [kMaxSMs] split-unit hand-off flags (zero between launches)
   void* head_w_tw;            // head weight [4C, d] TW
   float* t1;                  // [B n, d]
@@ -256,6 +258,7 @@ size_t carve(sdv2_handle* h, void* base) {
     B.wcv = tw(size_t(d) * d); B.bcv = cv.take<float>(d);
     B.wco = tw(size_t(d) * d); B.bco = cv.take<float>(d);
     B.gcq = cv.take<float>(d); B.gck = cv.take<float>(d);
+    B.gkq = cv.take<float>(d);
     B.w1 = tw(size_t(F) * d); B.b1 = cv.take<float>(F);
     B.w2 = tw(size_t(d) * F); B.b2 = cv.take<float>(d);
   }
@@ -282,6 +285,7 @@ size_t carve(sdv2_handle* h, void* base) {
   h->u = cv.take<float>(size_t(h->Mmax) * h->P);
   h->yh = cv.take<float>(size_t(h->Mmax) * h->P);
   h->attn_part = cv.take<float>(attn_scratch_floats(kMaxSMs, h->hd));
+  h->rowsq = cv.take<float>(h->Mmax);
   h->attn_flags = cv.take<int>(kMaxSMs);
   h->t1 = cv.take<float>(size_t(h->NE) * d);
   // activation scratch, aliased by the weight staging buffer during create
@@ -404,6 +408,10 @@ sdv2_status fill_dims(sdv2_handle* h, const sdv2_model_desc* md, const sdv2_geom
     }                                                                         \
   } while (0)
 
+__global__ void mul_vec_kernel(const float* __restrict__ a, const float* __restrict__ b, float* __restrict__ out, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = a[i] * b[i];
+}
+
 template <typename T>
 __global__ void convert_kernel(const float* __restrict__ src, T* __restrict__ dst, size_t n) {
   for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
@@ -456,6 +464,11 @@ sdv2_status gemm_act(sdv2_handle* h, const void* A, const void* W, int M, int N,
   return gemm_simt<bf16, bf16, bf16>(h, static_cast<const bf16*>(A), static_cast<const bf16*>(W), M, N, K, K, epi, ep);
 }
 
+// Cross-q RMS fused into the cross-Q GEMM epilogue (row sums of squares) and the
+// cross-attention scores (per-row scale, gain folded into the prompt K): the bf16 path
+// whenever the prompt fits the single-pass cross kernel.
+inline bool fused_cross_rms(const sdv2_handle* h) { return h->prec == SDV2_BF16 && h->Lt <= kXattnMaxJ * kAttnBKV; }
+
 sdv2_status attention(sdv2_handle* h, const AttnArgs& aa, int Mrows_entries, double flops, int bl) {
   ProfScope ps(h, aa.cross ? 2 : 1, flops);
   dim3 grid((h->L + 15) / 16, h->H, Mrows_entries);
@@ -477,6 +490,9 @@ sdv2_status attention(sdv2_handle* h, const AttnArgs& aa, int Mrows_entries, dou
       xa.scale_log2 = 1.4426950408889634f / sqrtf(float(h->hd));
       xa.o = aa.o;
       xa.ldo = aa.ldo;
+      xa.rowsq = h->rowsq;
+      xa.inv_d = 1.f / float(h->d);
+      xa.eps = h->md.eps;
       return tc_cross_attention(h->stream, h->aplan, aa.q, h->Mmax, h->Kx, h->Vx, 2LL * h->B * h->nb * h->Lt, h->d,
                                 h->hd, xa, h->td_dev, &h->err, h->pdl) ? SDV2_OK : SDV2_E_CUDA;
     }
@@ -564,8 +580,9 @@ sdv2_status launch_norm_args(sdv2_handle* h, int rows, const ModArgs& m) {
 // adaLN (mode 0: shift row sh_row, scale row sc_row of mod + e0[e]) or affine (mode 1).
 template <typename TA>
 sdv2_status launch_norm(sdv2_handle* h, int rows, int mode, const float* mod, int sc_row, int sh_row,
-                        const float* gamma, const float* beta) {
+                        const float* gamma, const float* beta, float* zero_rows = nullptr) {
   ModArgs m{};
+  m.zero_rows = zero_rows;
   if (mode == 0) {
     m.modA = mod; m.sc_off = sc_row * h->d; m.sh_off = sh_row * h->d;
     m.eA = h->st.e0; m.estride = 6 * h->d; m.esc_off = sc_row * h->d; m.esh_off = sh_row * h->d;
@@ -622,11 +639,13 @@ sdv2_status run_block(sdv2_handle* h, int bl, int rows, int n_act) {
   // 5. out projection + gated residual (g1 = row 2)
   ep.out = h->st.x; ep.ldo = d; ep.bias = B.bo; ep.mod = B.mod; ep.e0 = h->st.e0; ep.gate_row = 2;
   TRY(gemm_act(h, h->o, B.wo, rows, d, d, EPI_RES_GATE, ep));
-  // 6. cross-attention: affine norm3, q projection, RMS q
-  TRY(launch_norm<TA>(h, rows, 1, nullptr, 0, 0, B.n3g, B.n3b));
-  ep.out = h->q; ep.ldo = d; ep.bias = B.bcq;
-  TRY(gemm_act(h, h->a, B.wcq, rows, d, d, EPI_STORE, ep));
-  {
+  // 6. cross-attention: affine norm3, q projection, RMS q (fused on the bf16 path: the
+  //    GEMM epilogue sums q^2 per row, the cross kernel scales the scores, K carries g_cq)
+  const bool fused = fused_cross_rms(h);
+  TRY(launch_norm<TA>(h, rows, 1, nullptr, 0, 0, B.n3g, B.n3b, fused ? h->rowsq : nullptr));
+  ep.out = h->q; ep.ldo = d; ep.bias = B.bcq; ep.rowsq = h->rowsq;
+  TRY(gemm_act(h, h->a, B.wcq, rows, d, d, fused ? EPI_STORE_RSQ : EPI_STORE, ep));
+  if (!fused) {
     const int units_pt = (d / (16 / int(sizeof(TA))) + kRowThreads - 1) / kRowThreads;
     if (units_pt <= 2)
       launch_k(h->pdl, rms_rows2_kernel<TA, 2>, dim3((rows + 1) / 2), dim3(256), 0, h->stream, static_cast<TA*>(h->q), B.gcq, rows, d, h->md.eps);
@@ -672,7 +691,8 @@ sdv2_status embed_prompt(sdv2_handle* h, const float* prompt_host, int b_stream,
     TA* Vd = static_cast<TA*>(h->Vx) + (size_t(b) * 2 * h->B + slot) * px;
     ep.out = h->ctx_tmp; ep.bias = B.bck;
     TRY((gemm_simt<float, TA, float>(h, h->ctx, static_cast<const TA*>(B.wck), Lt, d, d, d, EPI_STORE, ep)));
-    launch_k(h->pdl, rms_rows_kernel<float, TA>, dim3((Lt + 7) / 8), dim3(256), 0, h->stream, h->ctx_tmp, Kd, B.gck, Lt, d, d, h->md.eps);
+    launch_k(h->pdl, rms_rows_kernel<float, TA>, dim3((Lt + 7) / 8), dim3(256), 0, h->stream, h->ctx_tmp, Kd,
+             fused_cross_rms(h) ? B.gkq : B.gck, Lt, d, d, h->md.eps);
     CKL();
     ep.out = Vd; ep.bias = B.bcv;
     TRY((gemm_simt<float, TA, TA>(h, h->ctx, static_cast<const TA*>(B.wcv), Lt, d, d, d, EPI_STORE, ep)));
@@ -962,6 +982,8 @@ sdv2_status sdv2_create(const sdv2_model_desc* md, const sdv2_geometry* g, const
       if (s != SDV2_OK) return fail(s);
     }
   }
+  for (int b = 0; b < h->nb; ++b)   // g_ck * g_cq for the fused cross-q RMS
+    mul_vec_kernel<<<(d + 255) / 256, 256, 0, h->stream>>>(h->bw[b].gck, h->bw[b].gcq, h->bw[b].gkq, d);
   if (cudaStreamSynchronize(h->stream) != cudaSuccess) {
     h->err = cudaGetErrorString(cudaGetLastError());
     return fail(SDV2_E_CUDA);
@@ -1004,7 +1026,7 @@ sdv2_status sdv2_create(const sdv2_model_desc* md, const sdv2_geometry* g, const
     for (int na = 1; na <= h->n; ++na) {
       const int M = na * h->B * h->L;
       EpiArgs ep{};
-      ep.L = h->L; ep.mod = B.mod; ep.e0 = h->st.e0; ep.gate_row = 2;
+      ep.L = h->L; ep.mod = B.mod; ep.e0 = h->st.e0; ep.gate_row = 2; ep.rowsq = h->rowsq;
       // weights of every local block (the timed launches cycle through them)
       const int nW = h->nb;
       std::vector<const void*> wl[6];
@@ -1017,7 +1039,7 @@ sdv2_status sdv2_create(const sdv2_model_desc* md, const sdv2_geometry* g, const
       struct Sh { const void* A; const void* const* W; int nW, N, K, epi; void* out; int ldo; const float* bias; } shapes[] = {
           {h->a, wl[0].data(), nW, 3 * d, d, EPI_STORE, h->qkv, 3 * d, B.bqkv},
           {h->o, wl[1].data(), nW, d, d, EPI_RES_GATE, h->st.x, d, B.bo},
-          {h->a, wl[2].data(), nW, d, d, EPI_STORE, h->q, d, B.bcq},
+          {h->a, wl[2].data(), nW, d, d, fused_cross_rms(h) ? EPI_STORE_RSQ : EPI_STORE, h->q, d, B.bcq},
           {h->o, wl[3].data(), nW, d, d, EPI_RES, h->st.x, d, B.bco},
           {h->a, wl[4].data(), nW, h->F, d, EPI_GELU, h->hbuf, h->F, B.b1},
           {h->hbuf, wl[5].data(), nW, d, h->F, EPI_RES_GATE, h->st.x, d, B.b2},

@@ -44,6 +44,11 @@ struct XattnArgs {
   float scale_log2;   // log2(e) / sqrt(hd)
   void* o;            // [rows, ldo] bf16
   int ldo;
+  // Fused cross-q RMS (C.5 step 6, q_c = g_cq RMS_d(q)): when rowsq != nullptr, q holds the
+  // raw projection, rowsq[row] its sum of squares over d, and the prompt K the gain-folded
+  // K_c * g_cq; scores of row r are scaled by rsqrt(rowsq[r] / d + eps).
+  const float* rowsq;
+  float inv_d, eps;
 };
 
 // unit u -> (entry, head, query tile): full tiles first, then the ragged last tiles
@@ -217,12 +222,16 @@ __global__ void __launch_bounds__(kXattnThreads, 1) xattn_tc_kernel(const __grid
     const int row = quarter * 32 + lane;
     const uint32_t lane_off = uint32_t(quarter * 32) << 16;
     auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(2 + quarter) : "memory"); };
-    const uint64_t sc2 = f2pack(a.scale_log2, a.scale_log2);
     int ui = 0;
     for (int u = c; u < units; u += G, ++ui) {
       int e, h, qt;
       xattn_unit(a, u, e, h, qt);
       const uint32_t ph = ui & 1;
+      // per-row softmax scale (the fused q RMS factor, 1 without the fusion)
+      const int qrow = qt * kAttnBQ + row;
+      float rscale = a.scale_log2;
+      if (a.rowsq) rscale *= rsqrtf(a.rowsq[e * a.L + (qrow < a.L ? qrow : a.L - 1)] * a.inv_d + a.eps);
+      const uint64_t sc2 = f2pack(rscale, rscale);
       // ---- max pass (S_0 kept in registers when slot 0 is needed for S_3)
       float s0[HC];
       float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
@@ -258,7 +267,7 @@ __global__ void __launch_bounds__(kXattnThreads, 1) xattn_tc_kernel(const __grid
           if (lane == 0) tc::mbar_arrive(s0_free);
         }
       }
-      float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3])) * a.scale_log2;
+      float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3])) * rscale;
       xm[half * 128 + row] = mx;
       pair_sync();
       mx = fmaxf(mx, xm[(half ^ 1) * 128 + row]);

@@ -59,6 +59,8 @@ def main():
     start = torch.cuda.Event(enable_timing=True)
     start.record(stage.stream)
     for c in range(N + n - 1):
+        if c % 1000 == 0:
+            print(f"call {c} t={time.time() - t0:.1f}s", file=sys.stderr, flush=True)
         if c in cfg.prompt_switch:
             stage.set_prompt(prompts[pidx[c]])
         X = min(c, N - 1)
