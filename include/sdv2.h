@@ -258,6 +258,9 @@ sdv2_status sdv2_set_block_tap(sdv2_handle* h, float* per_block_out);
 sdv2_status sdv2_kv_lane(sdv2_handle* h, int32_t local_block, int32_t lane, int32_t which,
                          void** ptr, size_t* elems);
 
+/* Test hook: synchronise the stream after every launch and log the call site on stderr
+ * (graphs are bypassed while on) — names a kernel that does not complete. */
+sdv2_status sdv2_debug_sync(sdv2_handle* h, int32_t enable);
 /* CUDA-graph replay of the per-call device work (default on; keyed by the number of
  * active entries and the call parity; not used while profiling or tapping). */
 sdv2_status sdv2_set_graphs(sdv2_handle* h, int32_t enable);

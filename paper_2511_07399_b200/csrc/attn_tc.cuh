@@ -609,12 +609,19 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
           pair_sync();
           mx = fmaxf(mx, xm[((gt & 1) * 2 + (half ^ 1)) * 128 + row]);
           if (quarter == 0) ATTN_TRACE(11 + 2 * half, gt);
-          // lazy rescale: P / O stay relative to m_used until the max grows by > 2^8
-          if (mx > m_used + 8.f) {
+          // lazy rescale: P / O stay relative to m_used until the max grows by > 2^8.  The
+          // decision is WARP-UNIFORM: the TMEM accesses below are .sync.aligned (every lane of
+          // the warp must execute them), so when any row of the warp needs it, every row
+          // rescales to max(m_used, mx) (alpha = 1 for a row whose max did not grow).  The two
+          // key-half warps of a row quarter hold the same rows and exchanged maxima, so they
+          // take the same decision.  (A per-row branch here hung the kernel when the rows of
+          // one warp disagreed: found on a 10k-chunk long-horizon run.)
+          if (__any_sync(0xffffffffu, mx > m_used + 8.f)) {
+            const float m_new = fmaxf(m_used, mx);
             if (t > 0) {     // O row (this half's HD/2 columns) *= 2^(m_used - m_new) once PV_{t-1} landed
               tc::mbar_wait(pv_done + (gt - 1) % 3, ((gt - 1) / 3) & 1);
               tc::tc_fence_after();
-              const float alpha = ex2(m_used - mx);
+              const float alpha = m_used == -INFINITY ? 0.f : ex2(m_used - m_new);
               l *= alpha;
   #pragma unroll
               for (int cc = 0; cc < HO / 16; ++cc) {
@@ -634,7 +641,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
               }
               tc::tmem_st_wait();
             }
-            m_used = mx;
+            m_used = m_new;
           }
           // P = exp2(s * scale - m_used) -> bf16 pairs over this half's own S columns (A
           // operand of the PV MMA); a row with no valid key yet writes P = 0

@@ -105,7 +105,9 @@ __device__ __forceinline__ void gemm_epilogue_chunk(const EpiArgs& ep, int r, in
             ssq += b.x * b.x + b.y * b.y;
           }
         }
-        if (EPI == EPI_STORE_RSQ && r < M) atomicAdd(ep.rowsq + r, ssq);
+        // one partial per (row, 32-column chunk), summed in fixed order by the consumer
+        // (no atomics: the bits do not depend on the order CTAs finish)
+        if (EPI == EPI_STORE_RSQ && r < M) ep.rowsq[size_t(r) * (N / 32) + c0 / 32] = ssq;
         if (ep.dbg & 8) {   // test hook: each thread stores its row segment directly
           if (r < M) {
             uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<TOut*>(ep.out) + size_t(r) * ep.ldo + c0);

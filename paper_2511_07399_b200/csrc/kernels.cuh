@@ -162,7 +162,7 @@ struct EpiArgs {
   const float* e0;      // [n, 6, d] (RES_GATE)
   int gate_row;         // 2 (g1) or 5 (g2)
   int L;                // rows per entry
-  float* rowsq;         // EPI_STORE_RSQ: per-row sum of squares of the stored bf16 row (atomic, zeroed upstream)
+  float* rowsq;         // EPI_STORE_RSQ: [M][N / 32] sums of squares of the stored bf16 row, per 32 columns
   long long* trace;     // test hook only (tc GEMM): clock64 stamps of CTA 0 / 1, nullptr = off
   int dbg;              // test hook only (tc GEMM epilogue timing): bit 0 no global stores,
                         // bit 1 no GELU, bit 2 one TMEM load in flight; 0 in the product path

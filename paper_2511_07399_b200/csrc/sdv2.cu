@@ -117,7 +117,7 @@ struct sdv2_handle {
   float* u;                   // patchified tokens [Mmax, 4C] fp32
   float* yh;                  // head output [Mmax, 4C] fp32
   float* attn_part;           // stream-K attention partials
-  float* rowsq;               // [Mmax] sum of squares of the raw cross q rows (fused q RMS)
+  float* rowsq;               // [Mmax][d / 32] partial sums of squares of the raw cross q rows (fused q RMS)
   int* attn_flags;            // [kMaxSMs] split-unit hand-off flags (zero between launches)
   void* head_w_tw;            // head weight [4C, d] TW
   float* t1;                  // [B n, d]
@@ -156,6 +156,7 @@ struct sdv2_handle {
   TickDesc* td_host_cur = nullptr;
   // CUDA graphs of the call body, keyed by (active entries, call parity)
   bool graphs = true;
+  bool debug_sync = false;   // test hook: synchronise + log after every launch (graphs off)
   bool pdl = true;        // programmatic dependent launch (sdv2_exec_options.pdl): +2 % fps measured
   bool tune = true;       // create-time GEMM tile tuning (sdv2_exec_options.tune_gemms)
   bool l2_persist = true;    // sdv2_exec_options.l2_persist
@@ -285,7 +286,7 @@ size_t carve(sdv2_handle* h, void* base) {
   h->u = cv.take<float>(size_t(h->Mmax) * h->P);
   h->yh = cv.take<float>(size_t(h->Mmax) * h->P);
   h->attn_part = cv.take<float>(attn_scratch_floats(kMaxSMs, h->hd));
-  h->rowsq = cv.take<float>(h->Mmax);
+  h->rowsq = cv.take<float>(size_t(h->Mmax) * (h->d / 32));
   h->attn_flags = cv.take<int>(kMaxSMs);
   h->t1 = cv.take<float>(size_t(h->NE) * d);
   // activation scratch, aliased by the weight staging buffer during create
@@ -406,7 +407,17 @@ sdv2_status fill_dims(sdv2_handle* h, const sdv2_model_desc* md, const sdv2_geom
       h->err = std::string("launch: ") + cudaGetErrorString(e_);              \
       return SDV2_E_CUDA;                                                     \
     }                                                                         \
+    debug_sync_point(h, __LINE__);                                            \
   } while (0)
+
+// Test hook (sdv2_debug_sync): every launch is followed by a stream synchronisation and a
+// line on stderr, so a kernel that never completes is named by the last line printed.
+inline void debug_sync_point(sdv2_handle* h, int line) {
+  if (!h->debug_sync) return;
+  fprintf(stderr, "sdv2 launch @%d\n", line);
+  fflush(stderr);
+  cudaStreamSynchronize(h->stream);
+}
 
 __global__ void mul_vec_kernel(const float* __restrict__ a, const float* __restrict__ b, float* __restrict__ out, int n) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = a[i] * b[i];
@@ -459,6 +470,7 @@ sdv2_status gemm_act(sdv2_handle* h, const void* A, const void* W, int M, int N,
     gemm_pdl_flag() = h->pdl;
     const bool ok = tc_gemm(h->stream, h->gplan, A, W, M, N, K, epi, ep, &h->err);
     gemm_pdl_flag() = false;
+    debug_sync_point(h, __LINE__ * 1000 + epi);
     return ok ? SDV2_OK : SDV2_E_CUDA;
   }
   return gemm_simt<bf16, bf16, bf16>(h, static_cast<const bf16*>(A), static_cast<const bf16*>(W), M, N, K, K, epi, ep);
@@ -491,10 +503,13 @@ sdv2_status attention(sdv2_handle* h, const AttnArgs& aa, int Mrows_entries, dou
       xa.o = aa.o;
       xa.ldo = aa.ldo;
       xa.rowsq = h->rowsq;
+      xa.nparts = h->d / 32;
       xa.inv_d = 1.f / float(h->d);
       xa.eps = h->md.eps;
-      return tc_cross_attention(h->stream, h->aplan, aa.q, h->Mmax, h->Kx, h->Vx, 2LL * h->B * h->nb * h->Lt, h->d,
-                                h->hd, xa, h->td_dev, &h->err, h->pdl) ? SDV2_OK : SDV2_E_CUDA;
+      const bool okx = tc_cross_attention(h->stream, h->aplan, aa.q, h->Mmax, h->Kx, h->Vx, 2LL * h->B * h->nb * h->Lt,
+                                          h->d, h->hd, xa, h->td_dev, &h->err, h->pdl);
+      debug_sync_point(h, __LINE__);
+      return okx ? SDV2_OK : SDV2_E_CUDA;
     }
     if (tc_attn_enabled()) {
       ++h->launches;
@@ -534,8 +549,13 @@ sdv2_status attention(sdv2_handle* h, const AttnArgs& aa, int Mrows_entries, dou
         ta.kv_row0 = bl * h->NE * h->S * h->L;
         ta.kv_lane_rows = h->S * h->L;
       }
-      return tc_attention(h->stream, h->aplan, aa.q, h->Mmax, Kb, Vb, kv_rows, h->d, h->hd, tiles, ta, h->td_dev,
-                          &h->err, h->pdl) ? SDV2_OK : SDV2_E_CUDA;
+      const bool oka = tc_attention(h->stream, h->aplan, aa.q, h->Mmax, Kb, Vb, kv_rows, h->d, h->hd, tiles, ta,
+                                    h->td_dev, &h->err, h->pdl);
+      if (h->debug_sync)
+        fprintf(stderr, "sdv2 self-attn block %d per_unit %d tiles %lld units %d\n", bl, ta.per_unit, tiles,
+                Mrows_entries * ta.H * ta.QT);
+      debug_sync_point(h, __LINE__);
+      return oka ? SDV2_OK : SDV2_E_CUDA;
     }
     if (h->hd == 64) attn_simt_kernel<bf16, 64><<<grid, 128, 0, h->stream>>>(aa, h->td_dev);
     else attn_simt_kernel<bf16, 128><<<grid, 128, 0, h->stream>>>(aa, h->td_dev);
@@ -642,7 +662,7 @@ sdv2_status run_block(sdv2_handle* h, int bl, int rows, int n_act) {
   // 6. cross-attention: affine norm3, q projection, RMS q (fused on the bf16 path: the
   //    GEMM epilogue sums q^2 per row, the cross kernel scales the scores, K carries g_cq)
   const bool fused = fused_cross_rms(h);
-  TRY(launch_norm<TA>(h, rows, 1, nullptr, 0, 0, B.n3g, B.n3b, fused ? h->rowsq : nullptr));
+  TRY(launch_norm<TA>(h, rows, 1, nullptr, 0, 0, B.n3g, B.n3b));
   ep.out = h->q; ep.ldo = d; ep.bias = B.bcq; ep.rowsq = h->rowsq;
   TRY(gemm_act(h, h->a, B.wcq, rows, d, d, fused ? EPI_STORE_RSQ : EPI_STORE, ep));
   if (!fused) {
@@ -837,7 +857,7 @@ sdv2_status tick(sdv2_handle* h, const float* chunk_latent, float* out_latent, i
                                                                 h->S, h->m, h->W, h->L, h->d, h->hd, h->T_reset);
     CKL();
   }
-  const bool use_graph = h->graphs && !h->prof && !h->tap && h->stream != nullptr;
+  const bool use_graph = h->graphs && !h->prof && !h->tap && !h->debug_sync && h->stream != nullptr;
   if (use_graph) {
     const int key = na * 2 + par;
     if (!h->graph_exec[key]) {
@@ -1261,6 +1281,12 @@ sdv2_status sdv2_kv_lane(sdv2_handle* h, int32_t local_block, int32_t lane, int3
   char* base = static_cast<char*>(which ? h->Vc : h->Kc);
   *ptr = base + ((size_t(local_block) * h->NE + lane) * per_lane) * h->ta;
   *elems = per_lane;
+  return SDV2_OK;
+}
+
+sdv2_status sdv2_debug_sync(sdv2_handle* h, int32_t enable) {
+  if (!h) return SDV2_E_INVALID;
+  h->debug_sync = enable != 0;
   return SDV2_OK;
 }
 

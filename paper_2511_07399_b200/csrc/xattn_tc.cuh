@@ -47,7 +47,8 @@ struct XattnArgs {
   // Fused cross-q RMS (C.5 step 6, q_c = g_cq RMS_d(q)): when rowsq != nullptr, q holds the
   // raw projection, rowsq[row] its sum of squares over d, and the prompt K the gain-folded
   // K_c * g_cq; scores of row r are scaled by rsqrt(rowsq[r] / d + eps).
-  const float* rowsq;
+  const float* rowsq;   // [rows][nparts] partial sums of squares (d / 32 per row)
+  int nparts;
   float inv_d, eps;
 };
 
@@ -230,7 +231,17 @@ __global__ void __launch_bounds__(kXattnThreads, 1) xattn_tc_kernel(const __grid
       // per-row softmax scale (the fused q RMS factor, 1 without the fusion)
       const int qrow = qt * kAttnBQ + row;
       float rscale = a.scale_log2;
-      if (a.rowsq) rscale *= rsqrtf(a.rowsq[e * a.L + (qrow < a.L ? qrow : a.L - 1)] * a.inv_d + a.eps);
+      if (a.rowsq) {   // sum the row's per-32-column partials in column order (deterministic)
+        // nparts = d / 32 is a multiple of 4: independent 16-byte loads, fixed summation order
+        const float4* rp = reinterpret_cast<const float4*>(a.rowsq + size_t(e * a.L + (qrow < a.L ? qrow : a.L - 1)) * a.nparts);
+        float ssq = 0.f;
+#pragma unroll 8
+        for (int i = 0; i < a.nparts / 4; ++i) {
+          const float4 v4 = __ldg(rp + i);
+          ssq += (v4.x + v4.y) + (v4.z + v4.w);
+        }
+        rscale *= rsqrtf(ssq * a.inv_d + a.eps);
+      }
       const uint64_t sc2 = f2pack(rscale, rscale);
       // ---- max pass (S_0 kept in registers when slot 0 is needed for S_3)
       float s0[HC];

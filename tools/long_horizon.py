@@ -26,6 +26,7 @@ def main():
     out = sys.argv[1]
     cfg = sg.CONFIGS["long_horizon"]
     N = int(sys.argv[2]) if len(sys.argv) > 2 else cfg.num_chunks
+    debug = os.environ.get("LH_DEBUG") == "1"     # sync + print every call from 2990 on
     md, g, sd = cfg.model, cfg.geom, cfg.stream
     n = g.steps
     W = gen_weights_parallel(md)
@@ -59,7 +60,13 @@ def main():
     start = torch.cuda.Event(enable_timing=True)
     start.record(stage.stream)
     for c in range(N + n - 1):
-        if c % 1000 == 0:
+        if debug and c == 3130:
+            import ctypes
+            stage.L.sdv2_debug_sync.argtypes = [ctypes.c_void_p, ctypes.c_int32]
+            stage.L.sdv2_debug_sync(stage.h, 1)
+        if c % 1000 == 0 or (debug and c >= 2990):
+            if debug:
+                torch.cuda.synchronize()
             print(f"call {c} t={time.time() - t0:.1f}s", file=sys.stderr, flush=True)
         if c in cfg.prompt_switch:
             stage.set_prompt(prompts[pidx[c]])
