@@ -378,46 +378,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
           }
         }
       }
-      if (kResTMA && x_late) {
-        // The x tile overlays the operand ring (x_late: one tile per cluster).  Fetch each
-        // 32-column box as soon as the ring stages under its bytes are released by the last
-        // MMAs, so the fetch overlaps the tail of the mainloop instead of following it.
-        GemmSegIter it1 = segs;
-        GemmSeg g1;
-        if (it1.next(g1)) {
-          const int mb = (g1.t % num_mg) * MC + cr, nb = g1.t / num_mg;
-          const int nbox = BN / 32;
-          uint32_t freed = 0, issued = 0;
-          auto stage_of = [&](int off) {   // ring stage owning smem byte `off`
-            return off < kStages * kGemmSmemA ? off / kGemmSmemA : (off - kStages * kGemmSmemA) / kSmemB;
-          };
-          for (int q = 0; q < kStages; ++q) {
-            tc::mbar_wait(empty + stage, phase ^ 1);
-            freed |= 1u << stage;
-            // every lane takes the same decisions (freed is warp-uniform); one lane issues
-            uint32_t now = 0;
-            for (int i = 0; i < nbox; ++i) {
-              if ((issued >> i) & 1) continue;
-              const int lo = i * (kGemmBM * 128), hi = lo + kGemmBM * 128 - 1;
-              bool ok = true;
-              for (int st = stage_of(lo); st <= stage_of(hi) && ok; ++st) ok = (freed >> st) & 1;
-              if (ok) now |= 1u << i;
-            }
-            if (now && tc::elect_one()) {
-              if (issued == 0) tc::mbar_expect_tx(x_full, uint32_t(BN) * kGemmBM * 4);
-              for (int i = 0; i < nbox; ++i)
-                if ((now >> i) & 1)
-                  tc::tma_load_2d(sX + i * (kGemmBM * 128), &tmX, x_full, nb * BN + i * 32, mb * kGemmBM);
-            }
-            issued |= now;
-            __syncwarp();
-            if (++stage == kStages) {
-              stage = 0;
-              phase ^= 1;
-            }
-          }
-        }
-      }
     }
   } else if (warp == 1) {
     if (cr == 0) {   // whole warp walks the loop; one elected lane issues (see tc::elect_one)
@@ -527,6 +487,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
       tc::tc_fence_after();
       const int r = mb * kGemmBM + row;
       const float* gsm = sGate + ((r < M ? r : M - 1) / ep.L > e_lo ? kGemmMaxBN : 0);
+      if (kResTMA && x_late && !partial && leader) {   // last MMA done: the operand ring is free
+        // (fetching each box earlier, as the last MMAs release the ring stages, measured
+        // 1.3 % slower on the step: the x boxes then compete with the last operand loads)
+        tc::mbar_expect_tx(x_full, uint32_t(BN) * kGemmBM * 4);
+        for (int c = 0; c < BN; c += 32)
+          tc::tma_load_2d(sX + (c / 32) * (kGemmBM * 128), &tmX, x_full, nb * BN + c, mb * kGemmBM);
+      }
       if (kResTMA && !partial) tc::mbar_wait(x_full, (nx++) & 1);
       const uint32_t tbase = tmem + (uint32_t(q * 32) << 16) + uint32_t(acc * BN);
       auto chunk = [&](const uint32_t(&v0)[32], int c) {

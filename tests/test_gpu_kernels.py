@@ -150,3 +150,35 @@ def test_gemm_configs_bitwise_identical(M, N, K, epi):
             assert ((out.float() - exp).norm() / exp.norm()).item() < 8e-3
         else:
             assert torch.equal(out, ref), (c, cands[0])
+
+
+@pytest.mark.gpu
+def test_attention_rescale_rows_disagree():
+    """Regression: rows of one softmax warp whose running max grows by more than 2^8 at
+    different key tiles (odd rows find a dominant key in tile 3, even rows never do).  The
+    lazy O rescale touches TMEM with warp-synchronous instructions, so its decision must be
+    warp-uniform; a per-row branch hung here.  Must finish and match SDPA."""
+    import torch
+    L_ = lib()
+    L_.sdv2_debug_attention.argtypes = [P, P, P, P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                        P, P]
+    L_.sdv2_debug_attention.restype = ctypes.c_int
+    torch.manual_seed(7)
+    Lq, Lk, H, hd = 256, 1024, 2, 128
+    k = torch.randn(Lk, H * hd, device="cuda")
+    v = torch.randn(Lk, H * hd, device="cuda")
+    q = 0.1 * torch.randn(Lq, H * hd, device="cuda")
+    q[1::2] = 4.0 * k[400]                       # odd rows: a dominant key in key tile 3
+    q, k, v = q.bfloat16(), k.bfloat16(), v.bfloat16()
+    o = torch.zeros(Lq, H * hd, device="cuda", dtype=torch.bfloat16)
+    scratch = torch.zeros(4096, dtype=torch.uint8, device="cuda")
+    st = L_.sdv2_debug_attention(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), Lq, Lk, H, hd,
+                                 scratch.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    assert st == 0
+    torch.cuda.synchronize()
+    qh = q.float().view(Lq, H, hd).transpose(0, 1)
+    kh = k.float().view(Lk, H, hd).transpose(0, 1)
+    vh = v.float().view(Lk, H, hd).transpose(0, 1)
+    ref = torch.nn.functional.scaled_dot_product_attention(qh, kh, vh).transpose(0, 1).reshape(Lq, H * hd)
+    err = (o.float() - ref).norm() / ref.norm()
+    assert err < 1.5e-2, err
