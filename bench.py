@@ -365,6 +365,49 @@ def run_ours(args, cfg):
                         "max": float(lats[-1]), "chunks": len(lats),
                         "definition": "host CLOCK_MONOTONIC, submit of chunk X -> completion of output X; "
                                       "each call submitted when the previous one completed"}
+    # ---- whole pipeline with the Stream-VAE stand-in (DiT FPS above
+    # excludes it, reading Q23): video chunk (4 frames, 8x the latent size) -> encode ->
+    # DiT call -> decode of the emitted chunk, all on the stage's stream, device-timed
+    with_vae = None
+    if args.vae and Bs == 1:
+        from paper_2511_07399_b200.sdv2 import StreamVAE
+        vd = sg.VAE
+        H8, W8 = 8 * g.latent_h, 8 * g.latent_w
+        vae = StreamVAE(vd, H8, W8, sg.gen_vae_weights(vd), stream=stream)
+        vae.reset()
+        vids = [torch.from_numpy(np.ascontiguousarray(sg.gen_video(vd, 4, H8, W8, seed=7 + i))).cuda() for i in range(4)]
+        lat_in = torch.empty(host_chunks[0].shape, dtype=torch.float32, device="cuda")
+        vid_out = torch.empty((3, 4, H8, W8), dtype=torch.float32, device="cuda")
+        nv = max(8, min(args.steps, 40))
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3 * nv + 1)]
+        for i in range(3):                          # warm-up (first calls pay the caches' zeros)
+            vae.encode_chunk(vids[i % 4].data_ptr(), lat_in.data_ptr())
+            stage.denoise_chunk(lat_in.data_ptr(), out_dev.data_ptr())
+            vae.decode_chunk(out_dev.data_ptr(), vid_out.data_ptr())
+        c += 3
+        torch.cuda.synchronize()
+        ev[0].record(stream)
+        for i in range(nv):
+            vae.encode_chunk(vids[i % 4].data_ptr(), lat_in.data_ptr())
+            ev[3 * i + 1].record(stream)
+            oc = stage.denoise_chunk(lat_in.data_ptr(), out_dev.data_ptr())
+            ev[3 * i + 2].record(stream)
+            if oc >= 0:
+                vae.decode_chunk(out_dev.data_ptr(), vid_out.data_ptr())
+            ev[3 * i + 3].record(stream)
+        torch.cuda.synchronize()
+        c += nv
+        enc = [ev[3 * i].elapsed_time(ev[3 * i + 1]) for i in range(nv)]
+        dit = [ev[3 * i + 1].elapsed_time(ev[3 * i + 2]) for i in range(nv)]
+        dec = [ev[3 * i + 2].elapsed_time(ev[3 * i + 3]) for i in range(nv)]
+        tot = ev[0].elapsed_time(ev[-1])
+        with_vae = {"video_fps": 4 * nv / (tot / 1e3), "video": [3, 4, H8, W8], "ms_per_chunk": tot / nv,
+                    "encode_ms": float(np.median(enc)), "dit_ms": float(np.median(dit)),
+                    "decode_ms": float(np.median(dec)),
+                    "vae_share": (sum(enc) + sum(dec)) / tot,
+                    "note": "Stream-VAE stand-in (Wan-VAE channel shapes) on the same stream; the paper "
+                            "reports the VAE at ~30 % of the time (P:301)"}
+        vae.close()
     # ---- per-kernel-class device time (events around each launch), same workload
     prof_steps = min(args.steps, 50)
     stage.profile_enable(True)
@@ -427,6 +470,7 @@ def run_ours(args, cfg):
         "roofline": roofline,
         "cpu_baseline": cpu,
         "clocks": clocks,
+        "with_vae": with_vae,
         "weight_gen_s": t_gen,
     }
     print(json.dumps(res))
@@ -443,6 +487,8 @@ def main():
     ap.add_argument("--pp-backend", default="nccl", choices=["nccl", "gloo"],
                     help="stage transport for --gpus > 1 (gloo: host staging, several ranks on one GPU)")
     ap.add_argument("--lib", default=None, help="alternative libsdv2.so build (A/B timing)")
+    ap.add_argument("--vae", action="store_true",
+                    help="also time video -> Stream-VAE encode -> DiT -> decode -> video (with_vae)")
     ap.add_argument("--no-l2-persist", dest="l2_persist", action="store_false",
                     help="no persisting-L2 window on the residual stream (A/B)")
     ap.add_argument("--window", type=int, default=0, help="override W (rolling-window chunks)")

@@ -388,6 +388,32 @@ def run_pipeline_bench(args, cfg):
     prof = stage.profile_read()
     stage.profile_enable(False)
     ext = prof["stage_extras"]["ms"] / ncal
+    # Stream-VAE stand-in on the first / last stage ("the first and last ranks handle
+    # VAE encoding and decoding in addition to DiT blocks"): its measured time joins the
+    # stage extras the partition balances
+    vae = None
+    if getattr(args, "vae", False) and rank in (0, world - 1):
+        from .sdv2 import StreamVAE
+        vd = sg.VAE
+        H8, W8 = 8 * g.latent_h, 8 * g.latent_w
+        vae_w = sg.gen_vae_weights(vd)
+        vae = StreamVAE(vd, H8, W8, vae_w, device=dev_index, stream=stage.stream)
+        vae.reset()
+        vae_vid = torch.from_numpy(np.ascontiguousarray(sg.gen_video(vd, 4, H8, W8))).to(f"cuda:{dev_index}")
+        vae_lat = torch.empty(tuple(dev_chunks[0].shape), dtype=torch.float32, device=f"cuda:{dev_index}")
+        vae_lat.zero_()
+        vae_out = torch.empty((3, 4, H8, W8), dtype=torch.float32, device=f"cuda:{dev_index}")
+        a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for i in range(4):
+            if i == 1:
+                a_.record(stage.stream)
+            if rank == 0:
+                vae.encode_chunk(vae_vid.data_ptr(), vae_lat.data_ptr())
+            if rank == world - 1:
+                vae.decode_chunk(vae_lat.data_ptr(), vae_out.data_ptr())
+        b_.record(stage.stream)
+        torch.cuda.synchronize(dev_index)
+        ext += a_.elapsed_time(b_) / 3
     r0 = stage.resident[0]
     mine = [0.0] * md.num_blocks
     for i, v in enumerate(blk_res):
@@ -418,6 +444,11 @@ def run_pipeline_bench(args, cfg):
     tr = StageTransport(rank, world, stage_io_tensors(stage, stage.workspace), host_staging=host_staging,
                         device=dev_index)
     stream = stage.stream
+    if vae is not None and vae.stream is not stream:     # stage re-created: the VAE follows its stream
+        vae.close()
+        vae = StreamVAE(vd, H8, W8, vae_w, device=dev_index, stream=stream)
+    if vae is not None:
+        vae.reset()
     dist.barrier()
 
     # ---- phases, each a drained run bracketed by sync + barrier:
@@ -457,8 +488,18 @@ def run_pipeline_bench(args, cfg):
     l0 = stage.tick_info()["kernel_launches"]
     sync_barrier()
     ta = ev()
-    outs = run_pipelined(stage, tr, lambda c: ptr_in(base + c), dev_out, args.steps,
-                         after_call=lambda c, oc: step_ev.append(ev()))
+    def vae_in(c):           # rank 0: encode the chunk's 4 video frames into the latent it admits
+        if vae is not None and rank == 0:
+            vae.encode_chunk(vae_vid.data_ptr(), vae_lat.data_ptr())
+
+    def vae_out_cb(c, oc):    # last rank: decode the emitted clean latent
+        if vae is not None and rank == world - 1 and oc >= 0:
+            vae.decode_chunk(out_dev.data_ptr(), vae_out.data_ptr())
+        step_ev.append(ev())
+
+    outs = run_pipelined(stage, tr, (lambda c: vae_lat.data_ptr()) if (vae is not None and rank == 0)
+                         else (lambda c: ptr_in(base + c)), dev_out, args.steps,
+                         on_call=vae_in, after_call=vae_out_cb)
     tb = ev()
     sync_barrier()
     clocks = clk.stop()
@@ -540,6 +581,7 @@ def run_pipeline_bench(args, cfg):
                        "window_chunks": g.window_chunks, "blocks": md.num_blocks, "dim": md.dim,
                        "parallelism": f"pp{world}", "transport": backend, "block_ranges": ranges,
                        "balance": balance, "px_frames_per_chunk": px,
+                       "stream_vae": bool(getattr(args, "vae", False)),
                        "l2": "per-step working set >> L2 (stage weights + KV lanes streamed each step)"},
             "latent_chunks_per_s": last[3] / (max_ms / 1e3),
             "steady_state": {"tick_ms_median": float(np.median(tick)) if tick else None,
@@ -569,6 +611,8 @@ def run_pipeline_bench(args, cfg):
         }
         del gm
         print(json.dumps(res))
+    if vae is not None:
+        vae.close()
     stage.close()
     dist.barrier()
     dist.destroy_process_group()
