@@ -36,6 +36,9 @@ __device__ __forceinline__ bool elect_one() {
 // mode 15 / 16: mode 8 / 9 issued by the whole converged warp through elect.sync
 // mode 17: mode 15 with one elect.sync around the 8 MMAs (not one per MMA)
 // mode 18: mode 17 with N = 64
+// mode 19: mode 17 with 8 TS MMAs (A = P from TMEM, N = 128: the attention PV step)
+// mode 20: mode 17 with 8 SS (S into columns 0..127) then 8 TS (O += P V, P read from
+//          columns 0..63): the attention's S / PV alternation, 16 MMAs per iteration
 __global__ void __launch_bounds__(160, 1) ubench(int mode, long long* out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -61,15 +64,23 @@ __global__ void __launch_bounds__(160, 1) ubench(int mode, long long* out) {
   const uint32_t idS = tc::idesc_bf16(128, NN);
   const uint32_t idO = tc::idesc_bf16(128, 128, true);
   long long t0 = clock64();
-  if (warp == 4 && (mode == 17 || mode == 18)) {
+  if (warp == 4 && (mode == 17 || mode == 18 || mode == 19 || mode == 20)) {
     const uint32_t qa = tc::smem_u32(sA), ka = tc::smem_u32(sB);
     for (int it = 0; it < kIters; ++it) {
       if (elect_one()) {
+        if (mode != 19) {
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const uint32_t off = (k >> 2) * (128 * 128) + (k & 3) * 32;
-          const uint32_t koff = (k >> 2) * (NN * 128) + (k & 3) * 32;
-          tc::mma_bf16(tmem, tc::sw128_kmajor_desc(qa + off), tc::sw128_kmajor_desc(ka + koff), idS, k > 0);
+          for (int k = 0; k < 8; ++k) {
+            const uint32_t off = (k >> 2) * (128 * 128) + (k & 3) * 32;
+            const uint32_t koff = (k >> 2) * (NN * 128) + (k & 3) * 32;
+            tc::mma_bf16(tmem, tc::sw128_kmajor_desc(qa + off), tc::sw128_kmajor_desc(ka + koff), idS, k > 0);
+          }
+        }
+        if (mode >= 19) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            tc::mma_bf16_ts(tmem + 256, tmem + (k >> 2) * 64 + (k & 3) * 8, tc::sw128_mnmajor_desc(ka + k * 2048, 128 * 128),
+                            idO, (it | k) > 0);
         }
       }
       __syncwarp();
@@ -179,8 +190,9 @@ int main(int argc, char** argv) {
                          "8 SS MMA N=64, no commits", "8 SS MMA N=192, no commits",
                          "8 SS MMA N=128, 2 accumulators", "8 SS MMA N=128, 4 accumulators",
                          "8 SS MMA N=256, 2 accumulators", "8 SS MMA N=128, warp + elect",
-                         "8 SS MMA N=256, warp + elect", "8 SS MMA N=128, one elect", "8 SS MMA N=64, one elect"};
-  for (int mode = 0; mode < 19; ++mode) {
+                         "8 SS MMA N=256, warp + elect", "8 SS MMA N=128, one elect", "8 SS MMA N=64, one elect",
+                         "8 TS MMA N=128, one elect", "8 SS + 8 TS (S, PV), one elect"};
+  for (int mode = 0; mode < 21; ++mode) {
     for (int rep = 0; rep < 2; ++rep) ubench<<<grid, 160, smem>>>(mode, d);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
