@@ -155,6 +155,20 @@ class LaneCache:
                 self.window.pop(0)
                 self.evictions += 1
 
+    def overwrite(self, act: dict, k, v):
+        """Clean-context re-run (reading Q5-clean, N4): chunk act["X"]'s K/V are replaced
+        in place -- its sink fill, or its window entry and the sinks it refreshed -- with
+        tags, positions and slots unchanged (no admission, no eviction, no re-base)."""
+        X = act["X"]
+        if act["sink_fill"] >= 0:
+            targets = [self.sinks[act["sink_fill"]]]
+        else:
+            targets = [self.sinks[i] for i, r in enumerate(act["refresh"]) if r] + [self.window[-1]]
+        for e in targets:
+            if e is None or e.tag != X:
+                raise ValueError(f"clean re-run of chunk {X}: cache entry is not chunk {X}")
+            e.k, e.v = k, v
+
     def attended(self) -> List[CacheEntry]:
         """[sinks || window] in temporal order, current chunk included."""
         return [s for s in self.sinks if s is not None] + list(self.window)

@@ -8,6 +8,11 @@ lane's explicit [sink || window] list, flow-matching x0 prediction, re-noise
 (O5).  By O6 any order that respects (X, j-1) -> (X, j) and per-lane chunk
 order yields the same per-entry math; this sequential order is the reference
 for the stream-batched and pipelined GPU executions.
+
+kv_mode 1 (reading Q5-clean; n = 1 only): before chunk X is admitted, the
+finished chunk X-1 is re-run through the DiT on its prediction x0 at sigma = 0 (t = 0,
+CausVid's clean-context pass, EXT) and the K/V of that pass replace its step-0 K/V in the
+cache (LaneCache.overwrite): later chunks attend to clean K/V of earlier chunks.
 """
 from __future__ import annotations
 
@@ -31,6 +36,9 @@ class StreamOracle:
         self.lanes = {(b, j): LaneCache(geom.sink_chunks, geom.window_chunks, sd.rope_reset_frames)
                       for b in self.blocks for j in range(geom.steps)}
         self.tap = tap
+        self.clean = getattr(geom, "kv_mode", 0) == 1
+        if self.clean and geom.steps != 1:
+            raise ValueError("the clean re-run (kv_mode 1) is defined for n = 1")
         self.prompt = None
         self.ctx_kv = None
         self.h = None
@@ -54,7 +62,7 @@ class StreamOracle:
         return act
 
     # ------------------------------------------------------------- one block
-    def block(self, x, e0, b, lane: LaneCache, act):
+    def block(self, x, e0, b, lane: LaneCache, act, rerun: bool = False):
         md, dt, W = self.md, self.dt, self.W
         p = f"blocks.{b}."
         w = lambda n: W[p + n].astype(dt)
@@ -68,7 +76,10 @@ class StreamOracle:
         k = M.rms_g(M.linear(a, w("wk"), w("bk")), w("gk"), md.eps)
         v = M.linear(a, w("wv"), w("bv"))
         # 4. cache update (re-base, write/refresh) then attention over all valid entries
-        lane.apply(act, k, v, self.g.chunk_frames)
+        if rerun:
+            lane.overwrite(act, k, v)
+        else:
+            lane.apply(act, k, v, self.g.chunk_frames)
         pt_q, ph_q, pw_q = M.token_positions(md, self.g, act["pos"])
         R = x.shape[0]          # a chunk, or a row prefix of one (bench sample only)
         phi_q = M.rope_angles(hd, pt_q[:R], ph_q[:R], pw_q[:R])
@@ -117,12 +128,26 @@ class StreamOracle:
         C, T, h, w_ = x_lat.shape
         return M.unpatchify(y, md, T, h, w_)
 
+    def clean_rerun(self, rec: dict):
+        """Re-run finished chunk rec["X"] on its prediction x0 at sigma = 0 (t = 0), with the
+        control record it was admitted with; its K/V replace its step-0 K/V in every block's
+        lane (Q5-clean).  The head is not evaluated (the pass only writes the cache)."""
+        md, dt, W = self.md, self.dt, self.W
+        act = rec["act"]
+        u = M.patchify(rec["out"].astype(dt), md)
+        x = M.linear(u, W["patch_w"].astype(dt), W["patch_b"].astype(dt))
+        _, e0 = M.time_embed(np.float32(0.0), W, md, dt)
+        for b in self.blocks:
+            x = self.block(x, e0, b, self.lanes[(b, 0)], act, rerun=True)
+
     # ------------------------------------------------------------- one chunk
     def step_chunk(self, X: int, v_X, prompt=None) -> dict:
         """Admit chunk X, run its n entries sequentially; returns output x0 and records."""
         if prompt is not None:
             self.set_prompt(prompt)
         dt, sd, g = self.dt, self.sd, self.g
+        if self.clean and self.records:
+            self.clean_rerun(self.records[-1])
         mot = self.motion.admit(v_X)
         act = self.admit_control(X)
         sig = mot["sigmas"]

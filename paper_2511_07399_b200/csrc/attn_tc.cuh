@@ -137,6 +137,12 @@ __device__ __forceinline__ float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// Three-input max (sm_100 FMNMX3): the row-max pass in one instruction per two scores.
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
 // Packed fp32x2 arithmetic (sm_100 FFMA2 / FADD2): two softmax elements per instruction.
 __device__ __forceinline__ uint64_t f2pack(float a, float b) {
   uint64_t r;
@@ -601,7 +607,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const __grid_c
   #pragma unroll
           for (int i = 0; i < HC; i += 8) {
   #pragma unroll
-            for (int k = 0; k < 4; ++k) mq[k] = fmaxf(mq[k], fmaxf(sv[i + 2 * k], sv[i + 2 * k + 1]));
+            for (int k = 0; k < 4; ++k) mq[k] = fmax3(mq[k], sv[i + 2 * k], sv[i + 2 * k + 1]);
           }
           float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3])) * a.scale_log2;
           // row max over both key halves (both warps then take the same rescale decision)

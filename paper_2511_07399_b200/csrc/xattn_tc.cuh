@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(kXattnThreads, 1) xattn_tc_kernel(const __grid
 #pragma unroll
         for (int i = 0; i < HC; i += 8) {
 #pragma unroll
-          for (int k = 0; k < 4; ++k) mq[k] = fmaxf(mq[k], fmaxf(sv[i + 2 * k], sv[i + 2 * k + 1]));
+          for (int k = 0; k < 4; ++k) mq[k] = fmax3(mq[k], sv[i + 2 * k], sv[i + 2 * k + 1]);
         }
         if (t == 0 && J == 4) {
 #pragma unroll

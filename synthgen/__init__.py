@@ -56,6 +56,7 @@ class Geometry:
     sink_chunks: int              # m
     window_chunks: int            # W
     streams: int = 1              # B: independent streams batched per call (SLO batch, N2)
+    kv_mode: int = 0              # 0: step-j K/V cached in lane j (R1); 1: clean re-run (Q5, N4; n = 1)
 
     def tokens_per_chunk(self, md: ModelDesc) -> int:
         return (self.chunk_frames // md.patch_t) * (self.latent_h // md.patch_h) * (self.latent_w // md.patch_w)
