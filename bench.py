@@ -251,6 +251,10 @@ def run_ours(args, cfg):
             g = dataclasses.replace(g, steps=args.denoise_steps)
             sd = dataclasses.replace(sd, timesteps=sg.SCHEDULES[args.denoise_steps])
         cfg = dataclasses.replace(cfg, geom=g, stream=sd)
+    if args.kv_mode == "clean":   # clean-context re-run (reading Q5-clean; n = 1)
+        import dataclasses
+        g = dataclasses.replace(g, kv_mode=1)
+        cfg = dataclasses.replace(cfg, geom=g)
     Bs = args.streams
     if Bs > 1:     # SLO batch: Bs independent streams per call
         import dataclasses
@@ -439,11 +443,13 @@ def run_ours(args, cfg):
         cores = len(os.sched_getaffinity(0))
         nbl = 2
         tsec = oracle_entry_seconds(cfg, {k: v for k, v in W.items()}, list(range(nbl)))
-        per_chunk = tsec * (md.num_blocks / nbl) * n
+        passes = 2 if getattr(g, "kv_mode", 0) == 1 else 1   # clean re-run: a second DiT pass per chunk
+        per_chunk = tsec * (md.num_blocks / nbl) * n * passes
         cpu = {"value": chunk_frames_px(cfg) / per_chunk, "unit": "frames/s", "cores": cores, "kind": "oracle",
                "host": host_info(),
                "sample": (f"one steady-state entry (full m+W window) of {cfg.name} through {nbl} of "
                           f"{md.num_blocks} blocks, NumPy fp32 on {cores} cores; x{n} steps per clean chunk"
+                          + (" x2 (clean re-run pass)" if passes == 2 else "")
                           + (" (block-extrapolated)" if nbl < md.num_blocks else ""))}
     stage.close()
     res = {
@@ -454,7 +460,8 @@ def run_ours(args, cfg):
                    "tokens_per_chunk": g.tokens_per_chunk(md), "steps_n": n, "sink_chunks": g.sink_chunks,
                    "window_chunks": g.window_chunks, "blocks": md.num_blocks, "dim": md.dim,
                    "parallelism": "pp1", "l2": "per-step working set >> L2 (weights 2.8GB+ streamed each step)",
-                   "px_frames_per_chunk": chunk_frames_px(cfg), "streams": Bs},
+                   "px_frames_per_chunk": chunk_frames_px(cfg), "streams": Bs,
+                   "kv_mode": "clean_rerun" if getattr(g, "kv_mode", 0) == 1 else "step_lanes"},
         "latent_chunks_per_s": Bs * outs / (total_ms / 1e3),
         "per_stream_fps": chunk_frames_px(cfg) * outs / (total_ms / 1e3),
         "ttff_ms": ttff_ms,
@@ -497,6 +504,8 @@ def main():
                     help="override n (in-flight denoising steps = Stream Batch size)")
     ap.add_argument("--latency-chunks", type=int, default=1024,
                     help="chunks of the host-clock per-chunk latency phase (0: skip)")
+    ap.add_argument("--kv-mode", default="step", choices=["step", "clean"],
+                    help="KV cache contents: step-j K/V per lane (R1) or the clean-context re-run (N4, n = 1)")
     ap.add_argument("--streams", type=int, default=1,
                     help="independent streams batched per call (SLO batch B; value = all streams' frames/s)")
     args = ap.parse_args()

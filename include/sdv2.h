@@ -73,6 +73,15 @@ typedef struct {
   int32_t sink_chunks;          /* m >= 0 sink chunks (first chunks, refreshed by P:190) */
   int32_t window_chunks;        /* W >= 1 rolling-window chunks, current chunk included */
   int32_t streams;              /* B >= 1 streams per call; streams * steps <= 16 */
+  int32_t kv_mode;              /* what the KV lanes cache (SURVEY reading Q5):
+                                 *  0 = step-j K/V in lane j, written during the step (R1);
+                                 *  1 = clean-context re-run (Q5-clean, CausVid, EXT; N4):
+                                 *      each call first re-runs the previous call's finished
+                                 *      chunks through the DiT on their prediction x0 at
+                                 *      t = 0 and overwrites their cached K/V (sink fill /
+                                 *      window slot / refreshed sinks) before admitting the
+                                 *      new chunk.  Needs steps == 1 and a single stage
+                                 *      (SDV2_E_UNSUPPORTED otherwise); ~2x DiT work per call. */
 } sdv2_geometry;
 
 /* Pipeline stage of this handle.  world = K stages; this rank runs DiT
@@ -112,7 +121,7 @@ typedef struct {
   int32_t rope_reset_frames;    /* T_reset >= max(m, W) * T', T_reset + T' <= 4096 */
   int32_t motion_k;             /* window of k+1 motion values, 0 <= k <= 62 */
   float motion_sigma;           /* > 0 */
-  float s_min, s_max;           /* 0 <= s_min < s_max <= 1 */
+  float s_min, s_max;           /* 0 <= s_min <= s_max <= 1 (equal: a constant noise rate) */
   float ema_lambda;             /* in (0, 1] */
   float sink_tau;               /* in [-1, 1] */
   uint64_t seed;

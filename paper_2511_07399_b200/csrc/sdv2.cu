@@ -136,7 +136,15 @@ struct sdv2_handle {
   float* rope;                // tables
   RopeTabs rt;
   TickDesc* td_dev;
-  TickDesc* td_host = nullptr;   // pinned ring
+  TickDesc* td_host = nullptr;   // pinned ring: [kTdRing] call descriptors, then [kTdRing] clean-pass ones
+  // kv_mode 1 (clean re-run): the previous call's descriptor (its entries are re-run with
+  // rebase cleared), the device copy the clean pass reads, sigma = 0 per entry
+  TickDesc td_prev;
+  bool td_prev_valid = false;
+  TickDesc* td_clean_dev = nullptr;
+  float* sig_zero = nullptr;
+  cudaGraphExec_t clean_graph_exec[kMaxEntries + 1] = {};
+  int64_t clean_graph_launches[kMaxEntries + 1] = {};
   cudaEvent_t td_ev[kTdRing];
   bool td_ev_used[kTdRing];
   size_t ws_bytes;
@@ -319,6 +327,8 @@ size_t carve(sdv2_handle* h, void* base) {
   const size_t rope_elems = size_t(2 * kMaxTOff + 1) * h->ct * 2 + size_t(h->hn) * h->ch * 2 + size_t(h->wn) * h->cw * 2;
   h->rope = cv.take<float>(rope_elems);
   h->td_dev = cv.take<TickDesc>(1);
+  h->td_clean_dev = cv.take<TickDesc>(1);
+  h->sig_zero = cv.take<float>(kMaxEntries);
   return cv.off + 1024;
 }
 
@@ -343,6 +353,11 @@ sdv2_status fill_dims(sdv2_handle* h, const sdv2_model_desc* md, const sdv2_geom
   if (g->steps < 1 || g->steps > kMaxSteps) return SDV2_E_SHAPE;
   if (g->streams < 1 || g->streams * g->steps > kMaxEntries) { *why = "streams * steps must be in [1, 16]"; return SDV2_E_SHAPE; }
   if (g->sink_chunks + g->window_chunks > kMaxSlots || g->sink_chunks > 31) return SDV2_E_SHAPE;
+  if (g->kv_mode != 0 && g->kv_mode != 1) { *why = "kv_mode must be 0 or 1"; return SDV2_E_INVALID; }
+  if (g->kv_mode == 1 && (g->steps != 1 || (pp && pp->world > 1))) {
+    *why = "kv_mode 1 (clean re-run) needs steps == 1 and a single stage";
+    return SDV2_E_UNSUPPORTED;
+  }
   h->C = md->latent_channels; h->T = g->chunk_frames; h->hh = g->latent_h; h->ww = g->latent_w;
   h->hn = h->hh / 2; h->wn = h->ww / 2;
   h->L = h->T * h->hn * h->wn;
@@ -622,6 +637,21 @@ sdv2_status launch_norm(sdv2_handle* h, int rows, int mode, const float* mod, in
     if (s_ != SDV2_OK) return s_;     \
   } while (0)
 
+// Drop every captured call graph (call bodies and clean passes): they bake in stream
+// constants and the active block range.
+void drop_graphs(sdv2_handle* h) {
+  for (auto& g : h->graph_exec)
+    if (g) {
+      cudaGraphExecDestroy(g);
+      g = nullptr;
+    }
+  for (auto& g : h->clean_graph_exec)
+    if (g) {
+      cudaGraphExecDestroy(g);
+      g = nullptr;
+    }
+}
+
 template <typename TA>
 sdv2_status run_block(sdv2_handle* h, int bl, int rows, int n_act) {
   const BlockW& B = h->bw[bl];
@@ -823,12 +853,104 @@ sdv2_status tick_body(sdv2_handle* h, int na, int par) {
   return SDV2_OK;
 }
 
+// kv_mode 1 (clean-context re-run, reading Q5-clean, N4): the previous call's finished
+// chunks (its na entries, n = 1) go through the DiT again on their prediction x0 (still
+// in out_stage) at sigma = 0, with the descriptor they were admitted with (rebase
+// cleared: it was applied then).  qkv_post2 writes their K/V over the step-0 K/V in the
+// same slots (window slot or sink fill, plus the sinks the chunk refreshed) and the
+// attention reads the same prefix as then.  No head: the pass only rewrites the cache.
+template <typename TA>
+sdv2_status clean_body(sdv2_handle* h, int na) {
+  const int rows = na * h->L;
+  launch_k(h->pdl, patchify_kernel, dim3((rows * h->P + 255) / 256), dim3(256), 0, h->stream, h->out_stage, h->u, rows,
+           h->L, h->C, h->T, h->hh, h->ww);
+  CKL();
+  {
+    EpiArgs ep{};
+    ep.out = h->st.x; ep.ldo = h->d; ep.bias = h->gw[G_PATCH_B]; ep.L = h->L;
+    TRY((gemm_simt<float, float, float>(h, h->u, h->gw[G_PATCH_W], rows, h->d, h->P, h->P, EPI_STORE, ep)));
+  }
+  launch_k(h->pdl, sinusoid_kernel, dim3(na), dim3(128), 0, h->stream, h->sig_zero, h->emb, na, h->md.freq_dim);
+  CKL();
+  const int d = h->d;
+  auto gemvs = [&](auto nmax) {
+    constexpr int NM = decltype(nmax)::value;
+    launch_k(h->pdl, gemv2_kernel<float, NM>, dim3((d + 31) / 32), dim3(256), size_t(na) * h->md.freq_dim * 4, h->stream,
+             h->gw[G_T1_W], h->gw[G_T1_B], h->emb, h->t1, na, d, h->md.freq_dim, 0);
+    launch_k(h->pdl, gemv2_kernel<float, NM>, dim3((d + 31) / 32), dim3(256), size_t(na) * d * 4, h->stream,
+             h->gw[G_T2_W], h->gw[G_T2_B], h->t1, h->st.e, na, d, d, 1);
+    launch_k(h->pdl, gemv2_kernel<TA, NM>, dim3((6 * d + 31) / 32), dim3(256), size_t(na) * d * 4, h->stream,
+             static_cast<const TA*>(h->tp_w), h->gw[G_TP_B], h->st.e, h->st.e0, na, 6 * d, d, 1);
+  };
+  if (na <= 4) gemvs(std::integral_constant<int, 4>{});
+  else if (na <= 8) gemvs(std::integral_constant<int, 8>{});
+  else gemvs(std::integral_constant<int, 16>{});
+  h->launches += 2;
+  CKL();
+  for (int b = h->a0; b < h->a1; ++b) {
+    ProfScope ps(h, 4, 0.0, b);
+    TRY(run_block<TA>(h, b, rows, na));
+  }
+  return SDV2_OK;
+}
+
+// Runs clean_body on the previous call's entries (from a graph keyed by their count),
+// with the kernels reading the clean descriptor; the block tap stays off.
+template <typename TA>
+sdv2_status clean_pass(sdv2_handle* h, TickDesc* tdc) {
+  const int na = tdc->n_active;
+  TickDesc* const td_dev = h->td_dev;
+  TickDesc* const td_cur = h->td_host_cur;
+  float* const tap = h->tap;
+  h->td_dev = h->td_clean_dev;
+  h->td_host_cur = tdc;
+  h->tap = nullptr;
+  sdv2_status st = SDV2_OK;
+  const bool use_graph = h->graphs && !h->prof && !tap && !h->debug_sync && h->stream != nullptr;
+  if (use_graph) {
+    if (!h->clean_graph_exec[na]) {
+      const int64_t l0 = h->launches;
+      cudaError_t e = cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal);
+      if (e == cudaSuccess) {
+        st = clean_body<TA>(h, na);
+        cudaGraph_t g = nullptr;
+        e = cudaStreamEndCapture(h->stream, &g);
+        if (st == SDV2_OK && e == cudaSuccess) e = cudaGraphInstantiate(&h->clean_graph_exec[na], g, 0);
+        if (g) cudaGraphDestroy(g);
+      }
+      if (st == SDV2_OK && e != cudaSuccess) {
+        h->err = std::string("clean-pass graph: ") + cudaGetErrorString(e);
+        st = SDV2_E_CUDA;
+      }
+      h->clean_graph_launches[na] = h->launches - l0;
+      h->launches = l0;
+    }
+    if (st == SDV2_OK) {
+      if (cudaGraphLaunch(h->clean_graph_exec[na], h->stream) != cudaSuccess) st = SDV2_E_CUDA;
+      h->launches += h->clean_graph_launches[na];
+    }
+  } else {
+    st = clean_body<TA>(h, na);
+  }
+  h->td_dev = td_dev;
+  h->td_host_cur = td_cur;
+  h->tap = tap;
+  return st;
+}
+
 template <typename TA>
 sdv2_status tick(sdv2_handle* h, const float* chunk_latent, float* out_latent, int64_t* out_chunk) {
   const int64_t call = h->ctl.calls();
   const int slot = int(call % kTdRing);
   if (h->td_ev_used[slot]) CK(cudaEventSynchronize(h->td_ev[slot]));
   TickDesc* tdh = h->td_host + slot;
+  TickDesc* tdc = h->td_host + kTdRing + slot;   // kv_mode 1: the clean pass's descriptor
+  const bool clean = h->g.kv_mode == 1 && h->td_prev_valid && h->td_prev.n_active > 0;
+  if (clean) {
+    *tdc = h->td_prev;
+    for (int e = 0; e < kMaxEntries; ++e) tdc->e[e].rebase = 0;   // applied at admission
+    CK(cudaMemcpyAsync(h->td_clean_dev, tdc, sizeof(TickDesc), cudaMemcpyHostToDevice, h->stream));
+  }
   h->ctl.plan_call(tdh);
   h->td_host_cur = tdh;
   CK(cudaMemcpyAsync(h->td_dev, tdh, sizeof(TickDesc), cudaMemcpyHostToDevice, h->stream));
@@ -847,6 +969,12 @@ sdv2_status tick(sdv2_handle* h, const float* chunk_latent, float* out_latent, i
   if (out_chunk) *out_chunk = h->info.out_chunk;
 
   if (first) CK(cudaMemcpyAsync(h->lat_in, chunk_latent, size_t(h->B) * h->CTHW * 4, cudaMemcpyDefault, h->stream));
+  // clean re-run of the previous call's chunks, before this call's re-base / writes
+  if (clean) TRY(clean_pass<TA>(h, tdc));
+  if (h->g.kv_mode == 1) {
+    h->td_prev = *tdh;
+    h->td_prev_valid = true;
+  }
   // RoPE re-base (rare: once every T_reset frames) of every local block's ring slots of
   // the re-basing lanes, before any block of this call writes or attends (R3).
   bool any_rebase = false;
@@ -960,7 +1088,7 @@ sdv2_status sdv2_create(const sdv2_model_desc* md, const sdv2_geometry* g, const
     *out = h;   // keep the handle so the caller can read sdv2_last_error, then destroy
     return st;
   };
-  if (cudaHostAlloc(reinterpret_cast<void**>(&h->td_host), sizeof(TickDesc) * kTdRing, cudaHostAllocDefault) != cudaSuccess)
+  if (cudaHostAlloc(reinterpret_cast<void**>(&h->td_host), sizeof(TickDesc) * 2 * kTdRing, cudaHostAllocDefault) != cudaSuccess)
     return fail(SDV2_E_CUDA);
   for (int i = 0; i < kTdRing; ++i) {
     cudaEventCreateWithFlags(&h->td_ev[i], cudaEventDisableTiming);
@@ -1011,6 +1139,7 @@ sdv2_status sdv2_create(const sdv2_model_desc* md, const sdv2_geometry* g, const
   if (h->prec == SDV2_BF16) {
     if (!tc_gemm_plan(h->gplan, &h->err)) return fail(SDV2_E_CUDA);
     if (cudaMemsetAsync(h->attn_flags, 0, kMaxSMs * sizeof(int), h->stream) != cudaSuccess ||
+        cudaMemsetAsync(h->sig_zero, 0, kMaxEntries * sizeof(float), h->stream) != cudaSuccess ||
         !attn_plan_init(h->aplan, h->gplan.encode, std::min(h->gplan.num_sms, kMaxSMs), h->attn_flags) ||
         !xattn_plan_init()) {
       h->err = "attention plan initialisation failed";
@@ -1090,7 +1219,7 @@ sdv2_status sdv2_reset_stream(sdv2_handle* h, const sdv2_stream_desc* sd, const 
     if (!(sd->timesteps[j] > 0.f) || sd->timesteps[j] > 1000.f) return SDV2_E_INVALID;
     if (j > 0 && !(sd->timesteps[j] < sd->timesteps[j - 1])) return SDV2_E_INVALID;
   }
-  if (!(sd->s_min < sd->s_max) || sd->s_min < 0.f || sd->s_max > 1.f) return SDV2_E_INVALID;
+  if (!(sd->s_min <= sd->s_max) || sd->s_min < 0.f || sd->s_max > 1.f) return SDV2_E_INVALID;
   if (!(sd->ema_lambda > 0.f) || sd->ema_lambda > 1.f) return SDV2_E_INVALID;
   if (!(sd->motion_sigma > 0.f) || sd->motion_k < 0 || sd->motion_k >= 63) return SDV2_E_INVALID;
   if (sd->sink_tau < -1.f || sd->sink_tau > 1.f) return SDV2_E_INVALID;
@@ -1147,13 +1276,9 @@ sdv2_status sdv2_reset_stream(sdv2_handle* h, const sdv2_stream_desc* sd, const 
     CK(cudaStreamSynchronize(h->stream));   // the host table vector dies here
   }
   if (old_T_reset != h->T_reset || std::memcmp(&old_cfg, &h->scfg, sizeof(StreamCfg)) != 0 ||
-      std::memcmp(&old_rt, &h->rt, sizeof(RopeTabs)) != 0) {
-    for (auto& g : h->graph_exec)
-      if (g) {
-        cudaGraphExecDestroy(g);
-        g = nullptr;
-      }
-  }
+      std::memcmp(&old_rt, &h->rt, sizeof(RopeTabs)) != 0)
+    drop_graphs(h);
+  h->td_prev_valid = false;   // kv_mode 1: nothing finished yet to re-run
   // zero lanes, controller state
   const size_t kv = size_t(h->nb) * h->NE * h->S * h->L * h->d * h->ta;
   CK(cudaMemsetAsync(h->Kc, 0, kv, h->stream));
@@ -1365,11 +1490,7 @@ sdv2_status sdv2_set_block_range(sdv2_handle* h, int32_t block_begin, int32_t bl
   h->b1 = block_end;
   h->a0 = block_begin - h->r0;
   h->a1 = block_end - h->r0;
-  for (auto& g : h->graph_exec)   // the captured call bodies loop over the old range
-    if (g) {
-      cudaGraphExecDestroy(g);
-      g = nullptr;
-    }
+  drop_graphs(h);   // the captured call bodies loop over the old range
   return SDV2_OK;
 }
 
@@ -1389,8 +1510,7 @@ sdv2_status sdv2_destroy(sdv2_handle* h) {
     if (h->td_host) cudaEventDestroy(h->td_ev[i]);
   if (h->td_host) cudaFreeHost(h->td_host);
   for (auto e : h->ev_pool) cudaEventDestroy(e);
-  for (auto& g : h->graph_exec)
-    if (g) cudaGraphExecDestroy(g);
+  drop_graphs(h);
   delete h;
   return SDV2_OK;
 }

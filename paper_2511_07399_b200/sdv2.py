@@ -35,7 +35,7 @@ class ModelDescC(ctypes.Structure):
 class GeometryC(ctypes.Structure):
     _fields_ = [("latent_h", ctypes.c_int32), ("latent_w", ctypes.c_int32), ("chunk_frames", ctypes.c_int32),
                 ("steps", ctypes.c_int32), ("sink_chunks", ctypes.c_int32), ("window_chunks", ctypes.c_int32),
-                ("streams", ctypes.c_int32)]
+                ("streams", ctypes.c_int32), ("kv_mode", ctypes.c_int32)]
 
 
 class PipelineC(ctypes.Structure):
@@ -168,7 +168,7 @@ def model_desc_c(md) -> ModelDescC:
 
 def geometry_c(g) -> GeometryC:
     return GeometryC(g.latent_h, g.latent_w, g.chunk_frames, g.steps, g.sink_chunks, g.window_chunks,
-                     getattr(g, "streams", 1))
+                     getattr(g, "streams", 1), getattr(g, "kv_mode", 0))
 
 
 def partition(costs: Sequence[float], stages: int, extra_first=0.0, extra_last=0.0):

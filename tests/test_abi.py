@@ -53,3 +53,22 @@ def test_workspace_sizing_and_validation():
     assert L.sdv2_workspace_bytes(ctypes.byref(md), ctypes.byref(g0), None, SDV2_BF16) == 0
     pp = PipelineC(3, 0, 0, 1)
     assert L.sdv2_workspace_bytes(ctypes.byref(md), ctypes.byref(g), ctypes.byref(pp), SDV2_BF16) == 0
+
+
+def test_clean_rerun_mode_validation():
+    """kv_mode 1 (clean-context re-run) is accepted for n = 1 on one stage, rejected
+    otherwise; any other kv_mode is rejected."""
+    import dataclasses
+    import synthgen as sg
+    from paper_2511_07399_b200.sdv2 import lib, model_desc_c, geometry_c, PipelineC, SDV2_BF16
+    L = lib()
+    cfg = sg.CONFIGS["tiny"]
+    md = model_desc_c(cfg.model)
+    ok = geometry_c(dataclasses.replace(cfg.geom, steps=1, kv_mode=1))
+    assert L.sdv2_workspace_bytes(ctypes.byref(md), ctypes.byref(ok), None, SDV2_BF16) > 0
+    two = geometry_c(dataclasses.replace(cfg.geom, steps=2, kv_mode=1))
+    assert L.sdv2_workspace_bytes(ctypes.byref(md), ctypes.byref(two), None, SDV2_BF16) == 0
+    pp = PipelineC(2, 0, 0, 1)
+    assert L.sdv2_workspace_bytes(ctypes.byref(md), ctypes.byref(ok), ctypes.byref(pp), SDV2_BF16) == 0
+    bad = geometry_c(dataclasses.replace(cfg.geom, kv_mode=2))
+    assert L.sdv2_workspace_bytes(ctypes.byref(md), ctypes.byref(bad), None, SDV2_BF16) == 0
