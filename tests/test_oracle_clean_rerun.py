@@ -57,9 +57,12 @@ def test_clean_rerun_key_is_block0_key_of_x0_at_t0():
     o.set_prompt(prompts[0])
     w = lambda n: W["blocks.0." + n].astype(np.float64)
     lane = o.lanes[(0, 0)]
+    starts = [0, *cfg.prompt_switch]
+    prompt_at = lambda X: prompts[starts.index(X)] if X in starts and X > 0 else None
     recs = [o.step_chunk(0, chunks[0])]
+    assert any(any(r["act"]["refresh"]) for r in run_stream(cfg, W, chunks, prompts))   # a refresh happens
     for Y in range(cfg.num_chunks - 1):
-        recs.append(o.step_chunk(Y + 1, chunks[Y + 1]))        # call Y + 1 re-ran chunk Y
+        recs.append(o.step_chunk(Y + 1, chunks[Y + 1], prompt_at(Y + 1)))   # call Y + 1 re-ran chunk Y
         x = M.patchify(recs[Y]["out"], md) @ W["patch_w"].astype(np.float64).T + W["patch_b"]
         # C.2 at t = 0 (sigma = 0): e0 = W_tp SiLU(W_t2 SiLU(W_t1 sinusoid(0) + b) + b) + b
         emb = np.concatenate([np.ones(md.freq_dim // 2), np.zeros(md.freq_dim // 2)])   # cos 0, sin 0
@@ -95,3 +98,40 @@ def test_clean_rerun_needs_single_step():
     g = dataclasses.replace(base.geom, kv_mode=1)               # n = 2
     with pytest.raises(ValueError):
         StreamOracle(base.model, g, base.stream, sg.gen_weights(base.model, seed=0))
+
+
+def _mut_rerun(kind):
+    """Misreadings of the clean re-run patched into StreamOracle.clean_rerun / LaneCache.overwrite."""
+    from oracle import control as C
+
+    def rerun(self, rec):
+        md, dt, W = self.md, self.dt, self.W
+        act = rec["act"]
+        src = rec["entries"][0]["x_in"] if kind == "noisy_input" else rec["out"]
+        u = M.patchify(src.astype(dt), md)
+        x = M.linear(u, W["patch_w"].astype(dt), W["patch_b"].astype(dt))
+        sig = rec["motion"]["sigmas"][0] if kind == "own_sigma" else np.float32(0.0)
+        _, e0 = M.time_embed(sig, W, md, dt)
+        for b in self.blocks:
+            x = self.block(x, e0, b, self.lanes[(b, 0)], act, rerun=True)
+
+    def overwrite_window_only(self, act, k, v):
+        X = act["X"]
+        if act["sink_fill"] >= 0:
+            e = self.sinks[act["sink_fill"]]
+        else:
+            e = self.window[-1]
+        assert e.tag == X
+        e.k, e.v = k, v
+
+    if kind == "window_only":
+        return [(C.LaneCache, "overwrite", overwrite_window_only)]
+    return [(StreamOracle, "clean_rerun", rerun)]
+
+
+@pytest.mark.parametrize("kind", ["noisy_input", "own_sigma", "window_only"])
+def test_pins_catch_rerun_misreadings(monkeypatch, kind):
+    for obj, attr, rep in _mut_rerun(kind):
+        monkeypatch.setattr(obj, attr, rep)
+    with pytest.raises(AssertionError):
+        test_clean_rerun_key_is_block0_key_of_x0_at_t0()
