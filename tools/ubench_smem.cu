@@ -20,7 +20,11 @@ __global__ void __launch_bounds__(160, 1) ub(const uint8_t* src, long long* out)
   uint32_t* slot = reinterpret_cast<uint32_t*>(bars + 8);
   volatile int* done = reinterpret_cast<volatile int*>(bars + 9);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const bool ts = mode == 2 || mode == 3, copies = mode == 1 || mode == 3 || mode == 4, mma = mode != 4;
+  const bool ts = mode == 2 || mode == 3, copies = mode == 1 || mode == 3 || mode >= 4, mma = mode != 4 && mode < 9;
+  // modes 9 / 10: copies alone, every SM streaming its own data: 9 = a 256 KB region per SM
+  // (37 MB total, L2-resident after the first pass), 10 = a 6.4 MB region per SM (948 MB, HBM)
+  const size_t region = mode == 9 ? (size_t(256) << 10) : mode == 10 ? (size_t(6400) << 10) : 65536;
+  const uint8_t* mysrc = mode >= 9 ? src + region * blockIdx.x : src;
   // modes 5..8: SS variants: D column 0 or 256, accumulate from the second MMA of each
   // iteration (k > 0) or always after the first overall ((it | k) > 0)
   const uint32_t dcol = (mode == 5 || mode == 7) ? 0u : 256u;
@@ -66,7 +70,7 @@ __global__ void __launch_bounds__(160, 1) ub(const uint8_t* src, long long* out)
     __syncwarp();
   } else if (warp == 0 && copies) {
     long long t0 = clock64(), n = 0;
-    const int maxn = mode == 4 ? 4000 : 1 << 30;
+    const int maxn = mode == 4 || mode >= 9 ? 4000 : 1 << 30;
     while (n < maxn && !*done) {
       const int b = int(n & 1);
       if (n >= 2) tc::mbar_wait(bars + b, uint32_t(((n - 2) >> 1) & 1));
@@ -74,7 +78,7 @@ __global__ void __launch_bounds__(160, 1) ub(const uint8_t* src, long long* out)
         tc::mbar_expect_tx(bars + b, 32768);
         asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 32768, [%2];" ::"r"(
                          tc::smem_u32(sD + b * 32768)),
-                     "l"(src + (n & 1) * 32768), "r"(tc::smem_u32(bars + b))
+                     "l"(mysrc + (size_t(n) * 32768) % region), "r"(tc::smem_u32(bars + b))
                      : "memory");
       }
       __syncwarp();
@@ -100,15 +104,16 @@ int main(int argc, char** argv) {
   long long* d;
   uint8_t* src;
   cudaMalloc(&d, sizeof(long long) * 4 * 1024);
-  cudaMalloc(&src, 65536);
-  cudaMemset(src, 0, 65536);
+  const size_t srcb = size_t(6400) << 10;
+  cudaMalloc(&src, srcb * 148);
+  cudaMemset(src, 0, srcb * 148);
   const int smem = 131072 + 1024 + 256;
-  void (*ks[9])(const uint8_t*, long long*) = {ub<0>, ub<1>, ub<2>, ub<3>, ub<4>, ub<5>, ub<6>, ub<7>, ub<8>};
+  void (*ks[11])(const uint8_t*, long long*) = {ub<0>, ub<1>, ub<2>, ub<3>, ub<4>, ub<5>, ub<6>, ub<7>, ub<8>, ub<9>, ub<10>};
   for (auto k : ks) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const char* names[] = {"8 SS MMA alone", "8 SS MMA + bulk copies", "8 TS MMA alone", "8 TS MMA + bulk copies",
                          "bulk copies alone", "SS D@0 acc k>0", "SS D@256 acc k>0", "SS D@0 acc always",
-                         "SS D@256 acc always"};
-  for (int mode = 0; mode < 9; ++mode) {
+                         "SS D@256 acc always", "copies, own 256 KB per SM", "copies, own 6.4 MB per SM"};
+  for (int mode = 0; mode < 11; ++mode) {
     for (int rep = 0; rep < 2; ++rep) ks[mode]<<<grid, 160, smem>>>(src, d);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
@@ -118,7 +123,7 @@ int main(int argc, char** argv) {
     long long h[4];
     cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
     const double mma_cyc = mode == 4 ? 0 : double(h[0]) / kIters;
-    const double copy_bpc = (mode == 1 || mode >= 3) && h[1] > 0 ? double(h[2]) * 32768.0 / double(h[1]) : 0;
+    const double copy_bpc = (mode == 1 || mode == 3 || mode == 4 || mode >= 9) && h[1] > 0 ? double(h[2]) * 32768.0 / double(h[1]) : 0;
     printf("mode %d %-26s MMA %7.1f cycles / 8 MMAs   copies %6.1f B/cycle\n", mode, names[mode], mma_cyc, copy_bpc);
   }
   return 0;
