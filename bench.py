@@ -264,7 +264,13 @@ def run_ours(args, cfg):
     big = md.dim >= 4096
     W = gen_weights_device(md) if big else gen_weights_parallel(md)
     t_gen = time.time() - t0
-    stage = Stage(md, g, W, precision=SDV2_BF16, device=local, l2_persist=args.l2_persist)
+    table = None
+    if args.gemm_table and os.path.exists(args.gemm_table):   # pinned GEMM configurations (e.g. for ncu)
+        table = [tuple(r) for r in json.load(open(args.gemm_table))["configs"]]
+    stage = Stage(md, g, W, precision=SDV2_BF16, device=local, l2_persist=args.l2_persist, gemm_table=table)
+    if args.gemm_table and table is None:   # record this run's tuned configurations
+        with open(args.gemm_table, "w") as f:
+            json.dump({"workload": cfg.name, "fields": "M N K epi MC BN SK XE", "configs": stage.gemm_configs()}, f)
     if big:   # free the fp32 device copies; the oracle baseline regenerates 2 blocks on host
         del W
         torch.cuda.empty_cache()
@@ -504,6 +510,8 @@ def main():
                     help="override n (in-flight denoising steps = Stream Batch size)")
     ap.add_argument("--latency-chunks", type=int, default=1024,
                     help="chunks of the host-clock per-chunk latency phase (0: skip)")
+    ap.add_argument("--gemm-table", default=None,
+                    help="JSON of GEMM configurations: used if the file exists, else written from this run's tuning")
     ap.add_argument("--kv-mode", default="step", choices=["step", "clean"],
                     help="KV cache contents: step-j K/V per lane (R1) or the clean-context re-run (N4, n = 1)")
     ap.add_argument("--streams", type=int, default=1,

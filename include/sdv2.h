@@ -197,7 +197,20 @@ typedef struct {
   int32_t pdl;
   int32_t graphs;
   int32_t l2_persist;
+  /* gemm_table   [NULL] gemm_table_len records of 8 int32 (M, N, K, epi, MC, BN, SK, XE),
+   *                    e.g. from sdv2_gemm_configs of an earlier handle: these shapes take
+   *                    the given configuration and are not timed (a record that is not one
+   *                    of the shape's candidates is ignored).  Makes the tile choice
+   *                    independent of the timing environment (profilers, clock state);
+   *                    the bits never depend on it (see above). */
+  const int32_t* gemm_table;
+  int32_t gemm_table_len;
 } sdv2_exec_options;
+
+/* The projection-GEMM configurations the handle uses (tuned, or from gemm_table): up to
+ * cap records of 8 int32 (M, N, K, epi, MC, BN, SK, XE) into out; *count = records
+ * available (may exceed cap).  SDV2_E_INVALID on NULL arguments. */
+sdv2_status sdv2_gemm_configs(const sdv2_handle* h, int32_t* out, int32_t cap, int32_t* count);
 
 /* Bytes of device workspace a handle needs (0 on invalid descriptors). */
 size_t sdv2_workspace_bytes(const sdv2_model_desc* md, const sdv2_geometry* g,

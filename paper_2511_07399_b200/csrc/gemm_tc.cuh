@@ -48,6 +48,14 @@ __host__ __device__ inline int gemm_stages(int BN, bool res_tma, int BNl) {
   const int st = (kGemmSmem - 1024 - 512 - kGemmEpiVec - xs) / (kGemmSmemA + BNl * kGemmBK * 2);
   return st > kGemmMaxStages ? kGemmMaxStages : st;
 }
+// Residual epilogues (x += g (acc + b), x += acc + b): 1 = the epilogue stages only the
+// update in shared memory and a TMA reduce-add applies it to x at L2 (no x tile fetched
+// into shared memory, no read-modify-write there); 0 = x tile fetched, updated in shared
+// memory, stored back.
+#ifndef SDV2_GEMM_XRED
+#define SDV2_GEMM_XRED 1
+#endif
+constexpr bool kGemmXRed = SDV2_GEMM_XRED != 0;
 constexpr int kResMaxBN = 192;   // residual epilogues: keep >= 3 stages next to the x tile
 
 // Pipeline trace (test hook): event `ev` of k-block / tile index `i` of CTA 0 and 1
@@ -449,7 +457,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
       const bool fixup = !partial && g.kb0 > 0;    // stream-K: add the earlier partials
       const int c_first = fixup ? it.cluster_of((long long)t * kblocks) : cid;
       float* ws_mine = sk.ws + size_t(cid * MC + cr) * kGemmSkSlotFloats;
-      if (kResTMA && !x_late && !partial && leader) {   // fetch the residual tile while the MMAs run
+      if (kResTMA && !kGemmXRed && !x_late && !partial && leader) {   // fetch the residual tile while the MMAs run
         tc::mbar_expect_tx(x_full, uint32_t(BN) * kGemmBM * 4);
         for (int c = 0; c < BN; c += 32)
           tc::tma_load_2d(sX + (c / 32) * (kGemmBM * 128), &tmX, x_full, nb * BN + c, mb * kGemmBM);
@@ -487,14 +495,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
       tc::tc_fence_after();
       const int r = mb * kGemmBM + row;
       const float* gsm = sGate + ((r < M ? r : M - 1) / ep.L > e_lo ? kGemmMaxBN : 0);
-      if (kResTMA && x_late && !partial && leader) {   // last MMA done: the operand ring is free
+      if (kResTMA && !kGemmXRed && x_late && !partial && leader) {   // last MMA done: the operand ring is free
         // (fetching each box earlier, as the last MMAs release the ring stages, measured
         // 1.3 % slower on the step: the x boxes then compete with the last operand loads)
         tc::mbar_expect_tx(x_full, uint32_t(BN) * kGemmBM * 4);
         for (int c = 0; c < BN; c += 32)
           tc::tma_load_2d(sX + (c / 32) * (kGemmBM * 128), &tmX, x_full, nb * BN + c, mb * kGemmBM);
       }
-      if (kResTMA && !partial) tc::mbar_wait(x_full, (nx++) & 1);
+      if (kResTMA && !kGemmXRed && !partial) tc::mbar_wait(x_full, (nx++) & 1);
       const uint32_t tbase = tmem + (uint32_t(q * 32) << 16) + uint32_t(acc * BN);
       auto chunk = [&](const uint32_t(&v0)[32], int c) {
         if (partial) {   // [chunk][j][row][4]: a warp stores 32 rows x 16 B contiguously
@@ -538,8 +546,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
               const uint32_t px = xrow + ((u ^ (row & 7)) << 4);
-              // x += g * (acc + b) on the packed f32x2 pipe
-              const float4 xv = tc::ld_shared_f4(px);
+              // x += g * (acc + b) on the packed f32x2 pipe (reduce-add: only the update is
+              // staged, x stays zero here)
+              const float4 xv = kGemmXRed ? make_float4(0.f, 0.f, 0.f, 0.f) : tc::ld_shared_f4(px);
               const float4 bb = tc::ld_shared_f4(bias4 + u * 16);
               float2 a01 = __fadd2_rn(make_float2(__uint_as_float(v[4 * u]), __uint_as_float(v[4 * u + 1])),
                                       make_float2(bb.x, bb.y));
@@ -602,8 +611,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_tc_kernel(const __grid_c
         tc::fence_proxy_async_smem();   // generic-proxy smem writes -> visible to the TMA store
         asm volatile("bar.sync 2, %0;" ::"n"(kGemmEpiThreads) : "memory");
         if (leader) {
-          for (int c = 0; c < BN; c += 32)
-            tc::tma_store_2d(&tmX, sX + (c / 32) * (kGemmBM * 128), nb * BN + c, mb * kGemmBM);
+          for (int c = 0; c < BN; c += 32) {
+            if (kGemmXRed) tc::tma_reduce_add_2d(&tmX, sX + (c / 32) * (kGemmBM * 128), nb * BN + c, mb * kGemmBM);
+            else tc::tma_store_2d(&tmX, sX + (c / 32) * (kGemmBM * 128), nb * BN + c, mb * kGemmBM);
+          }
           tc::tma_store_commit_wait_read();   // smem reusable for the next tile's load
         }
       }

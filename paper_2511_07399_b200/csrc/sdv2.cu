@@ -168,6 +168,7 @@ struct sdv2_handle {
   bool pdl = true;        // programmatic dependent launch (sdv2_exec_options.pdl): +2 % fps measured
   bool tune = true;       // create-time GEMM tile tuning (sdv2_exec_options.tune_gemms)
   bool l2_persist = true;    // sdv2_exec_options.l2_persist
+  std::vector<int32_t> gemm_table;   // sdv2_exec_options.gemm_table (records of 8)
   int64_t last_switch_call[kMaxEntries];   // call index of stream b's last sdv2_set_prompt (-1: none)
   cudaGraphExec_t graph_exec[2 * (kMaxEntries + 1)] = {};
   int64_t graph_launches[2 * (kMaxEntries + 1)] = {};
@@ -1070,6 +1071,8 @@ sdv2_status sdv2_create(const sdv2_model_desc* md, const sdv2_geometry* g, const
     h->pdl = opts->pdl != 0;
     h->graphs = opts->graphs != 0;
     h->l2_persist = opts->l2_persist != 0;
+    if (opts->gemm_table && opts->gemm_table_len > 0)
+      h->gemm_table.assign(opts->gemm_table, opts->gemm_table + size_t(opts->gemm_table_len) * 8);
   }
   h->ws_bytes = workspace_bytes;
   if (cudaSetDevice(device) != cudaSuccess) {
@@ -1138,6 +1141,17 @@ sdv2_status sdv2_create(const sdv2_model_desc* md, const sdv2_geometry* g, const
   }
   if (h->prec == SDV2_BF16) {
     if (!tc_gemm_plan(h->gplan, &h->err)) return fail(SDV2_E_CUDA);
+    // configurations given by the caller (exec options): valid candidates only
+    for (size_t i = 0; i + 8 <= h->gemm_table.size(); i += 8) {
+      const int32_t* r = h->gemm_table.data() + i;
+      GemmCfg gc{r[4], r[5], r[6]};
+      gc.XE = r[7];
+      for (const GemmCfg& c : tc_gemm_candidates(h->gplan, r[0], r[1], r[3]))
+        if (c.MC == gc.MC && c.BN == gc.BN && c.SK == gc.SK && c.XE == gc.XE) {
+          h->gplan.tuned[gemm_key(r[0], r[1], r[2], r[3])] = gc;
+          break;
+        }
+    }
     if (cudaMemsetAsync(h->attn_flags, 0, kMaxSMs * sizeof(int), h->stream) != cudaSuccess ||
         cudaMemsetAsync(h->sig_zero, 0, kMaxEntries * sizeof(float), h->stream) != cudaSuccess ||
         !attn_plan_init(h->aplan, h->gplan.encode, std::min(h->gplan.num_sms, kMaxSMs), h->attn_flags) ||
@@ -1500,6 +1514,22 @@ sdv2_status sdv2_block_kv(sdv2_handle* h, int32_t block, int32_t which, void** p
   char* base = static_cast<char*>(which ? h->Vc : h->Kc);
   *ptr = base + size_t(block - h->r0) * per_block * h->ta;
   *bytes = per_block * h->ta;
+  return SDV2_OK;
+}
+
+sdv2_status sdv2_gemm_configs(const sdv2_handle* h, int32_t* out, int32_t cap, int32_t* count) {
+  if (!h || !count || (cap > 0 && !out)) return SDV2_E_INVALID;
+  int32_t n = 0;
+  for (const auto& kv : h->gplan.tuned) {
+    int M = 0, N = 0, K = 0, epi = 0;
+    if (sscanf(kv.first.c_str(), "%d:%d:%d:%d", &M, &N, &K, &epi) != 4) continue;
+    if (n < cap) {
+      const int32_t rec[8] = {M, N, K, epi, kv.second.MC, kv.second.BN, kv.second.SK, kv.second.XE};
+      std::memcpy(out + size_t(n) * 8, rec, sizeof(rec));
+    }
+    ++n;
+  }
+  *count = n;
   return SDV2_OK;
 }
 

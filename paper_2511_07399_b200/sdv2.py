@@ -56,7 +56,8 @@ class StreamDescC(ctypes.Structure):
 
 class ExecOptionsC(ctypes.Structure):
     _fields_ = [("tune_gemms", ctypes.c_int32), ("pdl", ctypes.c_int32), ("graphs", ctypes.c_int32),
-                ("l2_persist", ctypes.c_int32)]
+                ("l2_persist", ctypes.c_int32), ("gemm_table", ctypes.POINTER(ctypes.c_int32)),
+                ("gemm_table_len", ctypes.c_int32)]
 
 
 class StageIOC(ctypes.Structure):
@@ -98,6 +99,7 @@ def _declare(lib):
     lib.sdv2_stage_io_buffers.argtypes = [P, ctypes.c_int32, ctypes.POINTER(StageIOC)]
     lib.sdv2_get_tick_info.argtypes = [P, ctypes.POINTER(TickInfoC)]
     lib.sdv2_destroy.argtypes = [P]
+    lib.sdv2_gemm_configs.argtypes = [P, ctypes.POINTER(ctypes.c_int32), ctypes.c_int32, ctypes.POINTER(ctypes.c_int32)]
     lib.sdv2_status_string.restype = ctypes.c_char_p
     lib.sdv2_status_string.argtypes = [ctypes.c_int]
     lib.sdv2_last_error.restype = ctypes.c_char_p
@@ -256,7 +258,8 @@ class Stage:
     """One pipeline stage (or the whole model when pipeline=None) of the hot path."""
 
     def __init__(self, md, geom, weights: Dict[str, np.ndarray], precision=SDV2_BF16, pipeline=None,
-                 device=0, stream=None, tune_gemms=True, pdl=True, graphs=True, l2_persist=True):
+                 device=0, stream=None, tune_gemms=True, pdl=True, graphs=True, l2_persist=True,
+                 gemm_table=None):
         import torch
         self.torch = torch
         self.md, self.geom = md, geom
@@ -298,7 +301,10 @@ class Stage:
             keep.append(a)
         w = WeightsC(ptrs, len(names))
         h = ctypes.c_void_p()
-        self._opts = ExecOptionsC(int(tune_gemms), int(pdl), int(graphs), int(l2_persist))
+        recs = [int(v) for r in (gemm_table or []) for v in r]
+        self._gemm_table = (ctypes.c_int32 * max(len(recs), 1))(*recs)
+        self._opts = ExecOptionsC(int(tune_gemms), int(pdl), int(graphs), int(l2_persist),
+                                  ctypes.cast(self._gemm_table, ctypes.POINTER(ctypes.c_int32)), len(recs) // 8)
         st = self.L.sdv2_create(ctypes.byref(self._mdc), ctypes.byref(self._gc), ppp, precision, ctypes.byref(w),
                                 ctypes.c_void_p(self.workspace.data_ptr()), nbytes + 1024, device,
                                 ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(self._opts), ctypes.byref(h))
@@ -404,6 +410,15 @@ class Stage:
         n = ctypes.c_size_t()
         _check(self.L.sdv2_kv_lane(self.h, local_block, lane, which, ctypes.byref(p), ctypes.byref(n)), self.h)
         return p.value, n.value
+
+    def gemm_configs(self):
+        """[(M, N, K, epi, MC, BN, SK, XE)] the handle's projection GEMMs run with
+        (sdv2_gemm_configs; pass back as Stage(..., gemm_table=...) to pin them)."""
+        cnt = ctypes.c_int32()
+        _check(self.L.sdv2_gemm_configs(self.h, None, 0, ctypes.byref(cnt)), self.h)
+        buf = (ctypes.c_int32 * max(8 * cnt.value, 1))()
+        _check(self.L.sdv2_gemm_configs(self.h, buf, cnt.value, ctypes.byref(cnt)), self.h)
+        return sorted(tuple(buf[8 * i:8 * i + 8]) for i in range(cnt.value))
 
     def close(self):
         if getattr(self, "h", None):

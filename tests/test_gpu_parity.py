@@ -139,3 +139,36 @@ def test_reset_with_new_stream_constants_drops_stale_graphs(prec):
     assert sorted(got) == sorted(fresh)
     for X in fresh:
         assert np.array_equal(got[X], fresh[X]), X
+
+
+@pytest.mark.gpu
+def test_pinned_gemm_table_reproduces_tuned_handle():
+    """sdv2_exec_options.gemm_table: a handle given another handle's tuned configurations
+    (sdv2_gemm_configs) uses exactly those, without timing, and gives the same bits."""
+    import torch
+    from paper_2511_07399_b200.sdv2 import Stage
+    cfg = sg.CONFIGS["tiny"]
+    W, chunks, prompts = tiny_inputs(cfg)
+    outs = []
+    table = None
+    for tune in (True, False):
+        stage = Stage(cfg.model, cfg.geom, W, precision=SDV2_BF16, tune_gemms=tune, gemm_table=table)
+        got = stage.gemm_configs()
+        if table is None:
+            table = got
+            assert len(table) >= 6 and all(len(r) == 8 for r in table)
+        else:
+            assert got == table
+        stage.reset_stream(cfg.stream, prompts[0])
+        out = torch.zeros(chunks[0].shape, dtype=torch.float32, device="cuda")
+        res = {}
+        for c, v in enumerate(chunks[:5]):
+            oc = stage.denoise_chunk(torch.from_numpy(v).cuda().data_ptr(), out.data_ptr())
+            torch.cuda.synchronize()
+            if oc >= 0:
+                res[oc] = out.cpu().numpy().copy()
+        stage.close()
+        outs.append(res)
+    assert sorted(outs[0]) == sorted(outs[1])
+    for X in outs[0]:
+        assert np.array_equal(outs[0][X], outs[1][X]), X
