@@ -1,6 +1,7 @@
 """Tiny stream through the library for compute-sanitizer (memcheck / racecheck /
 synccheck / initcheck): both precisions, graphs off (every launch visible), 10 chunks with
-a prompt switch, a re-base and sink refresh, and the kernel-level GEMM / attention hooks on
+a prompt switch, a re-base and sink refresh, the same with the clean-context re-run (kv_mode 1), and the
+kernel-level GEMM / attention hooks on
 ragged shapes incl. the stream-K attention split.  Exit 0 iff outputs match the oracle.
 
   compute-sanitizer --tool memcheck python tools/sanitize_tiny.py"""
@@ -32,6 +33,17 @@ def main():
             e = rel_l2(outs[X], recs[X]["out"])
             worst = max(worst, e)
             assert e <= tol, (prec, X, e)
+    # clean-context re-run (kv_mode 1, n = 1): the extra pass and its descriptor
+    import dataclasses
+    cc = dataclasses.replace(cfg, geom=dataclasses.replace(cfg.geom, steps=1, kv_mode=1),
+                             stream=dataclasses.replace(cfg.stream, timesteps=sg.SCHEDULES[1]))
+    rc = run_stream(cc, W, chunks[:cc.num_chunks], prompts, dtype=np.float64)
+    for prec, tol in ((SDV2_FP32, 1e-4), (SDV2_BF16, 2e-2)):
+        outs, _, _ = run_gpu(cc, W, chunks[:cc.num_chunks], prompts, prec, tap=False, graphs=False)
+        for X in range(cc.num_chunks):
+            e = rel_l2(outs[X], rc[X]["out"])
+            worst = max(worst, e)
+            assert e <= tol, ("clean", prec, X, e)
     L = lib()
     P = ctypes.c_void_p
     L.sdv2_debug_attention.argtypes = [P, P, P, P] + [ctypes.c_int32] * 4 + [P, P]
