@@ -67,8 +67,11 @@ def test_tc_gemm(M, N, K, epi):
                                         # hybrid schedule: 384 units = one whole-unit round + a split
                                         # of the remaining 236; 148 units (split only)
                                         (4096, 1024, 12, 128), (4736, 256, 4, 128),
-                                        # cross-attention shape at n = 1 (156 units of 4 key tiles)
-                                        (1560, 512, 12, 128)])
+                                        # cross-attention shape at n = 1 (156 units of 4 key tiles: the 8
+                                        # overflow units split into 4 one-tile pieces, merged in-kernel)
+                                        (1560, 512, 12, 128),
+                                        # overflow splits with 3 / 2 / 4 pieces, ragged key tails
+                                        (1920, 384, 10, 128), (1560, 200, 12, 128), (2048, 500, 10, 128)])
 def test_tc_attention(Lq, Lk, H, hd):
     import torch
     L_ = lib()
