@@ -1720,9 +1720,27 @@ extern "C" sdv2_status sdv2_debug_attention(const void* q, const void* K, const 
     xa.scale_log2 = 1.4426950408889634f / sqrtf(float(hd));
     xa.o = o;
     xa.ldo = H * hd;
+    // SDV2_ATTN_TRACE=<file>: CTA wall stamps of the cross kernel to <file>.xcta (test hook)
+    const char* xtrace_path = getenv("SDV2_ATTN_TRACE");
+    static long long* xtrace = nullptr;
+    if (xtrace_path) {
+      if (!xtrace && cudaMalloc(&xtrace, (4096 + 1024 * 8) * sizeof(long long)) != cudaSuccess) return SDV2_E_CUDA;
+      cudaMemsetAsync(xtrace, 0, (4096 + 1024 * 8) * sizeof(long long), s);
+      xa.trace = xtrace;
+    }
     if (!tc_cross_attention(s, ap, q, Lq, K, V, Lk, H * hd, hd, xa, static_cast<const TickDesc*>(scratch), &err)) {
       fprintf(stderr, "sdv2_debug_attention: %s\n", err.c_str());
       return SDV2_E_CUDA;
+    }
+    if (xtrace_path) {
+      std::vector<long long> hx(4096 + 1024 * 8);
+      cudaStreamSynchronize(s);
+      cudaMemcpy(hx.data(), xtrace, hx.size() * sizeof(long long), cudaMemcpyDeviceToHost);
+      if (FILE* f = fopen((std::string(xtrace_path) + ".xcta").c_str(), "w")) {
+        for (int t = 0; t < 1024; ++t)
+          for (int e = 0; e < 8; ++e) fprintf(f, "%lld%c", hx[4096 + t * 8 + e], e == 7 ? '\n' : ',');
+        fclose(f);
+      }
     }
     return SDV2_OK;
   }

@@ -50,7 +50,19 @@ struct XattnArgs {
   const float* rowsq;   // [rows][nparts] partial sums of squares (d / 32 per row)
   int nparts;
   float inv_d, eps;
+  long long* trace;     // test hook only: CTA wall stamps (globaltimer ns) [4096 + cta * 8 + event]
 };
+
+// test hook: 0 entry, 1 set up (after the PDL wait), 2 first Q landed (MMA warp), 3 first
+// S landed (softmax), 4 unit 0's P done, 5 unit 0's epilogue done, 6 last epilogue done, 7 exit
+#define XATTN_STAMP(ev)                                                                     \
+  do {                                                                                      \
+    if (a.trace != nullptr && blockIdx.x < 1024) {                                          \
+      unsigned long long t_;                                                                \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                \
+      a.trace[4096 + blockIdx.x * 8 + (ev)] = (long long)t_;                                \
+    }                                                                                       \
+  } while (0)
 
 // unit u -> (entry, head, query tile): full tiles first, then the ragged last tiles
 __device__ __forceinline__ void xattn_unit(const XattnArgs& a, int u, int& e, int& h, int& qt) {
@@ -96,6 +108,7 @@ __global__ void __launch_bounds__(kXattnThreads, 1) xattn_tc_kernel(const __grid
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = gridDim.x, c = blockIdx.x;
+  if (threadIdx.x == 0) XATTN_STAMP(0);
   const int QF = a.L / kAttnBQ;
   const int units = a.n_entries * a.H * (QF + (a.L % kAttnBQ ? 1 : 0));
   const int J = (a.Lk + kAttnBKV - 1) / kAttnBKV;
@@ -127,6 +140,7 @@ __global__ void __launch_bounds__(kXattnThreads, 1) xattn_tc_kernel(const __grid
   tc::tc_fence_after();
   pdl_wait();      // q is produced upstream; prompt K/V may have been rewritten by a switch
   pdl_trigger();
+  if (threadIdx.x == 0) XATTN_STAMP(1);
   const uint32_t tmem = *tmem_slot;
   const uint32_t tO = tmem + 384u;
   auto tS = [&](int slot) { return tmem + uint32_t(slot) * 128u; };
@@ -173,6 +187,7 @@ __global__ void __launch_bounds__(kXattnThreads, 1) xattn_tc_kernel(const __grid
       const uint32_t ph = ui & 1;
       const int qs = 0;
       tc::mbar_wait(q_full, ui & 1);
+      if (ui == 0 && lane == 0) XATTN_STAMP(2);
       const uint32_t qa = tc::smem_u32(sQ + qs * SM::Q);
       // S_t = Q K_t^T (S_3 into slot 0 once the softmax copied S_0 out)
       for (int t = 0; t < J; ++t, ++kvi) {
@@ -248,6 +263,7 @@ __global__ void __launch_bounds__(kXattnThreads, 1) xattn_tc_kernel(const __grid
       float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
       for (int t = 0; t < J; ++t) {
         tc::mbar_wait(s_full + t, ph);
+        if (ui == 0 && t == 0 && warp == 2 && lane == 0) XATTN_STAMP(3);
         tc::tc_fence_after();
         float sv[HC];
         {
@@ -322,6 +338,7 @@ __global__ void __launch_bounds__(kXattnThreads, 1) xattn_tc_kernel(const __grid
         if (lane == 0) tc::mbar_arrive(p_full + t);
       }
       // ---- epilogue: O / (l_half0 + l_half1) -> bf16
+      if (ui == 0 && warp == 2 && lane == 0) XATTN_STAMP(4);
       xl[half * 128 + row] = l;
       const int tl = J == 4 ? 0 : J - 1;     // last PV issued
       tc::mbar_wait(pv_done + tl, ph);
@@ -350,6 +367,7 @@ __global__ void __launch_bounds__(kXattnThreads, 1) xattn_tc_kernel(const __grid
       tc::tc_fence_before();
       pair_sync();                          // xm / xl reusable by the next unit
       if (lane == 0) tc::mbar_arrive(o_empty);
+      if (warp == 2 && lane == 0) XATTN_STAMP(ui == 0 ? 5 : 6);
     }
   }
   tc::tc_fence_before();
@@ -358,6 +376,7 @@ __global__ void __launch_bounds__(kXattnThreads, 1) xattn_tc_kernel(const __grid
     tc::tc_fence_after();
     tc::tmem_dealloc(tmem, 512);
   }
+  if (threadIdx.x == 0) XATTN_STAMP(7);
 }
 
 inline bool xattn_plan_init() {
