@@ -31,7 +31,9 @@ template <int HD>
 struct XattnSmem {
   static constexpr int Q = kAttnBQ * HD * 2;
   static constexpr int KV = kAttnBKV * HD * 2;
-  static constexpr int total = Q + kXattnKV * KV + 1024 + 512 + 2 * 1024 + 64;
+  static constexpr int O = kAttnBQ * HD * 2;   // bf16 output tile staged for the TMA store
+  // no alignment pad: the __align__(1024) extern block starts 1024-aligned (checked)
+  static constexpr int total = Q + kXattnKV * KV + O + 512 + 2 * 1024 + 64;
 };
 
 struct XattnArgs {
@@ -84,7 +86,8 @@ __device__ __forceinline__ void xattn_unit(const XattnArgs& a, int u, int& e, in
 template <int HD>
 __global__ void __launch_bounds__(kXattnThreads, 1) xattn_tc_kernel(const __grid_constant__ CUtensorMap tmQ,
                                                             const __grid_constant__ CUtensorMap tmK,
-                                                            const __grid_constant__ CUtensorMap tmV, XattnArgs a,
+                                                            const __grid_constant__ CUtensorMap tmV,
+                                                            const __grid_constant__ CUtensorMap tmO, XattnArgs a,
                                                             const TickDesc* __restrict__ td) {
   using SM = XattnSmem<HD>;
   constexpr int NCH = HD / 64;
@@ -92,7 +95,9 @@ __global__ void __launch_bounds__(kXattnThreads, 1) xattn_tc_kernel(const __grid
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;                         // one Q tile (a CTA rarely owns two units)
   uint8_t* sKV = sQ + SM::Q;                  // kXattnKV stages
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sKV + kXattnKV * SM::KV);
+  uint8_t* sO = sKV + kXattnKV * SM::KV;      // [HD / 64 boxes][128 rows][128 B], 128-byte swizzle
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sO + SM::O);
+  if (smem != smem_raw) __trap();             // the budget has no alignment pad
   uint64_t* q_full = bar;                     // [2]
   uint64_t* q_empty = bar + 2;                // [2]
   uint64_t* kv_full = bar + 4;                // [kXattnKV]
@@ -345,24 +350,33 @@ __global__ void __launch_bounds__(kXattnThreads, 1) xattn_tc_kernel(const __grid
       tc::tc_fence_after();
       pair_sync();
       const float inv = 1.f / (l + xl[(half ^ 1) * 128 + row]);
-      const int qr = qt * kAttnBQ + row;
-      bf16* orow = reinterpret_cast<bf16*>(a.o) + size_t(e * a.L + (qr < a.L ? qr : 0)) * a.ldo + h * HD + half * HO;
+      // the row's HO columns -> the staged tile (box = 64 columns x 128 rows, 16-byte
+      // granule g of row r at g ^ (r & 7)); rows >= L are clipped by the 3D map's bounds
 #pragma unroll
       for (int cc = 0; cc < HO / 32; ++cc) {
         uint32_t r0[32];
         tc::tmem_ld32(tO + lane_off + half * HO + cc * 32, r0);
         tc::tmem_ld_wait();
-        if (qr < a.L) {
-          uint32_t pk[16];
+        uint32_t pk[16];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            __nv_bfloat162 b2 = __floats2bfloat162_rn(__uint_as_float(r0[2 * i]) * inv, __uint_as_float(r0[2 * i + 1]) * inv);
-            pk[i] = *reinterpret_cast<uint32_t*>(&b2);
-          }
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-            reinterpret_cast<uint4*>(orow + cc * 32)[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+        for (int i = 0; i < 16; ++i) {
+          __nv_bfloat162 b2 = __floats2bfloat162_rn(__uint_as_float(r0[2 * i]) * inv, __uint_as_float(r0[2 * i + 1]) * inv);
+          pk[i] = *reinterpret_cast<uint32_t*>(&b2);
         }
+        const int c0 = half * HO + cc * 32;                  // first column of the 32
+        const uint32_t box = tc::smem_u32(sO + (c0 >> 6) * (kAttnBQ * 128)) + row * 128;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int g = ((c0 & 63) >> 3) + i;
+          tc::st_shared_v4(box + ((g ^ (row & 7)) << 4), make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]));
+        }
+      }
+      tc::fence_proxy_async_smem();
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      if (warp == 2 && lane == 0) {
+#pragma unroll
+        for (int b = 0; b < HD / 64; ++b) tc::tma_store_3d(&tmO, sO + b * (kAttnBQ * 128), h * HD + b * 64, qt * kAttnBQ, e);
+        tc::tma_store_commit_wait_read();   // staged tile reusable by this CTA's next unit
       }
       tc::tc_fence_before();
       pair_sync();                          // xm / xl reusable by the next unit
@@ -376,7 +390,30 @@ __global__ void __launch_bounds__(kXattnThreads, 1) xattn_tc_kernel(const __grid
     tc::tc_fence_after();
     tc::tmem_dealloc(tmem, 512);
   }
+  if (warp == 2 && lane == 0) tc::tma_store_wait_all();
   if (threadIdx.x == 0) XATTN_STAMP(7);
+}
+
+// 3D bf16 map over the output [entries][L][ld] with (64 x 128 x 1) boxes, 128-byte swizzle:
+// a 128-row tile of entry e ending past row L is clipped at the entry's end.
+inline const CUtensorMap* xattn_out_map(AttnPlan& p, const void* base, int entries, int L, int ld, std::string* err) {
+  const std::string key = "o3:" + std::to_string(reinterpret_cast<uintptr_t>(base)) + ":" + std::to_string(entries) +
+                          ":" + std::to_string(L) + ":" + std::to_string(ld);
+  auto it = p.maps.find(key);
+  if (it != p.maps.end()) return &it->second;
+  CUtensorMap m;
+  const cuuint64_t dims[3] = {cuuint64_t(ld), cuuint64_t(L), cuuint64_t(entries)};
+  const cuuint64_t strides[2] = {cuuint64_t(ld) * 2, cuuint64_t(L) * ld * 2};
+  const cuuint32_t box[3] = {64, cuuint32_t(kAttnBQ), 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = p.encode(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    *err = "xattn output map encode failed (" + std::to_string(int(r)) + ")";
+    return nullptr;
+  }
+  return &(p.maps.emplace(key, m).first->second);
 }
 
 inline bool xattn_plan_init() {
@@ -397,7 +434,8 @@ inline bool tc_cross_attention(cudaStream_t s, AttnPlan& p, const void* q, long 
   const CUtensorMap* mq = attn_map(p, q, q_rows, d, kAttnBQ, err);
   const CUtensorMap* mk = attn_map(p, Kbase, kv_rows, d, kAttnBKV, err);
   const CUtensorMap* mv = attn_map(p, Vbase, kv_rows, d, kAttnBKV, err);
-  if (!mq || !mk || !mv) return false;
+  const CUtensorMap* mo = xattn_out_map(p, a.o, int(q_rows / a.L), a.L, a.ldo, err);
+  if (!mq || !mk || !mv || !mo) return false;
   const int units = a.n_entries * a.H * a.QT;
   const int G = units < p.num_sms ? units : p.num_sms;
   if (G < 1) return true;
@@ -413,10 +451,10 @@ inline bool tc_cross_attention(cudaStream_t s, AttnPlan& p, const void* q, long 
   cudaError_t e;
   if (hd == 128) {
     cfg.dynamicSmemBytes = XattnSmem<128>::total;
-    e = cudaLaunchKernelEx(&cfg, xattn_tc_kernel<128>, *mq, *mk, *mv, a, td);
+    e = cudaLaunchKernelEx(&cfg, xattn_tc_kernel<128>, *mq, *mk, *mv, *mo, a, td);
   } else {
     cfg.dynamicSmemBytes = XattnSmem<64>::total;
-    e = cudaLaunchKernelEx(&cfg, xattn_tc_kernel<64>, *mq, *mk, *mv, a, td);
+    e = cudaLaunchKernelEx(&cfg, xattn_tc_kernel<64>, *mq, *mk, *mv, *mo, a, td);
   }
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
