@@ -476,7 +476,31 @@ __global__ void __launch_bounds__(256) flow_kernel(const float* __restrict__ y, 
 }
 
 // out[e][r] = W[r,:] . act(in[e,:]) + b[r], act = SiLU if pre_silu; the activated input
-// vectors are staged once per CTA in smem; 8 warps x 4 rows per CTA.
+// vectors are staged once per CTA in smem; 8 warps x 4 rows per CTA.  The 4 rows of a warp
+// are walked together with 16-byte weight loads (4 fp32 / 8 bf16 per lane and row), so
+// each lane keeps 4 independent loads in flight; a scalar loop covers Kd % (32 x vec).
+template <typename TW> struct GemvVec;
+template <> struct GemvVec<float> {
+  static constexpr int V = 4;
+  __device__ static void load(const float* p, float (&w)[4]) {
+    const float4 v = __ldg(reinterpret_cast<const float4*>(p));
+    w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
+  }
+};
+template <> struct GemvVec<bf16> {
+  static constexpr int V = 8;
+  __device__ static void load(const bf16* p, float (&w)[8]) {
+    const uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 t = __bfloat1622float2(h[i]);
+      w[2 * i] = t.x;
+      w[2 * i + 1] = t.y;
+    }
+  }
+};
+
 template <typename TW, int NMAX = kMaxEntries>
 __global__ void __launch_bounds__(256) gemv2_kernel(const TW* __restrict__ W, const float* __restrict__ b,
                                                     const float* __restrict__ in, float* __restrict__ out, int n,
@@ -490,24 +514,54 @@ __global__ void __launch_bounds__(256) gemv2_kernel(const TW* __restrict__ W, co
     xs[i] = z;
   }
   __syncthreads();
+  constexpr int V = GemvVec<TW>::V;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int rr = 0; rr < 4; ++rr) {
-    const int r = (blockIdx.x * 8 + warp) * 4 + rr;
-    if (r >= R) break;
-    float acc[NMAX];
+  const int rb = (blockIdx.x * 8 + warp) * 4;
+  if (rb >= R) return;
+  float acc[4][NMAX];
 #pragma unroll
-    for (int e = 0; e < NMAX; ++e) acc[e] = 0.f;
-    const TW* wr = W + size_t(r) * Kd;
-    for (int k = lane; k < Kd; k += 32) {
-      const float wv = to_f(wr[k]);
+  for (int rr = 0; rr < 4; ++rr)
 #pragma unroll
-      for (int e = 0; e < NMAX; ++e)
-        if (e < n) acc[e] += wv * xs[e * Kd + k];
+    for (int e = 0; e < NMAX; ++e) acc[rr][e] = 0.f;
+  const int kvec = (Kd / (32 * V)) * (32 * V);
+  for (int k = lane * V; k < kvec; k += 32 * V) {
+    float w[4][V];
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) {
+      const int r = rb + rr < R ? rb + rr : R - 1;
+      GemvVec<TW>::load(W + size_t(r) * Kd + k, w[rr]);
     }
 #pragma unroll
     for (int e = 0; e < NMAX; ++e) {
       if (e < n) {
-        const float s = warp_sum(acc[e]);
+        float xv[V];
+#pragma unroll
+        for (int j = 0; j < V; ++j) xv[j] = xs[e * Kd + k + j];
+#pragma unroll
+        for (int rr = 0; rr < 4; ++rr)
+#pragma unroll
+          for (int j = 0; j < V; ++j) acc[rr][e] += w[rr][j] * xv[j];
+      }
+    }
+  }
+  for (int k = kvec + lane; k < Kd; k += 32) {
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) {
+      const int r = rb + rr < R ? rb + rr : R - 1;
+      const float wv = to_f(W[size_t(r) * Kd + k]);
+#pragma unroll
+      for (int e = 0; e < NMAX; ++e)
+        if (e < n) acc[rr][e] += wv * xs[e * Kd + k];
+    }
+  }
+#pragma unroll
+  for (int rr = 0; rr < 4; ++rr) {
+    const int r = rb + rr;
+    if (r >= R) break;
+#pragma unroll
+    for (int e = 0; e < NMAX; ++e) {
+      if (e < n) {
+        const float s = warp_sum(acc[rr][e]);
         if (lane == 0) out[size_t(e) * R + r] = s + b[r];
       }
     }
