@@ -338,55 +338,72 @@ __global__ void __launch_bounds__(256) rms_rows2_kernel(TA* __restrict__ y, cons
 }
 
 // ----------------------------------------------------------------------------
-// Motion-aware noise controller, 1 CTA per stream b: per-frame d (fp64
-// accumulation), window max over the last k+1 values, clip, EMA s_X, sigma of every
-// entry of the stream (R5).  chunk / prev / st point at stream 0's; CTHW = chunk stride.
+// Motion-aware noise controller: per-frame d (fp64 accumulation), window
+// max over the last k+1 values, clip, EMA s_X, sigma of every entry of the stream (R5).
+// chunk / prev / st point at stream 0's; CTHW = chunk stride.
 // ----------------------------------------------------------------------------
-__global__ void __launch_bounds__(1024) motion_kernel(const float* __restrict__ chunk_all, float* prev_all,
-                                                      CtrlState* st_all, float* sig, float* sign, const TickDesc* td,
-                                                      StreamCfg cfg, int CHW, int HW, int T, int n_entries) {
+// Grid (kMotionSlices, B): CTA c of stream b owns a contiguous slice of the frame's C HW
+// values; per frame it writes its fp64 partial sum of squared differences and moves its
+// slice of the frame into prev; the last CTA of the stream to finish (arrival counter)
+// sums the partials in slice order (deterministic) and runs the controller update.
+constexpr int kMotionSlices = 32;
+__global__ void __launch_bounds__(256) motion_kernel(const float* __restrict__ chunk_all, float* prev_all,
+                                                     CtrlState* st_all, float* sig, float* sign, const TickDesc* td,
+                                                     StreamCfg cfg, int CHW, int HW, int T, int n_entries,
+                                                     double* part, unsigned* arrive) {
   pdl_wait();
   pdl_trigger();
-  __shared__ double red[32];
+  __shared__ double red[8];
+  __shared__ bool last;
   const int tid = threadIdx.x, nt = blockDim.x;
-  const int b = blockIdx.x;
+  const int b = blockIdx.y, c = blockIdx.x, P = gridDim.x;
   const float* chunk = chunk_all + size_t(b) * CHW;
   const int C = CHW / (HW * T);
+  const int n4 = C * HW / 4;                        // float4 per frame (C HW % 4 == 0)
+  const int i0 = int((long long)n4 * c / P), i1 = int((long long)n4 * (c + 1) / P);
   float* prev = prev_all + size_t(b) * C * HW;
   CtrlState* st = st_all + b;
-  const int X = td->e[b].X;
   for (int f = 0; f < T; ++f) {
     double acc = 0.0;
-    for (int i = tid * 4; i < C * HW; i += nt * 4) {
-      // C*HW is a multiple of 4 (checked at create); frame f of channel c is contiguous
-      const int c = i / HW, p = i % HW;
-      const float4 a = *reinterpret_cast<const float4*>(chunk + (size_t(c) * T + f) * HW + p);
-      const float4 b = *reinterpret_cast<const float4*>(prev + i);
-      const double d0 = double(a.x) - double(b.x), d1 = double(a.y) - double(b.y);
-      const double d2 = double(a.z) - double(b.z), d3 = double(a.w) - double(b.w);
+    for (int q = i0 + tid; q < i1; q += nt) {
+      const int i = q * 4;
+      // frame f of channel c is contiguous
+      const int ch = i / HW, p = i % HW;
+      const float4 a = *reinterpret_cast<const float4*>(chunk + (size_t(ch) * T + f) * HW + p);
+      const float4 v = *reinterpret_cast<const float4*>(prev + i);
+      const double d0 = double(a.x) - double(v.x), d1 = double(a.y) - double(v.y);
+      const double d2 = double(a.z) - double(v.z), d3 = double(a.w) - double(v.w);
       acc += d0 * d0 + d1 * d1 + d2 * d2 + d3 * d3;
+      *reinterpret_cast<float4*>(prev + i) = a;      // this frame is the next one's previous
     }
     acc = warp_sum_d(acc);
     if ((tid & 31) == 0) red[tid >> 5] = acc;
     __syncthreads();
-    if (tid < 32) {
-      double v = tid < (nt >> 5) ? red[tid] : 0.0;
-      v = warp_sum_d(v);
-      if (tid == 0) {
-        const double dd = st->has_prev ? sqrt(v / double(C * HW)) : 0.0;   // d = 0 at frame 0 (Q15)
-        st->ds[st->nd & 63] = dd;
-        st->nd += 1;
-      }
+    if (tid == 0) {
+      double v = 0.0;
+      for (int w = 0; w < (nt >> 5); ++w) v += red[w];
+      part[(size_t(b) * kMaxFrames + f) * kMotionSlices + c] = v;
     }
-    __syncthreads();
-    for (int i = tid * 4; i < C * HW; i += nt * 4) {
-      const int c = i / HW, p = i % HW;
-      *reinterpret_cast<float4*>(prev + i) = *reinterpret_cast<const float4*>(chunk + (size_t(c) * T + f) * HW + p);
-    }
-    if (tid == 0) st->has_prev = 1;
     __syncthreads();
   }
   if (tid == 0) {
+    __threadfence();
+    last = atomicAdd(arrive + b, 1u) == unsigned(P - 1);
+  }
+  __syncthreads();
+  if (!last || tid != 0) return;
+  __threadfence();
+  arrive[b] = 0u;   // re-armed for the next call
+  const int X = td->e[b].X;
+  for (int f = 0; f < T; ++f) {
+    double v = 0.0;
+    for (int k = 0; k < P; ++k) v += __ldcg(part + (size_t(b) * kMaxFrames + f) * kMotionSlices + k);
+    const double dd = st->has_prev ? sqrt(v / double(C * HW)) : 0.0;   // d = 0 at frame 0 (Q15)
+    st->ds[st->nd & 63] = dd;
+    st->nd += 1;
+    st->has_prev = 1;
+  }
+  {
     double mx = 0.0;
     const long long lo = st->nd - (cfg.k + 1) > 0 ? st->nd - (cfg.k + 1) : 0;
     for (long long i = lo; i < st->nd; ++i) mx = fmax(mx, st->ds[i & 63]);

@@ -143,6 +143,8 @@ struct sdv2_handle {
   bool td_prev_valid = false;
   TickDesc* td_clean_dev = nullptr;
   float* sig_zero = nullptr;
+  double* motion_part = nullptr;      // [B][kMaxFrames][kMotionSlices] motion partial sums
+  unsigned* motion_arrive = nullptr;  // [B] CTA arrival counters (zero between calls)
   cudaGraphExec_t clean_graph_exec[kMaxEntries + 1] = {};
   int64_t clean_graph_launches[kMaxEntries + 1] = {};
   cudaEvent_t td_ev[kTdRing];
@@ -329,6 +331,8 @@ size_t carve(sdv2_handle* h, void* base) {
   h->rope = cv.take<float>(rope_elems);
   h->td_dev = cv.take<TickDesc>(1);
   h->td_clean_dev = cv.take<TickDesc>(1);
+  h->motion_part = cv.take<double>(size_t(h->B) * kMaxFrames * kMotionSlices);
+  h->motion_arrive = cv.take<unsigned>(h->B);
   h->sig_zero = cv.take<float>(kMaxEntries);
   return cv.off + 1024;
 }
@@ -780,8 +784,8 @@ sdv2_status tick_body(sdv2_handle* h, int na, int par) {
   if (first) {
     ProfScope ps(h, 5, 0.0);
     // motion-aware noise controller then the step-0 blend on all SMs
-    launch_k(h->pdl, motion_kernel, dim3(h->B), dim3(1024), 0, h->stream, h->lat_in, h->prev_frame, h->ctrl, h->st.sig, h->st.sign, h->td_dev,
-             h->scfg, h->CTHW, h->hh * h->ww, h->T, h->NE);
+    launch_k(h->pdl, motion_kernel, dim3(kMotionSlices, h->B), dim3(256), 0, h->stream, h->lat_in, h->prev_frame, h->ctrl, h->st.sig, h->st.sign, h->td_dev,
+             h->scfg, h->CTHW, h->hh * h->ww, h->T, h->NE, h->motion_part, h->motion_arrive);
     CKL();
     launch_k(h->pdl, blend_kernel, dim3((h->CTHW + 255) / 256, h->B), dim3(256), 0, h->stream, h->lat_in, h->st.lat, h->st.sig, h->td_dev,
              h->scfg.seed, h->CTHW);
@@ -1135,6 +1139,12 @@ sdv2_status sdv2_create(const sdv2_model_desc* md, const sdv2_geometry* g, const
   }
   for (int b = 0; b < h->nb; ++b)   // g_ck * g_cq for the fused cross-q RMS
     mul_vec_kernel<<<(d + 255) / 256, 256, 0, h->stream>>>(h->bw[b].gck, h->bw[b].gcq, h->bw[b].gkq, d);
+  // both precisions: sigma = 0 of the clean pass, the motion kernel's arrival counters
+  if (cudaMemsetAsync(h->sig_zero, 0, kMaxEntries * sizeof(float), h->stream) != cudaSuccess ||
+      cudaMemsetAsync(h->motion_arrive, 0, h->B * sizeof(unsigned), h->stream) != cudaSuccess) {
+    h->err = "workspace initialisation failed";
+    return fail(SDV2_E_CUDA);
+  }
   if (cudaStreamSynchronize(h->stream) != cudaSuccess) {
     h->err = cudaGetErrorString(cudaGetLastError());
     return fail(SDV2_E_CUDA);
@@ -1153,7 +1163,6 @@ sdv2_status sdv2_create(const sdv2_model_desc* md, const sdv2_geometry* g, const
         }
     }
     if (cudaMemsetAsync(h->attn_flags, 0, kMaxSMs * sizeof(int), h->stream) != cudaSuccess ||
-        cudaMemsetAsync(h->sig_zero, 0, kMaxEntries * sizeof(float), h->stream) != cudaSuccess ||
         !attn_plan_init(h->aplan, h->gplan.encode, std::min(h->gplan.num_sms, kMaxSMs), h->attn_flags) ||
         !xattn_plan_init()) {
       h->err = "attention plan initialisation failed";
