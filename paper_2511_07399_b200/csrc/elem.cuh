@@ -174,8 +174,6 @@ __global__ void __launch_bounds__(256) qkv_post2_kernel(const TA* __restrict__ q
                                                         const float* __restrict__ gq, const float* __restrict__ gk,
                                                         const TickDesc* __restrict__ td, RopeTabs R, int rows, int d,
                                                         int hd, int L, int hn, int wn, int T, int S, float eps) {
-  pdl_wait();
-  pdl_trigger();
   using U = Unit<TA>;
   constexpr int UN = U::N;
   __shared__ float red[2][2 * (kRowThreads / 32)];
@@ -200,15 +198,14 @@ __global__ void __launch_bounds__(256) qkv_post2_kernel(const TA* __restrict__ q
   float cs[kP][UN / 2], sn[kP][UN / 2];
   float sq = 0.f, sk = 0.f;
   const int half = hd / 2;
+  // the gains, the tick descriptor's positions and the RoPE tables are not produced by
+  // the upstream kernel: their loads (a dependent chain) run before the PDL wait
+  if constexpr (kPre) {
 #pragma unroll
-  for (int i = 0; i < kMaxU; ++i) {
-    const int u = i * kRowThreads + t;
-    if (u < units && ok) {
-      const int c0 = u * UN;
-      U::load(qr + c0, q[i]);
-      U::load(kr + c0, k[i]);
-      U::load(vr + c0, vv[i]);
-      if constexpr (kPre) {
+    for (int i = 0; i < kMaxU; ++i) {
+      const int u = i * kRowThreads + t;
+      if (u < units && ok) {
+        const int c0 = u * UN;
 #pragma unroll
         for (int j = 0; j < UN; j += 4) {
           const float4 a4 = __ldg(reinterpret_cast<const float4*>(gq + c0 + j));
@@ -219,6 +216,18 @@ __global__ void __launch_bounds__(256) qkv_post2_kernel(const TA* __restrict__ q
 #pragma unroll
         for (int j = 0; j < UN; j += 2) rope_cs(R, ((c0 + j) >> 1) % half, pt, ph, pw, cs[i][j / 2], sn[i][j / 2]);
       }
+    }
+  }
+  pdl_wait();
+  pdl_trigger();
+#pragma unroll
+  for (int i = 0; i < kMaxU; ++i) {
+    const int u = i * kRowThreads + t;
+    if (u < units && ok) {
+      const int c0 = u * UN;
+      U::load(qr + c0, q[i]);
+      U::load(kr + c0, k[i]);
+      U::load(vr + c0, vv[i]);
     }
   }
 #pragma unroll
