@@ -5,6 +5,8 @@
 // float (fp32 parity path) or bf16 (tensor-core path); the residual stream x,
 // latents, sigma and time embeddings are fp32 on both paths (reading R8/Q29).
 #pragma once
+#include <type_traits>
+
 #include "common.cuh"
 #include "ctl.h"
 
@@ -242,13 +244,25 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const TIn* __restrict__ 
     }
     __syncthreads();
   }
+  const int c4 = n0 + tx * 4;
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < 4; ++i) {
+    const int r = m0 + ty * 4 + i;
+    if (r >= M) continue;
+    if constexpr (EPI == EPI_STORE && std::is_same<TOut, float>::value) {
+      if ((ep.ldo & 3) == 0 && c4 + 3 < N) {   // a 16-byte store per row and thread
+        const float4 b = *reinterpret_cast<const float4*>(ep.bias + c4);
+        *reinterpret_cast<float4*>(static_cast<float*>(ep.out) + size_t(r) * ep.ldo + c4) =
+            make_float4(acc[i][0] + b.x, acc[i][1] + b.y, acc[i][2] + b.z, acc[i][3] + b.w);
+        continue;
+      }
+    }
 #pragma unroll
     for (int jj = 0; jj < 4; ++jj) {
-      const int r = m0 + ty * 4 + i, c = n0 + tx * 4 + jj;
-      if (r < M && c < N) epi_store<TOut, EPI>(ep, r, c, N, acc[i][jj]);
+      const int c = c4 + jj;
+      if (c < N) epi_store<TOut, EPI>(ep, r, c, N, acc[i][jj]);
     }
+  }
 }
 
 // ----------------------------------------------------------------------------
