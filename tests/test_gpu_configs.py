@@ -306,3 +306,29 @@ def test_visual_sink_embedding(prec):
     stage.close()
     for X in range(cfg.num_chunks):
         assert rel_l2(got[X], recs[X]["out"]) <= TOL[prec], X
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("prec", [SDV2_FP32, SDV2_BF16])
+def test_batched_streams_equal_one_at_a_time(prec):
+    """SURVEY P6, first half, measured directly: 3 streams batched per call vs each stream
+    alone in its own handle (same Philox key, latents, prompts).  fp32 path: every kernel is
+    row / entry independent, so bit for bit.  bf16 path: the GEMMs are row independent (every
+    tuner candidate reduces in the same order) but the self-attention's stream-K split points
+    depend on the whole call's work, so the outputs agree to the split-merge rounding
+    (rel-L2 <= 2e-3, 10x below the oracle tolerance)."""
+    from gpu_harness import multi_inputs, run_gpu_streams
+    cfg = sg.CONFIGS["tiny"]
+    B, switches = 3, [(6,), (3,), ()]
+    W, chunks, prompts = multi_inputs(cfg, B, 10, switches)
+    batched, _, _ = run_gpu_streams(cfg, W, chunks, prompts, switches, prec, tap=False)
+    for b in range(B):
+        cb = dataclasses.replace(cfg, prompt_switch=tuple(switches[b]), num_chunks=len(chunks[b]))
+        sd = dataclasses.replace(cfg.stream, seed=cfg.stream.seed + (b << 32))
+        alone, _, _ = run_gpu(cb, W, chunks[b], prompts[b], prec, tap=False, stream_desc=sd)
+        assert sorted(alone) == sorted(batched[b]) and alone
+        for X in alone:
+            if prec == SDV2_FP32:
+                assert np.array_equal(alone[X], batched[b][X]), (b, X)
+            else:
+                assert rel_l2(batched[b][X], alone[X]) <= 2e-3, (b, X, rel_l2(batched[b][X], alone[X]))
