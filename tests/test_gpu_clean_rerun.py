@@ -90,3 +90,22 @@ def test_clean_rerun_full_width_bf16():
     outs, taps, meta = run_gpu(cfg, W, ch, prompts, SDV2_BF16)
     worst = _check(cfg, recs, outs, taps, meta, 2e-2)
     print(f"clean re-run 1.3B 480p: worst block rel-L2 {worst:.3e}")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("prec", [SDV2_FP32, SDV2_BF16])
+def test_clean_rerun_multi_stream(prec):
+    """kv_mode 1 with B = 2 streams batched per call (each with its own prompts and switch):
+    the clean pass re-runs both streams' previous chunks; each stream equals its own oracle."""
+    from gpu_harness import multi_inputs, run_gpu_streams, stream_oracles
+    cfg = _clean(sg.CONFIGS["tiny"])
+    switches = [(4,), ()]
+    W, chunks, prompts = multi_inputs(cfg, 2, 8, switches)
+    recs = stream_oracles(cfg, W, chunks, prompts, switches)
+    outs, _, meta = run_gpu_streams(cfg, W, chunks, prompts, switches, prec, tap=False)
+    for b in range(2):
+        assert len(outs[b]) == 8
+        for X, o in outs[b].items():
+            assert rel_l2(o, recs[b][X]["out"]) <= TOL[prec], (b, X)
+        for (X, j), (slots, _, _) in meta[b].items():
+            assert slots == {s: (t, p[0]) for s, (t, p) in recs[b][X]["lane_state"][(0, j)].items()}, (b, X)
